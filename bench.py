@@ -1,0 +1,378 @@
+"""bench.py -- GB/s of text matched on B200 (SFA run + composition), % of roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference] [--all]
+
+A step is one pass of the whole hot path (Alg. 5 of PAPER.md:552-576: byte ->
+column, chunk runs from f_I, composition f_1 . ... . f_p, finalisation) over
+one text of the workload, through the C-ABI (``sfa_match_async``), with the
+text already resident in HBM.  Default workload: BASELINE.json configs[1]
+(config 2: ``([0-4]{5}[5-9]{5})*`` over a 268,435,450-byte accepted text).
+The text (256 MiB) is larger than the 126 MB L2, so no flush is needed between
+steps.  ``--all`` adds per-config numbers for configs 1, 3, 4 and 5.
+
+Multi-GPU (torchrun): every rank matches its own copy of the workload (the
+texts are independent problems; no data-path collective), weak scaling;
+value = all ranks' bytes / the max over ranks of the device time.
+
+``--impl reference``: there is no reference implementation (the paper ships
+no code); the reference arm is the CPU oracle (Alg. 2, sequential DFA run,
+oracle/) timed on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GB/s of text matched on 1 B200 (SFA run + composition); % of roofline"
+UNIT = "GB/s"
+CONFIG_NAMES = {
+    1: "cfg1: (ab|ba)*c over {a,b,c}, 1 MiB accepted text",
+    2: "cfg2: ([0-4]{5}[5-9]{5})* over digits, 268,435,450-byte accepted text",
+    3: "cfg3: .*(w1|...|w32).* over all bytes, 1 GiB scrubbed a-z text, one planted word",
+    4: "cfg4: .*a[ab]{8} over {a,b}, 1 GiB i.i.d. text",
+    5: "cfg5: cfg3's DFA, batch of 65,536 x 64 KiB texts (4 GiB), 10% planted",
+}
+
+
+def workload(cfg: int):
+    """(regex, alphabet, text or (texts, offsets)) of a BASELINE.json config."""
+    import workloads as W
+    if cfg == 1:
+        return W.REGEX[1], W.ALPHABET[1], W.cfg1_accepted()
+    if cfg == 2:
+        return W.REGEX[2], W.ALPHABET[2], W.cfg2_accepted()
+    if cfg == 3:
+        return W.cfg3_regex(), None, W.cfg3_text(plant=True)
+    if cfg == 4:
+        return W.REGEX[4], W.ALPHABET[4], W.cfg4_text()
+    if cfg == 5:
+        t, off, _ = W.cfg5_batch()
+        return W.cfg3_regex(), None, (t, off)
+    raise ValueError(cfg)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons, sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def ncu_traffic(cfg: int):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"cfg{cfg}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args, world, rank):
+    """CPU oracle (Alg. 2) on the host cores: the reference arm of this tier."""
+    if rank != 0:
+        return
+    import oracle as O
+    cfg = args.config
+    rx, alpha, text = workload(cfg)
+    d = O.OracleDFA(rx, alpha)
+    sample = text[: min(text.size, args.ref_bytes)]
+    for _ in range(args.warmup):
+        d.run(sample[: 1 << 20])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        d.run(sample)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    gbs = sample.size * len(times) / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded, DESIGN.md input recipe)",
+        "config": {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(sample.size)},
+        "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {sample.size} bytes of the config-{cfg} text per step, "
+                                   f"Alg. 2 byte-at-a-time (oracle/oracle.c)"},
+        "e2e": {"value": gbs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, rx, alpha, text, budget_s):
+    import oracle as O
+    d = O.OracleDFA(rx, alpha)
+    sample = text[: min(text.size, 64 << 20)]
+    d.run(sample[: 1 << 20])
+    done, t0 = 0, time.perf_counter()
+    passes = 0
+    while True:
+        d.run(sample)
+        done += sample.size
+        passes += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    el = time.perf_counter() - t0
+    return {"value": done / el / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{passes} passes over the first {sample.size} bytes of the config-{cfg} text "
+                      f"({el:.1f} s), Alg. 2 byte-at-a-time, single thread"}
+
+
+def time_single(torch, P, sfa, dtext, stream, steps, warmup, res):
+    for _ in range(warmup):
+        sfa.match_async(dtext, res, stream)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        sfa.match_async(dtext, res, stream)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps  # ms
+
+
+def time_batch(torch, P, sfa, dtexts, doff, count, stream, steps, warmup, res):
+    for _ in range(warmup):
+        sfa.match_batch(dtexts, doff, count, res, stream)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        sfa.match_batch(dtexts, doff, count, res, stream)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def extra_config(torch, P, cfg, stream, steps, warmup, peak):
+    rx, alpha, text = workload(cfg)
+    sfa = P.SFA(rx, alpha)
+    if cfg == 5:
+        texts, off = text
+        dt = torch.from_numpy(texts).cuda()
+        do = torch.from_numpy(off.astype(np.int64)).cuda()
+        count = off.size - 1
+        res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
+        ms = time_batch(torch, P, sfa, dt, do, count, stream, steps, warmup, res)
+        nbytes = texts.size
+    else:
+        dt = torch.from_numpy(text).cuda()
+        res = torch.zeros(2, dtype=torch.int32, device="cuda")
+        ms = time_single(torch, P, sfa, dt, stream, steps, warmup, res)
+        nbytes = text.size
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    info = sfa.info()
+    return {"workload": CONFIG_NAMES[cfg], "value": gbs, "unit": UNIT, "ms_per_step": ms, "bytes": int(nbytes),
+            "roofline_frac": gbs / peak, "residency": P.RES_NAMES.get(info["residency"], "?"),
+            "sfa_states": info["sfa_states"], "dfa_states": info["dfa_states"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--all", action="store_true", help="also time configs 1, 3, 4, 5")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-bytes", type=int, default=64 << 20)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import paper_1405_0562_b200 as P
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_kind, peaks = load_peaks()
+
+    cfg = args.config
+    rx, alpha, text = workload(cfg)
+    sfa = P.SFA(rx, alpha)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        dtext = torch.from_numpy(text).cuda()
+        res = torch.zeros(2, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    # parity of the timed configuration (exact; the oracle is not called here)
+    q, acc = sfa.match(dtext, stream)
+    expected = {1: (3, True), 2: (0, True)}.get(cfg)
+    if expected is not None and (q, acc) != expected:
+        raise SystemExit(f"wrong result {(q, acc)} != {expected}")
+
+    for _ in range(args.warmup):
+        sfa.match_async(dtext, res, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)  # let the sampler start
+        e0.record(stream)
+        for _ in range(args.steps):
+            sfa.match_async(dtext, res, stream)
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    per_rank_gbs = text.size / (ms_per_step * 1e-3) / 1e9
+    value = world * per_rank_gbs
+
+    # end to end: host (pinned) -> device copies inside the timed region, result read back
+    pinned = torch.from_numpy(text).pin_memory()
+    sfa.match_host(pinned, stream)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.e2e_steps):
+        got = sfa.match_host(pinned, stream)
+    t1.record(stream)
+    t1.synchronize()
+    e2e_ms = t0.elapsed_time(t1) / args.e2e_steps
+    if expected is not None and got != expected:
+        raise SystemExit(f"wrong e2e result {got}")
+    e2e_val = world * text.size / (e2e_ms * 1e-3) / 1e9
+
+    extras = {}
+    if args.all and rank == 0:
+        for c in (1, 3, 4, 5):
+            if c != cfg:
+                steps = 200 if c != 5 else 20
+                extras[f"cfg{c}"] = extra_config(torch, P, c, stream, steps, args.warmup, peak)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    clocks = clk.summary()
+    info = sfa.info()
+    sm_hz = (clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    smem_peak = nsm * 32 * sm_hz / 1e9       # GB/s of text at one conflict-free LDS wavefront per byte
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded, DESIGN.md input recipe)",
+        "config": {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(text.size),
+                   "l2": "input 256 MiB-4 GiB > 126 MB L2: no flush needed" if text.size > (126 << 20)
+                   else "input smaller than L2 (L2-warm)",
+                   "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
+                   "dfa_states": info["dfa_states"], "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": per_rank_gbs / peak, "traffic": ncu_traffic(cfg),
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "kernel": "k_scan_tma (one launch per step; achieved = text bytes / launch time)",
+                     "smem_lookup_peak_gbs": smem_peak,
+                     "frac_of_min_roofline": per_rank_gbs / min(peak, smem_peak)},
+        "clocks": clocks,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(text.size), "d2h_bytes_per_step": 8,
+                "api": "sfa_match_host (pinned host text, 64 MiB slices copied and matched in a pipeline)"},
+        "gpu_launches": args.steps,
+    }
+    if extras:
+        line["per_config"] = extras
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, rx, alpha, text, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * sfa.h -- C-ABI of the B200-native SFA matcher (arXiv 1405.0562).
+ *
+ * The library (paper_1405_0562_b200/_lib/libsfa.so) runs the data-parallel hot
+ * path of Alg. 5 of the paper ("Parallel computation of
+ * SFA") on one NVIDIA B200 (sm_100a):
+ *
+ *   A1  byte -> table column                 (implementation; the paper indexes
+ *                                             a 256-wide table)
+ *   A2  chunk run from f_I, one lookup/byte  (Alg. 5 lines 1-5, PAPER.md:560-565,
+ *                                             "looks up the transition table once
+ *                                             for each character")
+ *   A3  f_fin = f_1 . ... . f_p              (line 6; '.' is reverse
+ *                                             composition f.g := g o f, PAPER.md:149,
+ *                                             associative)
+ *   A4  q_final = f_fin(q0), accept          (line 7; F_s)
+ *   A5  batches of independent texts        ("naive" parallelism)
+ *   A6  table residency (smem / L2)          (cache-miss cost)
+ *
+ * Any division of the text gives the same result (Theorem 3),
+ * so results are bit-exact against the sequential DFA run (Alg. 2,
+ * PAPER.md:259-272) of the canonical minimal complete DFA (C2/C3).
+ *
+ * Conventions
+ *   - All functions return an sfa_status (0 = SFA_OK) except sfa_free and
+ *     sfa_last_error.  No exception crosses the ABI.  On error a message is
+ *     available from sfa_last_error() (thread-local, valid until the next call
+ *     on the same thread).
+ *   - "d_" pointers are CUDA device pointers on the handle's device; "h_"
+ *     pointers and the plain output pointers are host memory.
+ *   - stream is a cudaStream_t (0 = legacy default stream).
+ *   - The handle owns its host tables, device tables and reusable device
+ *     scratch.  The caller owns texts, offsets, results and streams.
+ *   - A handle is immutable after sfa_compile except for sfa_set_residency.
+ *     Matches on one handle may be issued from any host thread and stream:
+ *     the library orders them on the device (a per-handle event makes each
+ *     launch wait for the previous one's use of the shared scratch).
+ */
+#ifndef SFA_H
+#define SFA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SFA_API __attribute__((visibility("default")))
+#else
+#define SFA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sfa_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    SFA_OK = 0,
+    SFA_ERR_SYNTAX = 1,        /* malformed regex; message has the byte position      */
+    SFA_ERR_UNSUPPORTED = 2,   /* back-references, look-around, anchors */
+    SFA_ERR_CAPACITY = 3,      /* NFA/DFA/SFA over the caps; |S| > 65535 (uint16 ids)  */
+    SFA_ERR_INVALID_ARG = 4,   /* NULL handle/output, d_text NULL with n > 0, ...      */
+    SFA_ERR_CUDA = 5,          /* a CUDA runtime/driver call failed                    */
+    SFA_ERR_OOM = 6            /* host or device allocation failed                    */
+} sfa_status;
+
+/* Table residency (A6).  AUTO picks the fastest mode that fits. */
+typedef enum {
+    SFA_RES_AUTO = 0,
+    SFA_RES_SMEM_PRIVATE = 1,  /* bank-private per-lane copies in shared memory     */
+    SFA_RES_SMEM_SHARED = 2,   /* one copy of the class-compressed table in smem     */
+    SFA_RES_HOT_L2 = 3,        /* frequent rows in smem, the rest from L2            */
+    SFA_RES_L2 = 4             /* whole table from global memory (L2-resident)       */
+} sfa_residency;
+
+typedef struct sfa_handle sfa_handle;
+
+/* One result per text: the DFA state q_final (canonical id, C3) and
+ * accept = [q_final in F_d] (0/1).  8 bytes. */
+typedef struct {
+    uint32_t final_state;
+    uint32_t accept;
+} sfa_result;
+
+typedef struct {
+    uint32_t nfa_positions;    /* Glushkov positions (McNaughton-Yamada) */
+    uint32_t dfa_subset_states;/* Alg. 1 output before minimisation              */
+    uint32_t dfa_states;       /* complete minimal |D| (dead state counted)      */
+    uint32_t dfa_live;         /* |D| without the dead state                     */
+    uint32_t dead_state;       /* canonical id of the dead state, UINT32_MAX if none */
+    uint32_t sfa_states;       /* |S| by Alg. 4 (constant-dead mapping counted)  */
+    uint32_t classes;          /* byte classes C (table columns)                 */
+    uint32_t sfa_depth;        /* longest shortest word f_I -> f (replay bound)  */
+    uint32_t residency;        /* effective sfa_residency for single texts       */
+    uint32_t compose_mode;     /* 0 = vector (|D| <= 32), 1 = replay (Lemma 1)   */
+    uint32_t range_lo, range_width; /* byte window of the PRIVATE layout (0 if n/a) */
+    uint64_t device_table_bytes;    /* bytes of SFA tables held on the device    */
+    double   dfa_seconds, sfa_seconds; /* host construction times (not the target) */
+} sfa_info_t;
+
+/*
+ * sfa_compile -- regex -> Glushkov NFA -> Alg. 1 subset construction
+ * -> minimisation -> canonical numbering ->
+ * Alg. 4 correspondence construction in its DFA form ->
+ * byte classes, device tables (uploaded to the current CUDA device).
+ *
+ *   regex        NUL-terminated pattern, grammar of DESIGN.md C10; full-match.
+ *   alphabet     bytes of Sigma; NULL = all 256 bytes (C2).
+ *   alphabet_len number of bytes at `alphabet`; ignored when alphabet is NULL.
+ *   max_sfa      cap on |S| (0 = default 65535, the uint16 id limit).
+ *   out          receives the handle; *out = NULL on error.
+ * Errors: SYNTAX, UNSUPPORTED, CAPACITY, INVALID_ARG, CUDA, OOM.
+ */
+SFA_API int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len,
+                uint32_t max_sfa, sfa_handle** out);
+
+/* Releases the handle and its device memory (synchronises the device work
+ * that used it).  NULL is a no-op. */
+SFA_API void sfa_free(sfa_handle* h);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+SFA_API const char* sfa_last_error(void);
+
+SFA_API int sfa_info(const sfa_handle* h, sfa_info_t* info);
+
+/*
+ * sfa_match -- one text in device memory (Alg. 5 with the device tree
+ * reduction).  Blocking: returns after the result is on the host (it
+ * synchronises `stream`).  n == 0 returns (q0 = 0, [eps in L]) with no launch.
+ *   d_text       device pointer to n bytes (any alignment), caller-owned.
+ *   final_state  host out: q_final.   accept: host out, 0/1.
+ */
+SFA_API int sfa_match(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_stream_t stream,
+              uint32_t* final_state, int* accept);
+
+/* Same work as sfa_match, stream-ordered and non-blocking: the result is
+ * written to device memory d_result (8 bytes, caller-owned) when the stream
+ * reaches it.  Suitable for CUDA-event timing and graph capture. */
+SFA_API int sfa_match_async(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_stream_t stream,
+                    sfa_result* d_result);
+
+/*
+ * sfa_match_batch -- count independent texts, text i = d_texts[d_offsets[i] :
+ * d_offsets[i+1]).  d_offsets (count+1 uint64, device) must be non-decreasing
+ * (not checked on the host: it is device memory; a decreasing pair yields an
+ * empty text).  Writes d_results[i] (device, count entries).  Async,
+ * stream-ordered.  count == 0 is a no-op; an empty text gives (0, [eps in L]).
+ */
+SFA_API int sfa_match_batch(const sfa_handle* h, const uint8_t* d_texts, const uint64_t* d_offsets,
+                    size_t count, sfa_stream_t stream, sfa_result* d_results);
+
+/*
+ * sfa_match_host -- end-to-end call on a HOST buffer (pinned or pageable):
+ * the text is copied to the device in slices on `stream` while earlier slices
+ * are matched (each slice yields one SFA state; slices compose by Lemma 1,
+ * PAPER.md:441), then the result is read back.  Blocking.
+ */
+SFA_API int sfa_match_host(const sfa_handle* h, const uint8_t* h_text, size_t n, sfa_stream_t stream,
+                   uint32_t* final_state, int* accept);
+
+/*
+ * Test / diagnostic knobs.
+ *
+ * sfa_match_chunked -- divides the text into exactly `nchunks` chunks by
+ * SPEC's rule (floor(n/p) bytes, the remainder to the leading chunks; if
+ * n < p, n one-byte chunks; C6), runs each from f_I on the device,
+ * reduces on the device, and optionally returns the per-chunk SFA states
+ * (canonical ids, host array of min(nchunks, max(n,1)) entries).  Blocking.
+ */
+SFA_API int sfa_match_chunked(const sfa_handle* h, const uint8_t* d_text, size_t n, uint32_t nchunks,
+                      sfa_stream_t stream, uint32_t* final_state, int* accept, uint32_t* h_chunk_states);
+
+/* Forces a residency mode (SFA_RES_*); CAPACITY if it does not fit. */
+SFA_API int sfa_set_residency(sfa_handle* h, int mode);
+
+/* Minimal DFA over all 256 bytes: table |D|*256 canonical ids, finals |D| (0/1). */
+SFA_API int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals);
+
+/* D-SFA: table |S|*256 canonical SFA ids, maps |S|*|D| (row s = f_s),
+ * finals |S| (s in F_s).  Any pointer may be NULL. */
+SFA_API int sfa_export_sfa(const sfa_handle* h, uint32_t* table, uint32_t* maps, uint8_t* finals);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFA_H */

@@ -1,0 +1,258 @@
+"""B200-native SFA matcher (arXiv 1405.0562, "Simultaneous Finite Automata").
+
+Thin ctypes binding over the C-ABI of ``include/sfa.h``
+(``paper_1405_0562_b200/_lib/libsfa.so``).  Argument marshalling only: every
+step of the hot path (byte -> column, chunk run, composition, finalisation)
+runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+library is missing or a call fails, an exception is raised.
+
+Device buffers are passed as ``torch`` tensors (``uint8`` / ``int64``
+/ ``uint64`` on a CUDA device) or raw integer device pointers; streams as
+``torch.cuda.Stream`` or raw ``cudaStream_t`` integers.  PyTorch is used only
+for device memory and streams.
+
+Functions keep the C names: ``sfa_compile``, ``sfa_match``,
+``sfa_match_async``, ``sfa_match_batch``, ``sfa_match_host``,
+``sfa_match_chunked``, ``sfa_set_residency``, ``sfa_info``,
+``sfa_export_dfa``, ``sfa_export_sfa``, ``sfa_free``; ``SFA`` wraps a handle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libsfa.so")
+
+SFA_OK, SFA_ERR_SYNTAX, SFA_ERR_UNSUPPORTED, SFA_ERR_CAPACITY, SFA_ERR_INVALID_ARG, SFA_ERR_CUDA, SFA_ERR_OOM = range(7)
+RES_AUTO, RES_SMEM_PRIVATE, RES_SMEM_SHARED, RES_HOT_L2, RES_L2 = range(5)
+RES_NAMES = {0: "auto", 1: "smem_private", 2: "smem_shared", 3: "hot_l2", 4: "l2"}
+_ERR_NAMES = {1: "syntax", 2: "unsupported", 3: "capacity", 4: "invalid argument", 5: "cuda", 6: "out of memory"}
+
+
+class SFAError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class sfa_result(C.Structure):
+    _fields_ = [("final_state", C.c_uint32), ("accept", C.c_uint32)]
+
+
+class sfa_info_t(C.Structure):
+    _fields_ = [
+        ("nfa_positions", C.c_uint32), ("dfa_subset_states", C.c_uint32), ("dfa_states", C.c_uint32),
+        ("dfa_live", C.c_uint32), ("dead_state", C.c_uint32), ("sfa_states", C.c_uint32),
+        ("classes", C.c_uint32), ("sfa_depth", C.c_uint32), ("residency", C.c_uint32),
+        ("compose_mode", C.c_uint32), ("range_lo", C.c_uint32), ("range_width", C.c_uint32),
+        ("device_table_bytes", C.c_uint64), ("dfa_seconds", C.c_double), ("sfa_seconds", C.c_double),
+    ]
+
+
+EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
+           "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_export_dfa",
+           "sfa_export_sfa")
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libsfa.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; run __graft_entry__.build() or python -m paper_1405_0562_b200._build")
+        L = C.CDLL(LIB_PATH)
+        vp, u8p, u32p, u64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+        L.sfa_compile.argtypes = [C.c_char_p, u8p, C.c_int, C.c_uint32, C.POINTER(vp)]
+        L.sfa_free.argtypes = [vp]
+        L.sfa_free.restype = None
+        L.sfa_last_error.restype = C.c_char_p
+        L.sfa_info.argtypes = [vp, C.POINTER(sfa_info_t)]
+        L.sfa_match.argtypes = [vp, vp, C.c_size_t, vp, u32p, C.POINTER(C.c_int)]
+        L.sfa_match_async.argtypes = [vp, vp, C.c_size_t, vp, vp]
+        L.sfa_match_batch.argtypes = [vp, vp, vp, C.c_size_t, vp, vp]
+        L.sfa_match_host.argtypes = [vp, vp, C.c_size_t, vp, u32p, C.POINTER(C.c_int)]
+        L.sfa_match_chunked.argtypes = [vp, vp, C.c_size_t, C.c_uint32, vp, u32p, C.POINTER(C.c_int), u32p]
+        L.sfa_set_residency.argtypes = [vp, C.c_int]
+        L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
+        L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
+        for f in EXPORTS:
+            if f not in ("sfa_free", "sfa_last_error"):
+                getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != SFA_OK:
+        raise SFAError(rc, lib().sfa_last_error().decode(errors="replace"))
+
+
+def _dptr(x) -> int:
+    """Device pointer of a CUDA tensor (or an int passed through)."""
+    if isinstance(x, int):
+        return x
+    if not x.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not x.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return x.data_ptr()
+
+
+def _stream(s) -> int:
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _nbytes(x) -> int:
+    return x.numel() * x.element_size()
+
+
+# --------------------------------------------------------------------------- C names
+def sfa_compile(regex, alphabet=None, max_sfa: int = 0) -> int:
+    """regex (str/bytes), alphabet (bytes or None = all 256 bytes) -> handle (int)."""
+    rx = regex.encode("latin-1") if isinstance(regex, str) else bytes(regex)
+    if b"\0" in rx:
+        raise SFAError(SFA_ERR_INVALID_ARG, "regex contains NUL")
+    h = C.c_void_p()
+    if alphabet is None:
+        rc = lib().sfa_compile(rx, None, 0, max_sfa, C.byref(h))
+    else:
+        al = np.frombuffer(bytes(alphabet), np.uint8).copy()
+        rc = lib().sfa_compile(rx, al.ctypes.data_as(C.POINTER(C.c_uint8)), al.size, max_sfa, C.byref(h))
+    _check(rc)
+    return h.value
+
+
+def sfa_free(h: int):
+    lib().sfa_free(h)
+
+
+def sfa_info(h: int) -> dict:
+    info = sfa_info_t()
+    _check(lib().sfa_info(h, C.byref(info)))
+    return {k: getattr(info, k) for k, _ in sfa_info_t._fields_}
+
+
+def sfa_match(h: int, d_text, n: int | None = None, stream=None):
+    """Blocking: -> (final_state, accept)."""
+    n = _nbytes(d_text) if n is None else n
+    q, a = C.c_uint32(), C.c_int()
+    _check(lib().sfa_match(h, _dptr(d_text) if n else None, n, _stream(stream), C.byref(q), C.byref(a)))
+    return q.value, bool(a.value)
+
+
+def sfa_match_async(h: int, d_text, d_result, n: int | None = None, stream=None):
+    """Stream-ordered: writes (final_state, accept) as 2 x uint32 at d_result (device)."""
+    n = _nbytes(d_text) if n is None else n
+    _check(lib().sfa_match_async(h, _dptr(d_text) if n else None, n, _stream(stream), _dptr(d_result)))
+
+
+def sfa_match_batch(h: int, d_texts, d_offsets, count: int, d_results, stream=None):
+    """Stream-ordered: d_results (device, count x 2 uint32) per text."""
+    if count == 0:
+        return
+    _check(lib().sfa_match_batch(h, _dptr(d_texts), _dptr(d_offsets), count, _stream(stream), _dptr(d_results)))
+
+
+def sfa_match_host(h: int, h_text, stream=None):
+    """End to end from host memory (numpy array or pinned CPU tensor): -> (final_state, accept)."""
+    if isinstance(h_text, np.ndarray):
+        ptr, n = h_text.ctypes.data, h_text.nbytes
+    else:
+        ptr, n = h_text.data_ptr(), _nbytes(h_text)
+    q, a = C.c_uint32(), C.c_int()
+    _check(lib().sfa_match_host(h, ptr if n else None, n, _stream(stream), C.byref(q), C.byref(a)))
+    return q.value, bool(a.value)
+
+
+def sfa_match_chunked(h: int, d_text, nchunks: int, n: int | None = None, stream=None, want_states: bool = True):
+    """Forced SPEC chunking (test knob): -> (final_state, accept, chunk_states or None)."""
+    n = _nbytes(d_text) if n is None else n
+    q, a = C.c_uint32(), C.c_int()
+    cnt = min(nchunks, max(n, 1))
+    states = np.zeros(cnt, np.uint32) if want_states else None
+    sp = states.ctypes.data_as(C.POINTER(C.c_uint32)) if want_states else None
+    _check(lib().sfa_match_chunked(h, _dptr(d_text) if n else None, n, nchunks, _stream(stream),
+                                   C.byref(q), C.byref(a), sp))
+    return q.value, bool(a.value), states
+
+
+def sfa_set_residency(h: int, mode: int):
+    _check(lib().sfa_set_residency(h, mode))
+
+
+def sfa_export_dfa(h: int):
+    info = sfa_info(h)
+    nd = info["dfa_states"]
+    table = np.zeros((nd, 256), np.uint32)
+    finals = np.zeros(nd, np.uint8)
+    _check(lib().sfa_export_dfa(h, table.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                finals.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return table, finals
+
+
+def sfa_export_sfa(h: int):
+    info = sfa_info(h)
+    ns, nd = info["sfa_states"], info["dfa_states"]
+    table = np.zeros((ns, 256), np.uint32)
+    maps = np.zeros((ns, nd), np.uint32)
+    finals = np.zeros(ns, np.uint8)
+    _check(lib().sfa_export_sfa(h, table.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                maps.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                finals.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return table, maps, finals
+
+
+# --------------------------------------------------------------------------- handle object
+class SFA:
+    """Owns one compiled handle: ``SFA(regex, alphabet)``."""
+
+    def __init__(self, regex, alphabet=None, max_sfa: int = 0):
+        self.h = sfa_compile(regex, alphabet, max_sfa)
+
+    def close(self):
+        if getattr(self, "h", None):
+            sfa_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        return sfa_info(self.h)
+
+    def match(self, d_text, stream=None):
+        return sfa_match(self.h, d_text, None, stream)
+
+    def match_async(self, d_text, d_result, stream=None):
+        return sfa_match_async(self.h, d_text, d_result, None, stream)
+
+    def match_batch(self, d_texts, d_offsets, count, d_results, stream=None):
+        return sfa_match_batch(self.h, d_texts, d_offsets, count, d_results, stream)
+
+    def match_host(self, h_text, stream=None):
+        return sfa_match_host(self.h, h_text, stream)
+
+    def match_chunked(self, d_text, nchunks, stream=None, want_states=True):
+        return sfa_match_chunked(self.h, d_text, nchunks, None, stream, want_states)
+
+    def set_residency(self, mode: int):
+        sfa_set_residency(self.h, mode)
+
+    def export_dfa(self):
+        return sfa_export_dfa(self.h)
+
+    def export_sfa(self):
+        return sfa_export_sfa(self.h)

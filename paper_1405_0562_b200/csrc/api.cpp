@@ -1,0 +1,572 @@
+// api.cpp -- the C-ABI of include/sfa.h: handle lifecycle, table residency
+// (A6), launch planning and the host<->device crossings.  All arithmetic of
+// the hot path runs in kernels.cu; this file only plans and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sfa.h"
+#include "compile.hpp"
+#include "kernels.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? SFA_ERR_OOM : SFA_ERR_CUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CU(call)                                                 \
+    do {                                                         \
+        cudaError_t e_ = (call);                                 \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);      \
+    } while (0)
+
+constexpr uint64_t kTmaMin = 4ull << 20;       // below: k_scan_direct
+constexpr uint64_t kDirectPiece = 64;          // bytes per thread in k_scan_direct
+constexpr uint32_t kMaxSlots = (1u << 16) + 2; // partial slots (CTAs + tail)
+constexpr uint64_t kSlice = 64ull << 20;       // sfa_match_host slice
+constexpr uint64_t kBatchSeg = 64ull << 10;    // bytes per batch task
+
+template <class T>
+cudaError_t upload(T** dst, const T* src, size_t count) {
+    *dst = nullptr;
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), count * sizeof(T));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+}  // namespace
+
+struct sfa_handle {
+    sfa::Automata A;
+    // byte window of the range tables (DevTables::lo / W)
+    uint32_t lo = 0, W = 1, other = 0;
+    int forced = SFA_RES_AUTO;
+
+    std::mutex mu;
+    bool uploaded = false;
+    int device = -1, sm_count = 0;
+    size_t smem_optin = 0;
+    // device tables
+    uint16_t* dT = nullptr;
+    uint8_t* dcls = nullptr;
+    uint16_t* dTrange = nullptr;
+    uint8_t* dmaps32 = nullptr;
+    uint16_t* dmaps16 = nullptr;
+    uint32_t* dimg0 = nullptr;
+    uint8_t* dfinal = nullptr;
+    uint32_t* drep_off = nullptr;
+    uint8_t* drep = nullptr;
+    uint64_t dev_bytes = 0;
+    // scratch
+    uint8_t* partials = nullptr;
+    uint32_t* ticket = nullptr;
+    sfa_result* dres = nullptr;       // 2 results (single-text matches and the slice ring)
+    sfa_result* hres = nullptr;       // pinned
+    uint32_t* task_off = nullptr;     // batch plan
+    uint32_t* work = nullptr;
+    uint8_t* seg_parts = nullptr;
+    size_t task_cap = 0, seg_cap = 0;
+    uint8_t* stage[2] = {nullptr, nullptr};   // sfa_match_host staging
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done = nullptr;    // orders uses of the shared scratch across streams
+
+    ~sfa_handle() {
+        if (!uploaded) return;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        cudaDeviceSynchronize();
+        for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
+                        (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
+                        (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1]})
+            if (p) cudaFree(p);
+        if (hres) cudaFreeHost(hres);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
+            if (ev_used[i]) cudaEventDestroy(ev_used[i]);
+        }
+        if (ev_done) cudaEventDestroy(ev_done);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        cudaSetDevice(prev);
+    }
+
+    bool vec() const { return A.nD <= 32; }
+
+    sfa::DevTables tables() const {
+        sfa::DevTables t;
+        t.T = dT;
+        t.cls = dcls;
+        t.Trange = dTrange;
+        t.maps32 = dmaps32;
+        t.maps16 = dmaps16;
+        t.img0 = dimg0;
+        t.dfinal = dfinal;
+        t.rep_off = drep_off;
+        t.rep = drep;
+        t.nS = A.nS;
+        t.C = A.C;
+        t.nD = A.nD;
+        t.lo = lo;
+        t.W = W;
+        return t;
+    }
+
+    // Lazy upload: sfa_compile works without a GPU (host tests); the first
+    // device call uploads to the then-current device.
+    int ensure_uploaded() {
+        if (uploaded) return SFA_OK;
+        CU(cudaGetDevice(&device));
+        int v = 0;
+        CU(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+        sm_count = v;
+        CU(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        smem_optin = static_cast<size_t>(v);
+        uploaded = true;  // from here on the destructor frees what was allocated
+
+        const uint32_t nS = A.nS, C = A.C, nD = A.nD;
+        std::vector<uint16_t> T16(static_cast<size_t>(nS) * C), R16(static_cast<size_t>(nS) * W);
+        for (size_t i = 0; i < T16.size(); ++i) T16[i] = static_cast<uint16_t>(A.T[i]);
+        for (uint32_t s = 0; s < nS; ++s) {
+            for (uint32_t j = 0; j + 1 < W; ++j) R16[static_cast<size_t>(s) * W + j] = T16[static_cast<size_t>(s) * C + A.cls[lo + j]];
+            R16[static_cast<size_t>(s) * W + W - 1] = T16[static_cast<size_t>(s) * C + other];
+        }
+        CU(upload(&dT, T16.data(), T16.size()));
+        CU(upload(&dTrange, R16.data(), R16.size()));
+        CU(upload(&dcls, A.cls, 256));
+        if (vec()) {
+            std::vector<uint8_t> m32(static_cast<size_t>(nS) * 32);
+            for (uint32_t s = 0; s < nS; ++s)
+                for (uint32_t q = 0; q < 32; ++q)
+                    m32[static_cast<size_t>(s) * 32 + q] = static_cast<uint8_t>(q < nD ? A.maps[static_cast<size_t>(s) * nD + q] : q);
+            CU(upload(&dmaps32, m32.data(), m32.size()));
+        }
+        if (nD <= 65535 && static_cast<uint64_t>(nS) * nD * 2 <= (1ull << 30)) {
+            std::vector<uint16_t> m16(static_cast<size_t>(nS) * nD);
+            for (size_t i = 0; i < m16.size(); ++i) m16[i] = static_cast<uint16_t>(A.maps[i]);
+            CU(upload(&dmaps16, m16.data(), m16.size()));
+            dev_bytes += m16.size() * 2;
+        }
+        CU(upload(&dimg0, A.img0.data(), A.img0.size()));
+        CU(upload(&dfinal, A.dfa_final.data(), A.dfa_final.size()));
+        CU(upload(&drep_off, A.rep_off.data(), A.rep_off.size()));
+        if (!A.rep.empty()) CU(upload(&drep, A.rep.data(), A.rep.size()));
+        dev_bytes += T16.size() * 2 + R16.size() * 2 + 256 + (vec() ? static_cast<uint64_t>(nS) * 32 : 0) +
+                     A.img0.size() * 4 + A.dfa_final.size() + A.rep_off.size() * 4 + A.rep.size();
+
+        CU(cudaMalloc(&partials, static_cast<size_t>(kMaxSlots) * 32));
+        CU(cudaMalloc(&ticket, sizeof(uint32_t)));
+        CU(cudaMemset(ticket, 0, sizeof(uint32_t)));
+        CU(cudaMalloc(&dres, 2 * sizeof(sfa_result)));
+        CU(cudaMalloc(&work, sizeof(uint32_t)));
+        CU(cudaMallocHost(&hres, 2 * sizeof(sfa_result)));
+        CU(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+        return SFA_OK;
+    }
+
+    // does `mode` fit for this launch kind?
+    bool fits(sfa::Res mode, int kind /*0 tma, 1 direct, 2 batch*/) const {
+        const sfa::DevTables t = tables();
+        size_t need = kind == 0 ? sfa::tma_smem_bytes(mode, t) : kind == 1 ? sfa::direct_smem_bytes(mode, t)
+                                                                           : sfa::table_smem_bytes(mode, t);
+        if (mode == sfa::Res::Global) return need <= smem_optin;
+        if (mode == sfa::Res::Private && (static_cast<uint64_t>(A.nS) * W * 128 > (1ull << 31))) return false;
+        return need <= smem_optin;
+    }
+    int resolve(int kind, sfa::Res* out) const {
+        if (forced != SFA_RES_AUTO) {
+            sfa::Res m = forced == SFA_RES_HOT_L2 ? sfa::Res::Global : static_cast<sfa::Res>(forced);
+            if (!fits(m, kind)) return fail(SFA_ERR_CAPACITY, "forced residency does not fit in shared memory");
+            *out = m;
+            return SFA_OK;
+        }
+        for (sfa::Res m : {sfa::Res::Private, sfa::Res::Shared, sfa::Res::Global})
+            if (fits(m, kind)) {
+                *out = m;
+                return SFA_OK;
+            }
+        return fail(SFA_ERR_CAPACITY, "no residency mode fits");
+    }
+
+    sfa::Scratch scratch() const {
+        sfa::Scratch s;
+        s.partials = partials;
+        s.ticket = ticket;
+        s.max_ctas = kMaxSlots - 2;
+        return s;
+    }
+
+    // One text on the device -> result (device), stream-ordered.
+    int launch_one(const uint8_t* d_text, uint64_t n, cudaStream_t stream, const uint32_t* q_in, sfa_result* d_result,
+                   uint64_t force_pieces = 0, uint32_t* piece_ids = nullptr) {
+        const bool direct = force_pieces > 0 || n < kTmaMin;
+        sfa::Res mode;
+        int rc = resolve(direct ? 1 : 0, &mode);
+        if (rc) return rc;
+        cudaError_t e;
+        if (direct) {
+            sfa::DirectArgs a;
+            a.t = tables();
+            a.text = d_text;
+            a.n = n;
+            a.npieces = force_pieces ? force_pieces : std::max<uint64_t>(1, (n + kDirectPiece - 1) / kDirectPiece);
+            a.sc = scratch();
+            a.q_in = q_in;
+            a.result = d_result;
+            a.piece_ids = piece_ids;
+            const uint64_t ctas = (a.npieces + sfa::direct_threads_per_cta() - 1) / sfa::direct_threads_per_cta();
+            if (ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "too many chunks");
+            e = sfa::launch_scan_direct(mode, vec(), a, stream);
+        } else {
+            sfa::ScanArgs a;
+            a.t = tables();
+            a.text = d_text;
+            a.n = n;
+            a.sc = scratch();
+            a.q_in = q_in;
+            a.result = d_result;
+            const uint64_t R = sfa::tma_rows_per_cta();
+            uint64_t head = (16 - (reinterpret_cast<uintptr_t>(d_text) & 15)) & 15;
+            head = std::min<uint64_t>(head, n);
+            const uint64_t body16 = (n - head) & ~uint64_t(15);
+            const uint64_t rtot = R * static_cast<uint64_t>(sm_count);
+            uint64_t L = 16 * ((body16 + 16 * rtot - 1) / (16 * rtot));
+            if (L == 0) L = 16;
+            const uint64_t rows = body16 / L;
+            a.plan.head = head;
+            a.plan.L = L;
+            a.plan.nchunks = static_cast<uint32_t>(rows);
+            a.plan.ctas = static_cast<uint32_t>((rows + R - 1) / R);
+            a.plan.tail_start = head + rows * L;
+            if (rows == 0 || a.plan.ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "bad scan plan");
+            e = sfa::launch_scan_tma(mode, vec(), a, stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+        return SFA_OK;
+    }
+
+    // serialise the shared scratch across streams
+    int begin(cudaStream_t stream) {
+        int rc = ensure_uploaded();
+        if (rc) return rc;
+        CU(cudaStreamWaitEvent(stream, ev_done, 0));
+        return SFA_OK;
+    }
+    int end(cudaStream_t stream) {
+        CU(cudaEventRecord(ev_done, stream));
+        return SFA_OK;
+    }
+};
+
+extern "C" {
+
+const char* sfa_last_error(void) { return g_err.c_str(); }
+
+int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa, sfa_handle** out) {
+    if (!out) return fail(SFA_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!regex) return fail(SFA_ERR_INVALID_ARG, "regex is NULL");
+    if (alphabet && alphabet_len < 0) return fail(SFA_ERR_INVALID_ARG, "alphabet_len < 0");
+    sfa_handle* h = new (std::nothrow) sfa_handle;
+    if (!h) return fail(SFA_ERR_OOM, "host allocation failed");
+    try {
+        h->A = sfa::compile_regex(regex, alphabet, alphabet ? alphabet_len : -1, max_sfa);
+    } catch (const sfa::CompileError& e) {
+        delete h;
+        return fail(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        delete h;
+        return fail(SFA_ERR_OOM, "host allocation failed during compile");
+    }
+    // Byte window: the smallest [lo, hi] such that every byte outside it has
+    // one class ("other"); table columns are lo..hi, then W-1 = other.  With
+    // cand = 0 the window never contains byte 0, with cand = 255 never byte
+    // 255, so W <= 256.
+    const uint8_t* cls = h->A.cls;
+    h->W = 257;
+    for (int cand : {0, 255}) {
+        const uint8_t o = cls[cand];
+        int lo = -1, hi = -1;
+        for (int b = 0; b < 256; ++b)
+            if (cls[b] != o) {
+                if (lo < 0) lo = b;
+                hi = b;
+            }
+        const uint32_t W = lo < 0 ? 1u : static_cast<uint32_t>(hi - lo + 2);
+        if (W < h->W) {
+            h->W = W;
+            h->lo = lo < 0 ? 0u : static_cast<uint32_t>(lo);
+            h->other = o;
+        }
+    }
+    *out = h;
+    return SFA_OK;
+}
+
+void sfa_free(sfa_handle* h) { delete h; }
+
+int sfa_info(const sfa_handle* h, sfa_info_t* info) {
+    if (!h || !info) return fail(SFA_ERR_INVALID_ARG, "NULL argument");
+    std::memset(info, 0, sizeof(*info));
+    const auto& A = h->A;
+    info->nfa_positions = A.nfa_positions;
+    info->dfa_subset_states = A.subset_states;
+    info->dfa_states = A.nD;
+    info->dfa_live = A.dead >= 0 ? A.nD - 1 : A.nD;
+    info->dead_state = A.dead >= 0 ? static_cast<uint32_t>(A.dead) : UINT32_MAX;
+    info->sfa_states = A.nS;
+    info->classes = A.C;
+    info->sfa_depth = A.depth;
+    info->compose_mode = h->vec() ? 0 : 1;
+    info->range_lo = h->lo;
+    info->range_width = h->W;
+    info->residency = 0;
+    if (h->uploaded) {
+        sfa::Res m;
+        if (h->resolve(0, &m) == SFA_OK) info->residency = static_cast<uint32_t>(m);
+    }
+    info->device_table_bytes = h->dev_bytes;
+    info->dfa_seconds = A.dfa_seconds;
+    info->sfa_seconds = A.sfa_seconds;
+    return SFA_OK;
+}
+
+int sfa_set_residency(sfa_handle* h, int mode) {
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (mode < SFA_RES_AUTO || mode > SFA_RES_L2) return fail(SFA_ERR_INVALID_ARG, "bad residency mode");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (mode == SFA_RES_AUTO) {
+        h->forced = mode;
+        return SFA_OK;
+    }
+    int rc = h->ensure_uploaded();
+    if (rc) return rc;
+    const int prev = h->forced;
+    h->forced = mode;
+    sfa::Res m;
+    rc = h->resolve(1, &m);
+    if (rc) h->forced = prev;
+    return rc;
+}
+
+int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals) {
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (table) std::memcpy(table, h->A.dfa.data(), h->A.dfa.size() * sizeof(uint32_t));
+    if (finals) std::memcpy(finals, h->A.dfa_final.data(), h->A.dfa_final.size());
+    return SFA_OK;
+}
+
+int sfa_export_sfa(const sfa_handle* h, uint32_t* table, uint32_t* maps, uint8_t* finals) {
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    const auto& A = h->A;
+    if (table)
+        for (uint32_t s = 0; s < A.nS; ++s)
+            for (int b = 0; b < 256; ++b) table[static_cast<size_t>(s) * 256 + b] = A.T[static_cast<size_t>(s) * A.C + A.cls[b]];
+    if (maps) std::memcpy(maps, A.maps.data(), A.maps.size() * sizeof(uint32_t));
+    if (finals) std::memcpy(finals, A.acc.data(), A.acc.size());
+    return SFA_OK;
+}
+
+int sfa_match_async(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_stream_t stream, sfa_result* d_result) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !d_result) return fail(SFA_ERR_INVALID_ARG, "NULL handle or result");
+    if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    if (n == 0) {
+        sfa_result r{0, h->A.dfa_final[0]};
+        h->hres[1] = r;
+        CU(cudaMemcpyAsync(d_result, &h->hres[1], sizeof(r), cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));  // hres[1] is reused
+        return h->end(s);
+    }
+    rc = h->launch_one(d_text, n, s, nullptr, d_result);
+    if (rc) return rc;
+    return h->end(s);
+}
+
+int sfa_match(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_stream_t stream, uint32_t* final_state,
+              int* accept) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !final_state || !accept) return fail(SFA_ERR_INVALID_ARG, "NULL argument");
+    if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    if (n == 0) {  // (q0, [eps in L]) without a launch
+        *final_state = 0;
+        *accept = h->A.dfa_final[0];
+        return SFA_OK;
+    }
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    rc = h->launch_one(d_text, n, s, nullptr, h->dres);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(h->hres, h->dres, sizeof(sfa_result), cudaMemcpyDeviceToHost, s));
+    rc = h->end(s);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(s));
+    *final_state = h->hres[0].final_state;
+    *accept = static_cast<int>(h->hres[0].accept);
+    return SFA_OK;
+}
+
+int sfa_match_chunked(const sfa_handle* hc, const uint8_t* d_text, size_t n, uint32_t nchunks, sfa_stream_t stream,
+                      uint32_t* final_state, int* accept, uint32_t* h_chunk_states) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !final_state || !accept || nchunks == 0) return fail(SFA_ERR_INVALID_ARG, "bad argument");
+    if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    if (n == 0) {
+        *final_state = 0;
+        *accept = h->A.dfa_final[0];
+        if (h_chunk_states) h_chunk_states[0] = 0;
+        return SFA_OK;
+    }
+    const uint64_t p = std::min<uint64_t>(nchunks, n);  // n < p: n one-byte chunks (C6)
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    uint32_t* dids = nullptr;
+    if (h_chunk_states) CU(cudaMallocAsync(&dids, p * sizeof(uint32_t), s));
+    rc = h->launch_one(d_text, n, s, nullptr, h->dres, p, dids);
+    if (rc) {
+        if (dids) cudaFreeAsync(dids, s);
+        return rc;
+    }
+    CU(cudaMemcpyAsync(h->hres, h->dres, sizeof(sfa_result), cudaMemcpyDeviceToHost, s));
+    if (dids) {
+        CU(cudaMemcpyAsync(h_chunk_states, dids, p * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaFreeAsync(dids, s));
+    }
+    rc = h->end(s);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(s));
+    *final_state = h->hres[0].final_state;
+    *accept = static_cast<int>(h->hres[0].accept);
+    return SFA_OK;
+}
+
+int sfa_match_batch(const sfa_handle* hc, const uint8_t* d_texts, const uint64_t* d_offsets, size_t count,
+                    sfa_stream_t stream, sfa_result* d_results) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (count == 0) return SFA_OK;
+    if (!d_offsets || !d_results) return fail(SFA_ERR_INVALID_ARG, "NULL offsets or results");
+    if (count > (1ull << 30)) return fail(SFA_ERR_INVALID_ARG, "count too large");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    sfa::Res mode;
+    rc = h->resolve(2, &mode);
+    if (rc) return rc;
+    if (h->task_cap < count + 1) {
+        if (h->task_off) CU(cudaFree(h->task_off));
+        h->task_off = nullptr;
+        h->task_cap = 0;
+        CU(cudaMalloc(&h->task_off, (count + 1) * sizeof(uint32_t)));
+        h->task_cap = count + 1;
+    }
+    // segments: at most (total bytes / seg) + count tasks; size the parts buffer
+    // lazily for the worst case of this count with one task per text plus the
+    // multi-segment texts (bounded by 2^32 tasks).
+    uint64_t total_bytes = 0;
+    {
+        uint64_t ends[2] = {0, 0};
+        CU(cudaMemcpyAsync(&ends[0], d_offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(&ends[1], d_offsets + count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        total_bytes = ends[1] > ends[0] ? ends[1] - ends[0] : 0;
+        if (!d_texts && total_bytes > 0) return fail(SFA_ERR_INVALID_ARG, "d_texts is NULL");
+    }
+    const uint64_t max_tasks = count + total_bytes / kBatchSeg + 1;
+    if (max_tasks > 0xffffffffull) return fail(SFA_ERR_INVALID_ARG, "batch too large");
+    const size_t need = max_tasks * (h->vec() ? 32 : 4);
+    if (h->seg_cap < need) {
+        if (h->seg_parts) CU(cudaFree(h->seg_parts));
+        h->seg_parts = nullptr;
+        h->seg_cap = 0;
+        CU(cudaMalloc(&h->seg_parts, need));
+        h->seg_cap = need;
+    }
+    sfa::BatchArgs a;
+    a.t = h->tables();
+    a.texts = d_texts;
+    a.off = d_offsets;
+    a.count = count;
+    a.seg = kBatchSeg;
+    a.task_off = h->task_off;
+    a.work = h->work;
+    a.seg_parts = h->seg_parts;
+    a.results = d_results;
+    cudaError_t e = sfa::launch_batch(mode, h->vec(), a, h->sm_count, s);
+    if (e != cudaSuccess) return cuda_fail(e, "batch launch");
+    return h->end(s);
+}
+
+int sfa_match_host(const sfa_handle* hc, const uint8_t* h_text, size_t n, sfa_stream_t stream, uint32_t* final_state,
+                   int* accept) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !final_state || !accept) return fail(SFA_ERR_INVALID_ARG, "NULL argument");
+    if (!h_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "h_text is NULL with n > 0");
+    if (n == 0) {
+        *final_state = 0;
+        *accept = h->A.dfa_final[0];
+        return SFA_OK;
+    }
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    if (!h->dmaps16) return fail(SFA_ERR_CAPACITY, "mapping table too large for sliced host matching");
+    if (!h->stage[0]) {
+        for (int i = 0; i < 2; ++i) {
+            CU(cudaMalloc(&h->stage[i], kSlice));
+            CU(cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_used[i], cudaEventDisableTiming));
+        }
+        CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    }
+    // The copy stream must not overwrite a staging buffer before earlier work
+    // on `s` (from a previous call) is done with it.
+    CU(cudaEventRecord(h->ev_used[0], s));
+    CU(cudaEventRecord(h->ev_used[1], s));
+    const uint64_t m = (n + kSlice - 1) / kSlice;
+    for (uint64_t k = 0; k < m; ++k) {
+        const int b = static_cast<int>(k & 1);
+        const uint64_t off = k * kSlice, len = std::min<uint64_t>(kSlice, n - off);
+        CU(cudaStreamWaitEvent(h->copy_stream, h->ev_used[b], 0));
+        CU(cudaMemcpyAsync(h->stage[b], h_text + off, len, cudaMemcpyHostToDevice, h->copy_stream));
+        CU(cudaEventRecord(h->ev_copied[b], h->copy_stream));
+        CU(cudaStreamWaitEvent(s, h->ev_copied[b], 0));
+        // slice k runs from q_{k-1} = result of slice k-1 (sequential reduction across slices)
+        const uint32_t* q_in = k == 0 ? nullptr : &h->dres[(k - 1) & 1].final_state;
+        rc = h->launch_one(h->stage[b], len, s, q_in, &h->dres[k & 1]);
+        if (rc) return rc;
+        CU(cudaEventRecord(h->ev_used[b], s));
+    }
+    CU(cudaMemcpyAsync(h->hres, &h->dres[(m - 1) & 1], sizeof(sfa_result), cudaMemcpyDeviceToHost, s));
+    rc = h->end(s);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(s));
+    *final_state = h->hres[0].final_state;
+    *accept = static_cast<int>(h->hres[0].accept);
+    return SFA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// kernels.hpp -- launch interface of the sm_100a kernels (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "plan.hpp"
+
+namespace sfa {
+
+// q_in (device, nullable): the DFA state the text is run from.  NULL means q0
+// (Alg. 5 line 7).  A non-NULL q_in chains slices of one text:
+// q_final = f_slice(q_in), the sequential reduction of Alg. 5 (right column,
+// PAPER.md:567-573) applied across slices.
+
+struct ScanArgs {
+    DevTables t;
+    const uint8_t* text;  // base of the text (device)
+    uint64_t n;
+    TmaPlan plan;
+    Scratch sc;
+    const uint32_t* q_in;
+    sfa_result* result;
+};
+
+struct DirectArgs {
+    DevTables t;
+    const uint8_t* text;
+    uint64_t n;
+    uint64_t npieces;
+    Scratch sc;
+    const uint32_t* q_in;
+    sfa_result* result;
+    uint32_t* piece_ids;  // optional, npieces entries (device SFA ids)
+};
+
+struct BatchArgs {
+    DevTables t;
+    const uint8_t* texts;
+    const uint64_t* off;   // count + 1
+    uint64_t count;
+    uint64_t seg;          // max bytes per task
+    uint32_t* task_off;    // count + 1 (scratch)
+    uint32_t* work;        // work-stealing counter (scratch)
+    uint8_t* seg_parts;    // per task: 32 B (vector) or 4 B (id)
+    sfa_result* results;   // count
+};
+
+size_t tma_smem_bytes(Res mode, const DevTables& t);
+size_t direct_smem_bytes(Res mode, const DevTables& t);
+size_t table_smem_bytes(Res mode, const DevTables& t);
+uint32_t tma_rows_per_cta();
+uint32_t direct_threads_per_cta();
+
+cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, cudaStream_t stream);
+cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);
+cudaError_t launch_batch(Res mode, bool vec, const BatchArgs& a, int sm_count, cudaStream_t stream);
+
+}  // namespace sfa

@@ -1,0 +1,48 @@
+// plan.hpp -- device-table descriptors and launch plans shared by host and device code.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/sfa.h"
+
+namespace sfa {
+
+// Device copies of the compiled automata (all owned by the handle).
+struct DevTables {
+    const uint16_t* T = nullptr;        // nS * C   next SFA id per (state, class)
+    const uint8_t* cls = nullptr;       // 256      byte -> class
+    const uint16_t* Trange = nullptr;   // nS * W   next SFA id per (state, window column)
+    const uint8_t* maps32 = nullptr;    // nS * 32  f_s(q) for |D| <= 32 (identity-padded)
+    const uint16_t* maps16 = nullptr;   // nS * nD  f_s(q) (any |D|; used to apply f_fin to q_in != q0)
+    const uint32_t* img0 = nullptr;     // nS       f_s(q0)
+    const uint8_t* dfinal = nullptr;    // nD       q in F_d
+    const uint32_t* rep_off = nullptr;  // nS + 1
+    const uint8_t* rep = nullptr;       // representative words (bytes)
+    uint32_t nS = 0, C = 0, nD = 0;
+    uint32_t lo = 0, W = 0;             // byte window: columns lo..lo+W-2, column W-1 = every other byte
+};
+
+// Residency modes that have a kernel (sfa_residency without AUTO).
+enum class Res : int { Private = SFA_RES_SMEM_PRIVATE, Shared = SFA_RES_SMEM_SHARED, Hot = SFA_RES_HOT_L2, Global = SFA_RES_L2 };
+
+// Per-launch scratch owned by the handle.
+struct Scratch {
+    uint8_t* partials = nullptr;   // per CTA (+1 tail slot): 32 B vector or 4 B id
+    uint32_t* ticket = nullptr;    // last-CTA-done counter (self-resetting)
+    uint32_t max_ctas = 0;         // slots available in partials (excluding the tail slot)
+};
+
+// Single-text scan through the TMA pipeline.  The text [0, n) is cut into
+//   head  [0, head)                           < 16 bytes, up to 16-B alignment
+//   rows  [head + r*L, head + (r+1)*L), r < nchunks   (the 2-D TMA tensor)
+//   tail  [tail_start, n)                     < L + 16 bytes
+// Every piece is a chunk of Alg. 5 (any division, Theorem 3).
+struct TmaPlan {
+    uint64_t head = 0;
+    uint64_t L = 0;           // row length, multiple of 16
+    uint32_t nchunks = 0;     // rows
+    uint32_t ctas = 0;
+    uint64_t tail_start = 0;  // head + nchunks * L
+};
+
+}  // namespace sfa

@@ -1,0 +1,317 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bit-exact on (final DFA state, accept bit) per text, and on the per-chunk SFA
+ids where the chunking is forced (canonical ids, C3), for all five
+BASELINE.json configs at full size, scaled sizes spanning several tiles with
+ragged tails, every residency mode, batches with empty and ragged texts, and
+the host-buffer end-to-end call.  The oracle is Alg. 2 of
+an independently built DFA; chunk ids come from the oracle's plain Alg. 5.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1405_0562_b200 as P
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+CFG1 = ("(ab|ba)*c", b"abc")
+CFG2 = ("([0-4]{5}[5-9]{5})*", b"0123456789")
+CFG4 = (".*a[ab]{8}", b"ab")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda(cuda_ok):
+    import torch
+    return torch
+
+
+def dev(torch, a: np.ndarray, pad_front: int = 0):
+    """Device copy of a uint8 array, starting `pad_front` bytes into a buffer
+    (so the text's address has any alignment)."""
+    buf = torch.empty(a.size + pad_front + 16, dtype=torch.uint8, device="cuda")
+    v = buf[pad_front:pad_front + a.size]
+    if a.size:
+        v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return buf, v
+
+
+def spec_bounds(n, p):
+    """SPEC's chunk rule (C6): floor(n/p), remainder to the leading chunks."""
+    p = min(p, n) if n else 1
+    q, r = divmod(n, p)
+    return np.array([g * q + min(g, r) for g in range(p + 1)], np.uint64)
+
+
+_cache = {}
+
+
+def oracle_pair(rx, alpha):
+    key = (rx, alpha)
+    if key not in _cache:
+        d = O.OracleDFA(rx, alpha)
+        _cache[key] = d
+    return _cache[key]
+
+
+def check_text(torch, sfa, d, text, pad=0):
+    buf, v = dev(torch, text, pad)
+    got = sfa.match(v)
+    exp = d.run(text)
+    assert got == exp, (len(text), pad, got, exp)
+    return got
+
+
+# --------------------------------------------------------------------------- config 1
+def test_cfg1_full_size_and_forced_chunk_counts(torch_cuda):
+    torch = torch_cuda
+    sfa = P.SFA(*CFG1)
+    d = oracle_pair(*CFG1)
+    s = O.OracleSFA(d)
+    for text, exp in [(W.cfg1_random(), (4, False)), (W.cfg1_accepted(), (3, True))]:
+        assert d.run(text) == exp                          # closed form
+        assert check_text(torch, sfa, d, text) == exp
+        buf, v = dev(torch, text)
+        for p in (1, 7, 64, 4096):
+            q, acc, ids = sfa.match_chunked(v, p)
+            assert (q, acc) == exp, p
+            o_ids, q_seq, q_par = s.run_chunked(text, spec_bounds(text.size, p))
+            assert q_seq == q_par == exp[0]
+            assert ids.tolist() == o_ids.tolist(), p           # bit-exact per-chunk SFA ids
+
+
+def test_cfg1_random_chunkings(torch_cuda):
+    torch = torch_cuda
+    sfa = P.SFA(*CFG1)
+    d = oracle_pair(*CFG1)
+    s = O.OracleSFA(d)
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        n = int(rng.integers(1, 5000))
+        # mostly-accepted texts so the state is not stuck in the dead state
+        t = W.cfg1_accepted(n // 2)
+        if rng.random() < 0.5:
+            t = t.copy()
+            t[rng.integers(0, t.size)] = np.uint8(rng.integers(97, 100))
+        buf, v = dev(torch, t, int(rng.integers(0, 16)))
+        for p in (1, 2, 3, 7, int(rng.integers(1, n + 2))):
+            q, acc, ids = sfa.match_chunked(v, p)
+            o_ids, q_seq, _ = s.run_chunked(t, spec_bounds(t.size, p))
+            assert (q, acc) == d.run(t)
+            assert ids.tolist() == o_ids.tolist()
+
+
+# --------------------------------------------------------------------------- config 2
+def test_cfg2_full_size_accept_and_reject(torch_cuda):
+    torch = torch_cuda
+    sfa = P.SFA(*CFG2)
+    d = oracle_pair(*CFG2)
+    a = W.cfg2_accepted()
+    assert a.size == 268_435_450
+    assert check_text(torch, sfa, d, a) == (0, True)
+    r = W.cfg2_rejected(text=a)
+    assert check_text(torch, sfa, d, r) == (2, False)
+    # same text at every 16-byte misalignment (head piece), and prefixes (ragged tail)
+    buf, v = dev(torch, a, 5)
+    assert sfa.match(v) == (0, True)
+    for cut in (1, 9, 15, 17, 12345, 1 << 20):
+        t = a[:a.size - cut]
+        assert sfa.match(v[:a.size - cut]) == d.run(t), cut
+
+
+def test_cfg2_scaled_sizes_every_alignment(torch_cuda):
+    """Sizes around the direct/TMA switch and the per-SM row count, all 16 alignments."""
+    torch = torch_cuda
+    sfa = P.SFA(*CFG2)
+    d = oracle_pair(*CFG2)
+    base = W.cfg2_accepted(1_200_000)          # 12 MB
+    rng = np.random.default_rng(8)
+    sizes = [0, 1, 15, 16, 17, 255, 4096, 65537, (4 << 20) - 1, 4 << 20, (4 << 20) + 1, 4_757_011,
+             10 * 148 * 992 + 7, 12_000_000]
+    for n in sizes:
+        t = base[:n].copy()
+        if n > 100 and rng.random() < 0.5:
+            t[rng.integers(0, n)] = np.uint8(48 + rng.integers(0, 10))   # maybe rejected
+        for pad in (0, 1, 7, 15):
+            check_text(torch, sfa, d, t, pad)
+
+
+# --------------------------------------------------------------------------- config 3
+def test_cfg3_full_size_contains_match(torch_cuda):
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    sfa = P.SFA(rx, None)
+    d = oracle_pair(rx, None)
+    t = W.cfg3_text()
+    assert check_text(torch, sfa, d, t)[1] is False
+    words = W.cfg3_words()
+    s = W._streams(3)
+    w = words[int(s[3].integers(0, len(words)))]
+    off = int(s[2].integers(0, t.size - len(w) + 1))
+    t[off:off + len(w)] = np.frombuffer(w, np.uint8)          # == cfg3_text(plant=True)
+    assert check_text(torch, sfa, d, t)[1] is True
+
+
+def test_cfg3_scaled_with_planted_words(torch_cuda):
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    sfa = P.SFA(rx, None)
+    d = oracle_pair(rx, None)
+    t0 = W.cfg3_text(1 << 23)
+    rng = np.random.default_rng(4)
+    words = W.cfg3_words()
+    for trial in range(12):
+        t = t0[: int(rng.integers(1, t0.size))].copy()
+        if trial % 2:
+            w = words[int(rng.integers(0, 32))]
+            if len(w) <= t.size:
+                o = int(rng.integers(0, t.size - len(w) + 1))
+                t[o:o + len(w)] = np.frombuffer(w, np.uint8)
+        if trial % 3 == 0:
+            t[rng.integers(0, t.size)] = np.uint8(rng.integers(0, 256))   # out-of-window byte
+        check_text(torch, sfa, d, t, int(rng.integers(0, 16)))
+
+
+# --------------------------------------------------------------------------- config 4
+def test_cfg4_full_size(torch_cuda):
+    torch = torch_cuda
+    sfa = P.SFA(*CFG4)
+    d = oracle_pair(*CFG4)
+    t = W.cfg4_text()
+    q, acc = check_text(torch, sfa, d, t)
+    assert acc == (t[-9] == ord("a"))                         # closed form
+
+
+# --------------------------------------------------------------------------- config 5 (batch)
+def _batch(torch, sfa, texts, off):
+    count = off.size - 1
+    bt, vt = dev(torch, texts)
+    do = torch.from_numpy(off.astype(np.int64)).cuda()
+    res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
+    sfa.match_batch(vt if texts.size else bt, do, count, res)
+    torch.cuda.synchronize()
+    r = res.cpu().numpy().view(np.uint32).reshape(count, 2)
+    return r[:, 0], r[:, 1]
+
+
+def test_cfg5_full_size_batch(torch_cuda):
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    sfa = P.SFA(rx, None)
+    d = oracle_pair(rx, None)
+    texts, off, idx = W.cfg5_batch()
+    q, acc = _batch(torch, sfa, texts, off)
+    qo, acco = d.run_batch(texts, off)
+    assert (q == qo).all() and (acc == acco).all()
+    assert np.flatnonzero(acc).tolist() == idx.tolist()        # exactly the planted texts
+
+
+@pytest.mark.parametrize("rx,alpha", [CFG1, CFG2, CFG4, (W.cfg3_regex(), None)])
+def test_batch_ragged_with_empty_texts(torch_cuda, rx, alpha):
+    torch = torch_cuda
+    sfa = P.SFA(rx, alpha)
+    d = oracle_pair(rx, alpha)
+    for seed, count, max_len in [(1, 1, 0), (2, 3, 10), (3, 500, 3000), (4, 40, 300_000)]:
+        texts, off = W.ragged_batch(seed, count, max_len, alpha if alpha else b"abcdefghijklmnopqrstuvwxyz")
+        q, acc = _batch(torch, sfa, texts, off)
+        qo, acco = d.run_batch(texts, off)
+        assert (q == qo).all() and (acc == acco).all(), (seed, count)
+
+
+def test_batch_count_zero_is_noop(torch_cuda):
+    sfa = P.SFA(*CFG1)
+    sfa.match_batch(0, 0, 0, 0)
+
+
+# --------------------------------------------------------------------------- residency modes
+@pytest.mark.parametrize("rx,alpha,modes", [(*CFG1, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_L2)),
+                                            (*CFG2, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_L2)),
+                                            (*CFG4, (P.RES_SMEM_SHARED, P.RES_L2)),
+                                            (W.cfg3_regex(), None, (P.RES_L2,))])
+def test_every_residency_mode(torch_cuda, rx, alpha, modes):
+    torch = torch_cuda
+    d = oracle_pair(rx, alpha)
+    sfa = P.SFA(rx, alpha)
+    rng = np.random.default_rng(6)
+    al = np.frombuffer(alpha if alpha else b"abcdefghijklmnopqrstuvwxyz", np.uint8)
+    texts = [al[rng.integers(0, al.size, size=n)] for n in (1, 1000, 5_000_000)]
+    if rx == CFG2[0]:
+        texts.append(W.cfg2_accepted(700_000))
+    if rx == CFG1[0]:
+        texts.append(W.cfg1_accepted(3_000_000))
+    for m in modes:
+        sfa.set_residency(m)
+        assert P.sfa_info(sfa.h)["residency"] == m
+        for t in texts:
+            check_text(torch, sfa, d, t, 3)
+
+
+def test_private_capacity_refused_for_big_table(torch_cuda):
+    sfa = P.SFA(W.cfg3_regex(), None)
+    with pytest.raises(P.SFAError) as e:
+        sfa.set_residency(P.RES_SMEM_PRIVATE)
+    assert e.value.code == P.SFA_ERR_CAPACITY
+
+
+# --------------------------------------------------------------------------- random regexes
+def test_random_regexes_small_texts(torch_cuda):
+    torch = torch_cuda
+    from test_oracle import _random_regex
+    rng = np.random.default_rng(21)
+    for _ in range(40):
+        rx = _random_regex(rng, 5)
+        alpha = b"abcd" if rng.random() < 0.6 else None
+        d = O.OracleDFA(rx, alpha)
+        sfa = P.SFA(rx, alpha)
+        for n in (0, 1, 2, 33, 700, 20_000):
+            t = np.frombuffer(b"abcde", np.uint8)[rng.integers(0, 5, size=n)]
+            check_text(torch, sfa, d, t, int(rng.integers(0, 16)))
+
+
+# --------------------------------------------------------------------------- API entry points
+def test_empty_text_and_async_and_host(torch_cuda):
+    torch = torch_cuda
+    sfa = P.SFA("(ab)*", b"ab")
+    empty = torch.empty(0, dtype=torch.uint8, device="cuda")
+    assert sfa.match(empty) == (0, True)
+    res = torch.zeros(2, dtype=torch.int32, device="cuda")
+    t = np.frombuffer(b"ab" * 3_000_000, np.uint8)
+    buf, v = dev(torch, t)
+    sfa.match_async(v, res)
+    torch.cuda.synchronize()
+    assert res.cpu().tolist() == [0, 1]
+    sfa.match_async(empty, res)
+    torch.cuda.synchronize()
+    assert res.cpu().tolist() == [0, 1]
+    assert sfa.match_host(t) == (0, True)
+    assert sfa.match_host(t[:-1]) == (1, False)
+
+
+def test_match_host_slices_full_cfg2(torch_cuda):
+    """sfa_match_host: 64 MiB slices chained by q_in (sequential reduction across
+    slices) from pinned memory == Alg. 2."""
+    torch = torch_cuda
+    sfa = P.SFA(*CFG2)
+    d = oracle_pair(*CFG2)
+    a = W.cfg2_accepted()
+    pinned = torch.from_numpy(a).pin_memory()
+    assert sfa.match_host(pinned) == (0, True)
+    for n in (a.size - 3, (64 << 20) + 5, (128 << 20) - 1):
+        assert sfa.match_host(pinned[:n]) == d.run(a[:n]), n
+    r = W.cfg2_rejected(text=a)
+    assert sfa.match_host(r) == (2, False)
+
+
+def test_match_host_replay_mode(torch_cuda):
+    """q_in chaining through maps16 (|D| > 32)."""
+    torch = torch_cuda
+    sfa = P.SFA(*CFG4)
+    d = oracle_pair(*CFG4)
+    t = W.cfg4_text(150 << 20)
+    assert sfa.match_host(t) == d.run(t)
+    rx = W.cfg3_regex()
+    sfa3 = P.SFA(rx, None)
+    d3 = oracle_pair(rx, None)
+    t3 = W.cfg3_text(130 << 20, plant=True)
+    assert sfa3.match_host(t3) == d3.run(t3)
