@@ -180,10 +180,11 @@ struct sfa_handle {
     // does `mode` fit for this launch kind?
     bool fits(sfa::Res mode, int kind /*0 tma, 1 direct, 2 batch*/) const {
         const sfa::DevTables t = tables();
-        size_t need = kind == 0 ? sfa::tma_smem_bytes(mode, t) : kind == 1 ? sfa::direct_smem_bytes(mode, t)
-                                                                           : sfa::table_smem_bytes(mode, t);
-        if (mode == sfa::Res::Global) return need <= smem_optin;
-        if (mode == sfa::Res::Private && (static_cast<uint64_t>(A.nS) * W * 128 > (1ull << 31))) return false;
+        if (kind == 0) {
+            sfa::TmaConfig c;
+            return sfa::tma_choose(mode, t, smem_optin, &c);
+        }
+        const size_t need = kind == 1 ? sfa::direct_smem_bytes(mode, t) : sfa::table_smem_bytes(mode, t);
         return need <= smem_optin;
     }
     int resolve(int kind, sfa::Res* out) const {
@@ -238,21 +239,27 @@ struct sfa_handle {
             a.sc = scratch();
             a.q_in = q_in;
             a.result = d_result;
-            const uint64_t R = sfa::tma_rows_per_cta();
-            uint64_t head = (16 - (reinterpret_cast<uintptr_t>(d_text) & 15)) & 15;
+            sfa::TmaConfig cfg;
+            if (!sfa::tma_choose(mode, a.t, smem_optin, &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
+            // box heights (rows_per_cta / NB) keep every TMA destination 128-B aligned
+            const uint64_t R = cfg.rows_per_cta, NB = cfg.nb * (128 / cfg.rowb), G = static_cast<uint64_t>(sm_count);
+            uint64_t head = (256 - (reinterpret_cast<uintptr_t>(d_text) & 255)) & 255;
             head = std::min<uint64_t>(head, n);
-            const uint64_t body16 = (n - head) & ~uint64_t(15);
-            const uint64_t rtot = R * static_cast<uint64_t>(sm_count);
-            uint64_t L = 16 * ((body16 + 16 * rtot - 1) / (16 * rtot));
-            if (L == 0) L = 16;
-            const uint64_t rows = body16 / L;
+            const uint64_t body = n - head;
+            // rows of L bytes (a multiple of 256), at most G*R of them, spread
+            // evenly over G CTAs in multiples of NB (TMA box count x alignment)
+            uint64_t L = 256 * ((body + 256 * G * R - 1) / (256 * G * R));
+            if (L == 0) L = 256;
+            const uint64_t rows = body / L;
+            const uint64_t rc = NB * ((rows + G * NB - 1) / (G * NB));
             a.plan.head = head;
             a.plan.L = L;
             a.plan.nchunks = static_cast<uint32_t>(rows);
-            a.plan.ctas = static_cast<uint32_t>((rows + R - 1) / R);
+            a.plan.rows_per_cta = static_cast<uint32_t>(rc);
+            a.plan.ctas = rc ? static_cast<uint32_t>((rows + rc - 1) / rc) : 0;
             a.plan.tail_start = head + rows * L;
             if (rows == 0 || a.plan.ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "bad scan plan");
-            e = sfa::launch_scan_tma(mode, vec(), a, stream);
+            e = sfa::launch_scan_tma(mode, vec(), a, cfg, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "scan launch");
         return SFA_OK;

@@ -2,20 +2,22 @@
 // SFA chunk run (Alg. 5 lines 1-5).
 //
 // A "step policy" owns where the SFA transition table delta_s lives (A6,
-// residency) and how one text byte advances a chunk's SFA state (A1 + A2):
+// residency) and how one text byte advances a chunk's SFA state (A1 + A2).
+// Every table sits at dynamic shared-memory offset 0 so its base is a
+// compile-time immediate of the LDS.
 //
 //   StepPrivate  byte -> column by arithmetic on a byte window [lo, lo+W-2]
-//                (all other bytes share column W-1), table in shared memory as
-//                32 bank-private copies with premultiplied lane addresses:
-//                per byte  PRMT/SHF + VIADDMNMX + LEA + LDS.32, 1 conflict-free
-//                shared wavefront.
-//   StepShared   class map (u16, 2*class) + one u16 table in shared memory:
-//                per byte  LDS.U16 (class) + IMAD + LDS.U16 (next state).
-//   StepGlobal   class map in shared memory, u16 table read through L1/L2.
+//                (every other byte shares column W-1); table in shared memory
+//                as 32 bank-private u16 copies (lane L only touches bank L):
+//                per byte  PRMT (byte) + VIADDMNMX (column) + IMAD (address)
+//                + LDS.U16, one conflict-free wavefront per warp.
+//   StepShared   one copy of the [nS x W] window table in shared memory, u32
+//                entries premultiplied to row offsets: per byte PRMT +
+//                VIADDMNMX + LEA + LDS (random banks: conflicts possible).
+//   StepGlobal   the u16 window table read through L1/L2 (any |S|).
 //
-// Every policy exposes the same interface so the kernels are generic:
-//   init(lane) -> state of f_I;  step(state, byte) -> state;
-//   id(state, lane) -> SFA id;   from_id(id, lane) -> state.
+// Interface:  init(lane) -> state of f_I;  step(state, byte) -> state;
+//             id(state, lane) -> SFA id;   from_id(id, lane) -> state.
 #pragma once
 
 #include <cstdint>
@@ -25,20 +27,28 @@
 
 namespace sfa {
 
+// The kernels' dynamic shared memory.  Tables are indexed through this symbol
+// (not through a cvta'd address) so the shared-window base folds into the LDS
+// immediate instead of costing an add per byte.
+extern __shared__ __align__(1024) uint8_t dsmem[];
+
+__device__ __forceinline__ uint32_t ld_tbl_u16(uint32_t off) { return *reinterpret_cast<const uint16_t*>(dsmem + off); }
+__device__ __forceinline__ uint32_t ld_tbl_u32(uint32_t off) { return *reinterpret_cast<const uint32_t*>(dsmem + off); }
+
 // ------------------------------------------------------------------------------------------
 // PTX wrappers
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
-    uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     uint16_t v;
-    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
@@ -53,7 +63,13 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
-__device__ __forceinline__ uint32_t ldg_u16(const uint16_t* p) { return __ldg(p); }
+// byte k of w, zero-extended: one PRMT
+template <int K>
+__device__ __forceinline__ uint32_t byte_of(uint32_t w) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "n"(0x4440 | K));
+    return r;
+}
 
 // mbarrier (shared::cta)
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -101,104 +117,114 @@ __device__ __forceinline__ void bar_compute(uint32_t nthreads) {
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 constexpr unsigned kFull = 0xffffffffu;
 
+// column of a byte in the window table: min(byte - lo (mod 2^32), W - 1)
+__device__ __forceinline__ uint32_t window_col(uint32_t byte, uint32_t neg_lo, uint32_t wmax) {
+    return __viaddmin_u32(byte, neg_lo, wmax);
+}
+
 // ------------------------------------------------------------------------------------------
 // Step policies
 // ------------------------------------------------------------------------------------------
 struct StepPrivate {
-    // table: nS * W * 32 words; word ((s*W + j)*32 + L) of lane L's copy holds
-    // the shared-memory byte address of row delta_s(s, column j) in lane L's
-    // copy, so one LEA + one LDS advances the state.
-    uint32_t base;     // shared address of the table
-    uint32_t neg_lo;   // -lo (mod 2^32)
-    uint32_t wmax;     // W - 1 (the "every other byte" column)
-    uint32_t row_words;  // W * 32
+    // Lane L's copy lives in bank L.  Cell (s, j) of lane L is the u16 at byte
+    //   j*X + (s>>1)*128 + 4L + 2(s&1)          (X = 128 * ceil(nS/2))
+    // and holds enc(delta_s(s, j), L) = (s'>>1)*128 + 4L + 2(s'&1), the
+    // column-0 offset of the next state in lane L's copy, so the next address
+    // is one IMAD: col*X + state.  Needs X <= 65536 (nS <= 1024).
+    uint32_t X, neg_lo, wmax;
 
-    static __host__ __device__ size_t smem_bytes(const DevTables& t) {
-        return static_cast<size_t>(t.nS) * t.W * 32 * 4;
-    }
+    static __host__ __device__ uint32_t col_bytes(const DevTables& t) { return 128u * ((t.nS + 1) / 2); }
+    static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.W) * col_bytes(t); }
+    static __host__ __device__ bool supported(const DevTables& t) { return t.nS <= 1024; }
+    static __device__ __forceinline__ uint32_t enc(uint32_t s, uint32_t L) { return (s >> 1) * 128u + 4u * L + 2u * (s & 1u); }
+
+    // the table must be at dsmem offset 0 (smem == dsmem)
     __device__ void setup(const DevTables& t, uint8_t* smem, int tid, int nthreads) {
-        base = smem_u32(smem);
+        X = col_bytes(t);
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
-        row_words = t.W * 32;
         uint32_t* tbl = reinterpret_cast<uint32_t*>(smem);
-        const uint32_t total = t.nS * row_words;
+        const uint32_t words_per_col = X / 4, total = t.W * words_per_col;
         for (uint32_t i = tid; i < total; i += nthreads) {
-            uint32_t cell = i >> 5, L = i & 31;  // cell = s*W + j
-            uint32_t nxt = t.Trange[cell];
-            tbl[i] = base + (nxt * row_words + L) * 4u;
+            const uint32_t j = i / words_per_col, rem = i - j * words_per_col;
+            const uint32_t pair = rem >> 5, L = rem & 31;
+            const uint32_t s0 = 2 * pair, s1 = s0 + 1;
+            const uint32_t v0 = enc(t.Trange[s0 * t.W + j], L);
+            const uint32_t v1 = s1 < t.nS ? enc(t.Trange[s1 * t.W + j], L) : 0u;
+            tbl[i] = v0 | (v1 << 16);
         }
     }
-    __device__ __forceinline__ uint32_t init(uint32_t lane) const { return base + lane * 4u; }
+    __device__ __forceinline__ uint32_t init(uint32_t lane) const { return 4u * lane; }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
-        uint32_t col = __viaddmin_u32(byte, neg_lo, wmax);  // min(byte - lo, W-1), wrapping below lo
-        return lds_u32(st + (col << 7));
+        const uint32_t col = window_col(byte, neg_lo, wmax);
+        return ld_tbl_u16(col * X + st);
     }
-    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return ((st - base) >> 2) / row_words; }
-    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t lane) const {
-        return base + (s * row_words + lane) * 4u;
-    }
+    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return ((st >> 7) << 1) | ((st >> 1) & 1u); }
+    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t lane) const { return enc(s, lane); }
 };
 
 struct StepShared {
-    // cls: 256 x u16 holding 2*class; T: nS*C u16 SFA ids.
-    uint32_t cls_base, t_base, two_c;
+    // one copy of the window table, u32 entries premultiplied to byte offsets:
+    // state = 4*W*s (offset of row s), cell (s, j) holds 4*W*delta_s(s, j).
+    uint32_t neg_lo, wmax, row;
 
-    static __host__ __device__ size_t smem_bytes(const DevTables& t) {
-        return 512 + ((static_cast<size_t>(t.nS) * t.C * 2 + 15) & ~size_t(15));
-    }
+    static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.nS) * t.W * 4; }
+    static __host__ __device__ bool supported(const DevTables& t) { return static_cast<uint64_t>(t.nS) * t.W * 4 < (1u << 24); }
+    // the table must be at dsmem offset 0 (smem == dsmem)
     __device__ void setup(const DevTables& t, uint8_t* smem, int tid, int nthreads) {
-        cls_base = smem_u32(smem);
-        t_base = cls_base + 512;
-        two_c = 2 * t.C;
-        uint16_t* c16 = reinterpret_cast<uint16_t*>(smem);
-        for (int b = tid; b < 256; b += nthreads) c16[b] = static_cast<uint16_t>(2 * t.cls[b]);
-        uint16_t* T16 = reinterpret_cast<uint16_t*>(smem + 512);
-        const uint32_t total = t.nS * t.C;
-        for (uint32_t i = tid; i < total; i += nthreads) T16[i] = t.T[i];
+        neg_lo = 0u - t.lo;
+        wmax = t.W - 1;
+        row = 4 * t.W;
+        uint32_t* T32 = reinterpret_cast<uint32_t*>(smem);
+        const uint32_t total = t.nS * t.W;
+        for (uint32_t i = tid; i < total; i += nthreads) T32[i] = static_cast<uint32_t>(t.Trange[i]) * row;
     }
     __device__ __forceinline__ uint32_t init(uint32_t) const { return 0; }
-    __device__ __forceinline__ uint32_t step(uint32_t s, uint32_t byte) const {
-        uint32_t c2 = lds_u16(cls_base + 2 * byte);
-        return lds_u16(t_base + s * two_c + c2);
+    __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
+        const uint32_t col = window_col(byte, neg_lo, wmax);
+        return ld_tbl_u32(st + 4 * col);
     }
-    __device__ __forceinline__ uint32_t id(uint32_t s, uint32_t) const { return s; }
-    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return s; }
+    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return st / row; }
+    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return s * row; }
 };
 
 struct StepGlobal {
-    uint32_t cls_base, C;
+    // the u16 window table through L1/L2: state = s*W (element offset of row s)
+    uint32_t neg_lo, wmax, W;
     const uint16_t* T;
 
-    static __host__ __device__ size_t smem_bytes(const DevTables&) { return 512; }
-    __device__ void setup(const DevTables& t, uint8_t* smem, int tid, int nthreads) {
-        cls_base = smem_u32(smem);
-        C = t.C;
-        T = t.T;
-        uint16_t* c16 = reinterpret_cast<uint16_t*>(smem);
-        for (int b = tid; b < 256; b += nthreads) c16[b] = static_cast<uint16_t>(t.cls[b]);
+    static __host__ __device__ size_t smem_bytes(const DevTables&) { return 0; }
+    static __host__ __device__ bool supported(const DevTables&) { return true; }
+    __device__ void setup(const DevTables& t, uint8_t*, int, int) {
+        neg_lo = 0u - t.lo;
+        wmax = t.W - 1;
+        W = t.W;
+        T = t.Trange;
     }
     __device__ __forceinline__ uint32_t init(uint32_t) const { return 0; }
-    __device__ __forceinline__ uint32_t step(uint32_t s, uint32_t byte) const {
-        uint32_t c = lds_u16(cls_base + 2 * byte);
-        return ldg_u16(T + s * C + c);
+    __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
+        const uint32_t col = window_col(byte, neg_lo, wmax);
+        return static_cast<uint32_t>(__ldg(T + st + col)) * W;
     }
-    __device__ __forceinline__ uint32_t id(uint32_t s, uint32_t) const { return s; }
-    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return s; }
+    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return st / W; }
+    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return s * W; }
 };
 
-// 16 text bytes in text order (little-endian words)
+// 4 text bytes of one word, in text order (little-endian)
+template <class Step>
+__device__ __forceinline__ uint32_t step4(const Step& S, uint32_t st, uint32_t w) {
+    st = S.step(st, byte_of<0>(w));
+    st = S.step(st, byte_of<1>(w));
+    st = S.step(st, byte_of<2>(w));
+    st = S.step(st, byte_of<3>(w));
+    return st;
+}
 template <class Step>
 __device__ __forceinline__ uint32_t step16(const Step& S, uint32_t st, const uint4& v) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) st = S.step(st, (v.x >> (8 * k)) & 0xffu);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) st = S.step(st, (v.y >> (8 * k)) & 0xffu);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) st = S.step(st, (v.z >> (8 * k)) & 0xffu);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) st = S.step(st, (v.w >> (8 * k)) & 0xffu);
-    return st;
+    st = step4(S, st, v.x);
+    st = step4(S, st, v.y);
+    st = step4(S, st, v.z);
+    return step4(S, st, v.w);
 }
 
 // A byte range [a, b) of `t`, from state st, with 16-byte loads where aligned.

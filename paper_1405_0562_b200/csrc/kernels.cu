@@ -18,12 +18,20 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.hpp"
 
 namespace sfa {
+
+template <class Step>
+__host__ __device__ size_t table_bytes(const DevTables& t) {
+    return (Step::smem_bytes(t) + 15) & ~size_t(15);
+}
 
 // ------------------------------------------------------------------------------------------
 // Composition policy: vector form (|D| <= 32) or replay form (any |D|).
@@ -117,9 +125,10 @@ __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& 
         uint32_t b0 = min(nslots, warp * per), b1 = min(nslots, b0 + per);
         uint32_t acc = CP::fold_slots(S, t, sc.partials + b0 * CP::kSlot, b1 - b0, CP::identity(), true);
         CP::store(red + warp * CP::kSlot, acc);
-    } else {
-        uint32_t s = 0;
-        if (lane == 0 && head > 0) s = S.id(run_range(S, S.init(0), text, 0, head), 0);
+    } else {  // head [0, head), split over the 32 lanes
+        const uint64_t per = (head + 31) / 32;
+        const uint64_t h0 = min(head, lane * per), h1 = min(head, h0 + per);
+        const uint32_t s = S.id(run_range(S, S.init(lane), text, h0, h1), lane);
         CP::store(slot_head, CP::fold_states(S, t, s));
     }
     bar_compute(nthreads);
@@ -158,40 +167,60 @@ __device__ __forceinline__ void store_partial(uint8_t* partials, uint32_t slot, 
 
 // ------------------------------------------------------------------------------------------
 // k_scan_tma
+//
+// Shared memory (dynamic):  [table | red slots | flag | mbarriers | stage ring]
+// The table is first so its base is an immediate of every LDS.  A stage holds
+// ROWB bytes of each of the CTA's R rows (row-major, ROWB per row), loaded by
+// NB 2-D TMA boxes of [ROWB x BR]; the ring depth is chosen at launch from the
+// shared memory left after the table.  The producer also prefetches each
+// row's next 256-byte line into L2 once (a second tensor map with 256-B boxes)
+// so the TMA loads hit L2.
 // ------------------------------------------------------------------------------------------
-constexpr int kNW = 31;      // compute warps
-constexpr int kStages = 4;   // smem ring depth
-constexpr int kPF = 8;       // L2 prefetch distance (stages)
-constexpr int kRow = 16;     // bytes of each row per stage
+constexpr int kNW = 31;        // compute warps
+constexpr int kMaxRing = 8;    // max smem ring depth
+constexpr int kLine = 256;     // L2 prefetch granularity (bytes of a row)
 
 template <int K>
+__host__ __device__ constexpr int Sh_NB() { return (K * kNW * 32 + 255) / 256; }
+
+template <int K, int ROWB>
 struct TmaShape {
     static constexpr int R = K * kNW * 32;            // rows (chunks) per CTA
     static constexpr int NB = (R + 255) / 256;        // TMA boxes per stage (box dim <= 256)
     static constexpr int BR = R / NB;                 // rows per box
     static_assert(R % NB == 0, "rows must split evenly into boxes");
-    static constexpr uint32_t kStageBytes = R * kRow;
+    static_assert(ROWB % 16 == 0 && kLine % ROWB == 0, "row slice must be 16-B granular");
+    static constexpr uint32_t kStageBytes = R * ROWB;
     static constexpr uint32_t kRedBytes = ((K * kNW + 2) * 32 + 15) & ~15u;
-    static constexpr uint32_t kFixed = kStages * kStageBytes + 2 * kStages * 8 + kRedBytes + 16;
+    // bytes besides the table and the ring
+    static constexpr uint32_t kFixed = kRedBytes + 16 + 2 * kMaxRing * 8 + 128;
 };
 
-template <class Step, int K, bool VEC>
+struct TmaMaps {
+    CUtensorMap load;      // box [ROWB x BR]
+    CUtensorMap pref;      // box [256 x BR], L2 prefetch only
+};
+
+template <class Step, int K, int ROWB, bool VEC>
 __global__ void __launch_bounds__((kNW + 1) * 32, 1)
-k_scan_tma(const __grid_constant__ CUtensorMap tmap, const ScanArgs a) {
-    using Sh = TmaShape<K>;
+k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_t tbl_bytes, const uint32_t nring,
+           const uint32_t pf_lines) {
+    // rows of this CTA: [blockIdx.x * rc, +rc), loaded as NB boxes of br rows
+    const uint32_t rc = a.plan.rows_per_cta, br = rc / Sh_NB<K>();
+    using Sh = TmaShape<K, ROWB>;
     using CP = Comp<Step, VEC>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* stage_buf = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * Sh::kStageBytes);
-    uint8_t* red = smem + kStages * Sh::kStageBytes + 2 * kStages * 8;
+    uint8_t* smem = dsmem;
+    uint8_t* tbl = smem;
+    uint8_t* red = smem + ((tbl_bytes + 15) & ~15u);
     uint32_t* flag = reinterpret_cast<uint32_t*>(red + Sh::kRedBytes);
-    uint8_t* tbl = red + Sh::kRedBytes + 16;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + Sh::kRedBytes + 16);
+    const uint32_t ring0 = (smem_u32(bars + 2 * kMaxRing) + 127) & ~127u;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nstages = static_cast<uint32_t>(a.plan.L / kRow);
-    const uint32_t full0 = smem_u32(bars), empty0 = full0 + kStages * 8;
+    const uint32_t nstages = static_cast<uint32_t>(a.plan.L / ROWB);
+    const uint32_t full0 = smem_u32(bars), empty0 = full0 + kMaxRing * 8;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (uint32_t s = 0; s < nring; ++s) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, kNW);
         }
@@ -201,19 +230,29 @@ k_scan_tma(const __grid_constant__ CUtensorMap tmap, const ScanArgs a) {
 
     if (warp == kNW) {  // ---- TMA producer ----
         if (lane == 0) {
-            prefetch_tmap(&tmap);
-            const int y0 = blockIdx.x * Sh::R;
-            for (uint32_t i = 0; i < kPF && i < nstages; ++i)
-                for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&tmap, i * kRow, y0 + j * Sh::BR);
+            prefetch_tmap(&maps.load);
+            prefetch_tmap(&maps.pref);
+            const int y0 = blockIdx.x * rc;
+            const uint32_t nlines = static_cast<uint32_t>((a.plan.L + kLine - 1) / kLine);
+            for (uint32_t l = 0; l <= pf_lines && l < nlines; ++l)
+                for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&maps.pref, l * kLine, y0 + j * br);
+            constexpr uint32_t kStagesPerLine = kLine / ROWB;
+            uint32_t slot = 0, phase = 0;
             for (uint32_t i = 0; i < nstages; ++i) {
-                const uint32_t slot = i % kStages;
-                if (i >= kStages) mbar_wait(empty0 + 8 * slot, ((i / kStages) - 1) & 1);
-                mbar_expect_tx(full0 + 8 * slot, Sh::kStageBytes);
-                const uint32_t dst = smem_u32(stage_buf) + slot * Sh::kStageBytes;
+                if (i >= nring) mbar_wait(empty0 + 8 * slot, phase ^ 1);
+                mbar_expect_tx(full0 + 8 * slot, rc * ROWB);
+                const uint32_t dst = ring0 + slot * Sh::kStageBytes;
                 for (int j = 0; j < Sh::NB; ++j)
-                    tma_load_2d(dst + j * Sh::BR * kRow, &tmap, full0 + 8 * slot, i * kRow, y0 + j * Sh::BR);
-                if (i + kPF < nstages)
-                    for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&tmap, (i + kPF) * kRow, y0 + j * Sh::BR);
+                    tma_load_2d(dst + j * br * ROWB, &maps.load, full0 + 8 * slot, i * ROWB, y0 + j * br);
+                if (i % kStagesPerLine == 0) {  // entering line l: prefetch line l + pf_lines + 1
+                    const uint32_t l = i / kStagesPerLine + pf_lines + 1;
+                    if (l < nlines)
+                        for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&maps.pref, l * kLine, y0 + j * br);
+                }
+                if (++slot == nring) {
+                    slot = 0;
+                    phase ^= 1;
+                }
             }
         }
         return;
@@ -238,47 +277,56 @@ k_scan_tma(const __grid_constant__ CUtensorMap tmap, const ScanArgs a) {
     uint32_t st[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) st[k] = S.init(lane);
-    const uint32_t buf0 = smem_u32(stage_buf);
     const uint32_t row0 = warp * 32 + lane;
-    uint4 v[K];
-    if (nstages > 0) {
-        mbar_wait(full0, 0);
+    uint32_t rsrc[K];  // stage offset of each of this thread's rows (row 0 for idle threads)
 #pragma unroll
-        for (int k = 0; k < K; ++k) v[k] = lds_v4(buf0 + (k * kNW * 32 + row0) * kRow);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0);
+    for (int k = 0; k < K; ++k) {
+        const uint32_t r = k * kNW * 32 + row0;
+        rsrc[k] = (r < rc ? r : 0u) * ROWB;
     }
+    uint32_t slot = 0, phase = 0;
     for (uint32_t i = 0; i < nstages; ++i) {
-        uint4 nv[K];
-        const bool more = i + 1 < nstages;
-        if (more) {  // fetch the next stage's 16 bytes before consuming this one
-            const uint32_t slot = (i + 1) % kStages;
-            mbar_wait(full0 + 8 * slot, ((i + 1) / kStages) & 1);
+        mbar_wait(full0 + 8 * slot, phase);
+        const uint32_t src = ring0 + slot * Sh::kStageBytes;
+        uint4 v[K][ROWB / 16];
 #pragma unroll
-            for (int k = 0; k < K; ++k) nv[k] = lds_v4(buf0 + slot * Sh::kStageBytes + (k * kNW * 32 + row0) * kRow);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int c = 0; c < ROWB / 16; ++c) v[k][c] = lds_v4(src + rsrc[k] + c * 16);
+#pragma unroll
+        for (int c = 0; c < ROWB / 16; ++c) {
+            const uint32_t* w[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) w[k] = reinterpret_cast<const uint32_t*>(&v[k][c]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<0>(w[k][q]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<1>(w[k][q]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<2>(w[k][q]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
+            }
         }
-        const uint32_t* w[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) w[k] = reinterpret_cast<const uint32_t*>(&v[k]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], (w[k][q] >> (8 * b)) & 0xffu);
-        if (more) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = nv[k];
+        // Release the slot only now: every lane has consumed its loaded bytes,
+        // so no LDS of this stage can still be in flight when the producer's
+        // next TMA write lands (an arrive right after issuing the LDS raced).
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+        if (++slot == nring) {
+            slot = 0;
+            phase ^= 1;
         }
     }
 
     // ---- composition: warp -> block (rows are ordered k-major, then warp, then lane) ----
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const uint32_t row = blockIdx.x * Sh::R + k * kNW * 32 + row0;
-        const uint32_t s = row < a.plan.nchunks ? S.id(st[k], lane) : 0u;  // rows past the text: f_I
+        const uint32_t r = k * kNW * 32 + row0;
+        const uint32_t row = blockIdx.x * rc + r;
+        const uint32_t s = (r < rc && row < a.plan.nchunks) ? S.id(st[k], lane) : 0u;  // rows past the text: f_I
         CP::store(red + (k * kNW + warp) * CP::kSlot, CP::fold_states(S, a.t, s));
     }
     bar_compute(kNW * 32);
@@ -304,10 +352,9 @@ __device__ __forceinline__ uint64_t piece_start(uint64_t g, uint64_t n, uint64_t
 template <class Step, bool VEC>
 __global__ void __launch_bounds__(kDirectWarps * 32)
 k_scan_direct(const DirectArgs a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* red = smem;
-    uint32_t* flag = reinterpret_cast<uint32_t*>(smem + kDirectRed);
-    uint8_t* tbl = smem + kDirectRed + 16;
+    uint8_t* tbl = dsmem;  // table at offset 0
+    uint8_t* red = dsmem + ((table_bytes<Step>(a.t) + 15) & ~size_t(15));
+    uint32_t* flag = reinterpret_cast<uint32_t*>(red + kDirectRed);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     Step S;
     S.setup(a.t, tbl, threadIdx.x, blockDim.x);
@@ -368,8 +415,7 @@ template <class Step, bool VEC>
 __global__ void __launch_bounds__(kBatchWarps * 32)
 k_batch_scan(const BatchArgs a) {
     using CP = Comp<Step, VEC>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* tbl = smem;
+    uint8_t* tbl = dsmem;
     const int lane = threadIdx.x & 31;
     Step S;
     S.setup(a.t, tbl, threadIdx.x, blockDim.x);
@@ -411,9 +457,8 @@ template <class Step, bool VEC>
 __global__ void __launch_bounds__(kBatchWarps * 32)
 k_batch_combine(const BatchArgs a) {
     using CP = Comp<Step, VEC>;
-    extern __shared__ __align__(128) uint8_t smem[];
     Step S;
-    S.setup(a.t, smem, threadIdx.x, blockDim.x);
+    S.setup(a.t, dsmem, threadIdx.x, blockDim.x);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -449,31 +494,47 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-template <class Step>
-size_t table_bytes(const DevTables& t) {
-    return (Step::smem_bytes(t) + 15) & ~size_t(15);
-}
 
-template <class Step, bool VEC>
-cudaError_t tma_launch(const ScanArgs& a, cudaStream_t stream) {
-    using Sh = TmaShape<1>;
-    auto kern = k_scan_tma<Step, 1, VEC>;
-    const size_t smem = Sh::kFixed + table_bytes<Step>(a.t);
+template <class Step, int K, int ROWB, bool VEC>
+cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
+    using Sh = TmaShape<K, ROWB>;
+    auto kern = k_scan_tma<Step, K, ROWB, VEC>;
+    const uint32_t tbytes = static_cast<uint32_t>(table_bytes<Step>(a.t));
+    const size_t smem = tbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
-    CUtensorMap tmap;
+    TmaMaps maps;
     cuuint64_t dims[2] = {a.plan.L, a.plan.nchunks};
     cuuint64_t strides[1] = {a.plan.L};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kRow), static_cast<cuuint32_t>(Sh::BR)};
+    const cuuint32_t br = a.plan.rows_per_cta / Sh::NB;
+    if (br == 0 || br > 256 || br * Sh::NB != a.plan.rows_per_cta || (br * ROWB) % 128) return cudaErrorInvalidValue;
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(ROWB), br};
+    cuuint32_t pbox[2] = {static_cast<cuuint32_t>(kLine), br};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.text + a.plan.head), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    void* base = const_cast<uint8_t*>(a.text + a.plan.head);
+    CUresult r = enc(&maps.load, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    kern<<<a.plan.ctas, (kNW + 1) * 32, smem, stream>>>(tmap, a);
+    r = enc(&maps.pref, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, pbox, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    kern<<<a.plan.ctas, (kNW + 1) * 32, smem, stream>>>(maps, a, tbytes, cfg.nring, cfg.pf_lines);
     return cudaGetLastError();
+}
+
+template <class Step, bool VEC>
+cudaError_t tma_launch(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
+    switch (cfg.K * 1000 + cfg.rowb) {
+        case 1016: return tma_launch_t<Step, 1, 16, VEC>(a, cfg, stream);
+        case 1032: return tma_launch_t<Step, 1, 32, VEC>(a, cfg, stream);
+        case 2016: return tma_launch_t<Step, 2, 16, VEC>(a, cfg, stream);
+        case 2032: return tma_launch_t<Step, 2, 32, VEC>(a, cfg, stream);
+    }
+    return cudaErrorInvalidValue;
 }
 
 template <class Step, bool VEC>
@@ -509,21 +570,53 @@ cudaError_t batch_launch(const BatchArgs& a, int sm_count, cudaStream_t stream) 
 
 size_t table_smem_bytes(Res mode, const DevTables& t) {
     switch (mode) {
-        case Res::Private: return table_bytes<StepPrivate>(t);
-        case Res::Shared: return table_bytes<StepShared>(t);
+        case Res::Private: return StepPrivate::supported(t) ? table_bytes<StepPrivate>(t) : SIZE_MAX / 2;
+        case Res::Shared: return StepShared::supported(t) ? table_bytes<StepShared>(t) : SIZE_MAX / 2;
         default: return table_bytes<StepGlobal>(t);
     }
 }
-size_t tma_smem_bytes(Res mode, const DevTables& t) { return TmaShape<1>::kFixed + table_smem_bytes(mode, t); }
 size_t direct_smem_bytes(Res mode, const DevTables& t) { return kDirectRed + 16 + table_smem_bytes(mode, t); }
-uint32_t tma_rows_per_cta() { return TmaShape<1>::R; }
 uint32_t direct_threads_per_cta() { return kDirectWarps * 32; }
 
-cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, cudaStream_t stream) {
+static int Sh_NB_host(int K) { return K == 1 ? Sh_NB<1>() : Sh_NB<2>(); }
+
+// (K, ROWB) candidates in order of preference; the ring takes what is left.
+bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out) {
+    const size_t tb = table_smem_bytes(mode, t);
+    if (tb > smem_optin) return false;
+    static const int cand[][2] = {{1, 32}, {2, 32}, {2, 16}, {1, 16}};
+    const char* env = getenv("SFA_TMA_CONFIG");  // "K,ROWB,ring" (diagnostic sweeps)
+    int fk = 0, fr = 0, fn = 0;
+    if (env) sscanf(env, "%d,%d,%d", &fk, &fr, &fn);
+    for (int pass = 0; pass < 2; ++pass) {
+        for (auto& c : cand) {
+            const int K = c[0], rowb = c[1];
+            if (fk && (K != fk || rowb != fr)) continue;
+            const size_t R = static_cast<size_t>(K) * kNW * 32;
+            const size_t stage = R * rowb;
+            const size_t fixed = (((K * kNW + 2) * 32 + 15) & ~15u) + 16 + 2 * kMaxRing * 8 + 128;
+            if (tb + fixed + 2 * stage > smem_optin) continue;
+            uint32_t ring = static_cast<uint32_t>(std::min<size_t>(kMaxRing, (smem_optin - tb - fixed) / stage));
+            if (fn) ring = std::min<uint32_t>(ring, static_cast<uint32_t>(fn));
+            if (pass == 0 && ring < 3 && !fk) continue;
+            out->K = K;
+            out->rowb = rowb;
+            out->nring = ring;
+            out->rows_per_cta = static_cast<uint32_t>(R);
+            out->nb = Sh_NB_host(K);
+            // prefetch about 256 KiB of each SM's rows ahead of the loads
+            out->pf_lines = static_cast<uint32_t>(std::max<size_t>(1, (256u << 10) / (R * kLine)));
+            return true;
+        }
+    }
+    return false;
+}
+
+cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
     switch (mode) {
-        case Res::Private: return vec ? tma_launch<StepPrivate, true>(a, stream) : tma_launch<StepPrivate, false>(a, stream);
-        case Res::Shared: return vec ? tma_launch<StepShared, true>(a, stream) : tma_launch<StepShared, false>(a, stream);
-        default: return vec ? tma_launch<StepGlobal, true>(a, stream) : tma_launch<StepGlobal, false>(a, stream);
+        case Res::Private: return vec ? tma_launch<StepPrivate, true>(a, cfg, stream) : tma_launch<StepPrivate, false>(a, cfg, stream);
+        case Res::Shared: return vec ? tma_launch<StepShared, true>(a, cfg, stream) : tma_launch<StepShared, false>(a, cfg, stream);
+        default: return vec ? tma_launch<StepGlobal, true>(a, cfg, stream) : tma_launch<StepGlobal, false>(a, cfg, stream);
     }
 }
 

@@ -48,13 +48,22 @@ struct BatchArgs {
     sfa_result* results;   // count
 };
 
-size_t tma_smem_bytes(Res mode, const DevTables& t);
-size_t direct_smem_bytes(Res mode, const DevTables& t);
-size_t table_smem_bytes(Res mode, const DevTables& t);
-uint32_t tma_rows_per_cta();
-uint32_t direct_threads_per_cta();
+// Shape of a k_scan_tma launch: K chunks per compute thread, ROWB bytes of
+// every row per pipeline stage, nring stages in the smem ring, L2 prefetch
+// distance in 256-byte lines.
+struct TmaConfig {
+    int K = 1, rowb = 16;
+    uint32_t nring = 2, rows_per_cta = 0, pf_lines = 1;
+    uint32_t nb = 4;   // TMA boxes per stage: rows_per_cta of a launch must be a multiple
+};
 
-cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, cudaStream_t stream);
+size_t direct_smem_bytes(Res mode, const DevTables& t);
+size_t table_smem_bytes(Res mode, const DevTables& t);   // SIZE_MAX/2 if the layout cannot hold t
+uint32_t direct_threads_per_cta();
+// false if `mode` cannot run the TMA scan within smem_optin bytes
+bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out);
+
+cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);
 cudaError_t launch_batch(Res mode, bool vec, const BatchArgs& a, int sm_count, cudaStream_t stream);
 

@@ -33,15 +33,18 @@ struct Scratch {
 };
 
 // Single-text scan through the TMA pipeline.  The text [0, n) is cut into
-//   head  [0, head)                           < 16 bytes, up to 16-B alignment
-//   rows  [head + r*L, head + (r+1)*L), r < nchunks   (the 2-D TMA tensor)
-//   tail  [tail_start, n)                     < L + 16 bytes
+//   head  [0, head)                           < 256 bytes, up to 256-B alignment
+//   rows  [head + r*L, head + (r+1)*L), r < nchunks   (the 2-D TMA tensor;
+//         L a multiple of 256, so each row's 256-B L2 lines are whole)
+//   tail  [tail_start, n)                     < L bytes
+// CTA b runs rows [b*rows_per_cta, (b+1)*rows_per_cta).
 // Every piece is a chunk of Alg. 5 (any division, Theorem 3).
 struct TmaPlan {
     uint64_t head = 0;
     uint64_t L = 0;           // row length, multiple of 16
     uint32_t nchunks = 0;     // rows
     uint32_t ctas = 0;
+    uint32_t rows_per_cta = 0;
     uint64_t tail_start = 0;  // head + nchunks * L
 };
 

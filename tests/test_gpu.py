@@ -315,3 +315,21 @@ def test_match_host_replay_mode(torch_cuda):
     d3 = oracle_pair(rx, None)
     t3 = W.cfg3_text(130 << 20, plant=True)
     assert sfa3.match_host(t3) == d3.run(t3)
+
+
+# --------------------------------------------------------------------------- every TMA pipeline shape
+@pytest.mark.parametrize("shape", ["1,16,0", "1,32,0", "2,16,0", "2,32,0", "1,16,2", "2,16,2", "1,32,3"])
+def test_every_tma_shape(torch_cuda, shape, monkeypatch):
+    """k_scan_tma for each (K chunks/thread, bytes/row/stage, ring depth) the
+    launcher can pick (SFA_TMA_CONFIG forces one), on texts spanning several
+    rows per thread and ragged tails."""
+    torch = torch_cuda
+    monkeypatch.setenv("SFA_TMA_CONFIG", shape)
+    for rx, alpha, text in [(*CFG2, W.cfg2_accepted(2_000_000)), (*CFG1, W.cfg1_accepted(5_000_000)),
+                            (*CFG4, W.cfg4_text(20_000_000))]:
+        d = oracle_pair(rx, alpha)
+        sfa = P.SFA(rx, alpha)
+        for n in (text.size, text.size - 1, 4_200_001, 9_999_937):
+            t = text[:n]
+            for pad in (0, 5):
+                check_text(torch, sfa, d, t, pad)
