@@ -73,6 +73,15 @@ typedef enum {
     SFA_RES_L2 = 4             /* whole table from global memory (L2-resident)       */
 } sfa_residency;
 
+/* Composition of chunk states (A3).  AUTO: TABLE when |S| <= 4096, else VEC
+ * when |D| <= 32, else REPLAY. */
+typedef enum {
+    SFA_COMPOSE_AUTO = 0,
+    SFA_COMPOSE_VEC = 1,       /* mapping vectors, one lane per DFA state, warp shuffles (|D| <= 32) */
+    SFA_COMPOSE_TABLE = 2,     /* SFA ids; composition table comp[a][b] built on the host (|S| <= 4096) */
+    SFA_COMPOSE_REPLAY = 3     /* SFA ids; s_a . s_b = delta_s^(s_a, rep(s_b)) (Lemma 1) */
+} sfa_compose;
+
 typedef struct sfa_handle sfa_handle;
 
 /* One result per text: the DFA state q_final (canonical id, C3) and
@@ -92,7 +101,7 @@ typedef struct {
     uint32_t classes;          /* byte classes C (table columns)                 */
     uint32_t sfa_depth;        /* longest shortest word f_I -> f (replay bound)  */
     uint32_t residency;        /* effective sfa_residency for single texts       */
-    uint32_t compose_mode;     /* 0 = vector (|D| <= 32), 1 = replay (Lemma 1)   */
+    uint32_t compose_mode;     /* effective sfa_compose (VEC, TABLE or REPLAY)   */
     uint32_t range_lo, range_width; /* byte window of the PRIVATE layout (0 if n/a) */
     uint64_t device_table_bytes;    /* bytes of SFA tables held on the device    */
     double   dfa_seconds, sfa_seconds; /* host construction times (not the target) */
@@ -172,6 +181,11 @@ SFA_API int sfa_match_chunked(const sfa_handle* h, const uint8_t* d_text, size_t
 
 /* Forces a residency mode (SFA_RES_*); CAPACITY if it does not fit. */
 SFA_API int sfa_set_residency(sfa_handle* h, int mode);
+
+/* Forces a composition mode (SFA_COMPOSE_*); CAPACITY if the handle cannot
+ * use it (VEC needs |D| <= 32, TABLE |S| <= 4096).  Results do not depend on
+ * it (composition is exact); only the epilogue cost does. */
+SFA_API int sfa_set_compose(sfa_handle* h, int mode);
 
 /* Minimal DFA over all 256 bytes: table |D|*256 canonical ids, finals |D| (0/1). */
 SFA_API int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals);

@@ -13,7 +13,7 @@ for device memory and streams.
 
 Functions keep the C names: ``sfa_compile``, ``sfa_match``,
 ``sfa_match_async``, ``sfa_match_batch``, ``sfa_match_host``,
-``sfa_match_chunked``, ``sfa_set_residency``, ``sfa_info``,
+``sfa_match_chunked``, ``sfa_set_residency``, ``sfa_set_compose``, ``sfa_info``,
 ``sfa_export_dfa``, ``sfa_export_sfa``, ``sfa_free``; ``SFA`` wraps a handle.
 """
 from __future__ import annotations
@@ -29,6 +29,8 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libsfa.so")
 SFA_OK, SFA_ERR_SYNTAX, SFA_ERR_UNSUPPORTED, SFA_ERR_CAPACITY, SFA_ERR_INVALID_ARG, SFA_ERR_CUDA, SFA_ERR_OOM = range(7)
 RES_AUTO, RES_SMEM_PRIVATE, RES_SMEM_SHARED, RES_HOT_L2, RES_L2 = range(5)
 RES_NAMES = {0: "auto", 1: "smem_private", 2: "smem_shared", 3: "hot_l2", 4: "l2"}
+COMPOSE_AUTO, COMPOSE_VEC, COMPOSE_TABLE, COMPOSE_REPLAY = range(4)
+COMPOSE_NAMES = {0: "auto", 1: "vec", 2: "table", 3: "replay"}
 _ERR_NAMES = {1: "syntax", 2: "unsupported", 3: "capacity", 4: "invalid argument", 5: "cuda", 6: "out of memory"}
 
 
@@ -53,8 +55,8 @@ class sfa_info_t(C.Structure):
 
 
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
-           "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_export_dfa",
-           "sfa_export_sfa")
+           "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
+           "sfa_export_dfa", "sfa_export_sfa")
 
 _lib = None
 
@@ -78,6 +80,7 @@ def lib() -> C.CDLL:
         L.sfa_match_host.argtypes = [vp, vp, C.c_size_t, vp, u32p, C.POINTER(C.c_int)]
         L.sfa_match_chunked.argtypes = [vp, vp, C.c_size_t, C.c_uint32, vp, u32p, C.POINTER(C.c_int), u32p]
         L.sfa_set_residency.argtypes = [vp, C.c_int]
+        L.sfa_set_compose.argtypes = [vp, C.c_int]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
         for f in EXPORTS:
@@ -190,6 +193,10 @@ def sfa_set_residency(h: int, mode: int):
     _check(lib().sfa_set_residency(h, mode))
 
 
+def sfa_set_compose(h: int, mode: int):
+    _check(lib().sfa_set_compose(h, mode))
+
+
 def sfa_export_dfa(h: int):
     info = sfa_info(h)
     nd = info["dfa_states"]
@@ -250,6 +257,9 @@ class SFA:
 
     def set_residency(self, mode: int):
         sfa_set_residency(self.h, mode)
+
+    def set_compose(self, mode: int):
+        sfa_set_compose(self.h, mode)
 
     def export_dfa(self):
         return sfa_export_dfa(self.h)

@@ -9,6 +9,7 @@ from __future__ import annotations
 import glob
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -17,7 +18,7 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libsfa.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cpp", "compile.cpp", "kernels.cu"]
+SOURCES = ["api.cpp", "compile.cpp", "kernels.cu", "kernels_private.cu", "kernels_shared.cu", "kernels_global.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr"]
 
@@ -33,17 +34,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         newest = max(os.path.getmtime(p) for p in _inputs())
         if os.path.getmtime(LIB) >= newest:
             return LIB
-    objs = []
-    for s in SOURCES:
-        src = os.path.join(CSRC, s)
-        obj = os.path.join(LIBDIR, s + ".o")
+    objs, cmds = [], []
+    for src_name in SOURCES:
+        src = os.path.join(CSRC, src_name)
+        obj = os.path.join(LIBDIR, src_name + f".{os.getpid()}.o")
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
-        if s.endswith(".cu"):
-            cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
+        if src_name.endswith(".cu") and verbose:
+            cmd[1:1] = ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd))
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    # one nvcc per translation unit, in parallel (the kernels are split by step policy)
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"])
     os.replace(tmp, LIB)

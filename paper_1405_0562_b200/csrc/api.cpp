@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -37,6 +39,8 @@ constexpr uint64_t kDirectPiece = 64;          // bytes per thread in k_scan_dir
 constexpr uint32_t kMaxSlots = (1u << 16) + 2; // partial slots (CTAs + tail)
 constexpr uint64_t kSlice = 64ull << 20;       // sfa_match_host slice
 constexpr uint64_t kBatchSeg = 64ull << 10;    // bytes per batch task
+constexpr uint32_t kCompMaxStates = 4096;      // composition table up to |S|^2 = 16M entries
+constexpr size_t kAuxMax = 16u << 10;          // comp / maps32 copied into smem up to this size
 
 template <class T>
 cudaError_t upload(T** dst, const T* src, size_t count) {
@@ -69,6 +73,11 @@ struct sfa_handle {
     uint8_t* dfinal = nullptr;
     uint32_t* drep_off = nullptr;
     uint8_t* drep = nullptr;
+    void* dcomp = nullptr;                    // composition table (u8 if nS <= 256, else u16)
+    uint4* drep16 = nullptr;                  // rep(s) slots (depth <= 15)
+    uint32_t* daux[2] = {nullptr, nullptr};   // aux smem images: [0] comp (TABLE), [1] maps32 (VEC)
+    uint32_t aux_bytes[2] = {0, 0};
+    int compose = SFA_COMPOSE_AUTO;
     uint64_t dev_bytes = 0;
     // scratch
     uint8_t* partials = nullptr;
@@ -92,7 +101,9 @@ struct sfa_handle {
         cudaDeviceSynchronize();
         for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
                         (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
-                        (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1]})
+                        (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1],
+                        (void*)dcomp, (void*)drep16, (void*)daux[0],
+                        (void*)daux[1]})
             if (p) cudaFree(p);
         if (hres) cudaFreeHost(hres);
         for (int i = 0; i < 2; ++i) {
@@ -104,10 +115,32 @@ struct sfa_handle {
         cudaSetDevice(prev);
     }
 
-    bool vec() const { return A.nD <= 32; }
+    bool has_comp() const { return A.nS <= kCompMaxStates; }
+    // effective composition mode
+    int compose_mode() const {
+        if (compose != SFA_COMPOSE_AUTO) return compose;
+        if (has_comp()) return SFA_COMPOSE_TABLE;
+        return A.nD <= 32 ? SFA_COMPOSE_VEC : SFA_COMPOSE_REPLAY;
+    }
+    bool vec() const { return compose_mode() == SFA_COMPOSE_VEC; }
 
-    sfa::DevTables tables() const {
+    // device tables as seen by a kernel (aux = the composition mode's smem image)
+    sfa::DevTables tables(sfa::Res = sfa::Res::Global) const {
         sfa::DevTables t;
+        const int cm = compose_mode();
+        t.comp = cm == SFA_COMPOSE_TABLE ? dcomp : nullptr;
+        t.comp_u8 = A.nS <= 256 ? 1u : 0u;
+        t.rep16 = drep16;
+        if (cm == SFA_COMPOSE_TABLE && daux[0]) {
+            t.aux = daux[0];
+            t.aux_bytes = aux_bytes[0];
+            t.aux_comp = 1;
+        } else if (cm == SFA_COMPOSE_VEC && daux[1]) {
+            t.aux = daux[1];
+            t.aux_bytes = aux_bytes[1];
+            t.aux_maps = 1;
+            t.aux_maps_off = 0;
+        }
         t.T = dT;
         t.cls = dcls;
         t.Trange = dTrange;
@@ -147,7 +180,7 @@ struct sfa_handle {
         CU(upload(&dT, T16.data(), T16.size()));
         CU(upload(&dTrange, R16.data(), R16.size()));
         CU(upload(&dcls, A.cls, 256));
-        if (vec()) {
+        if (nD <= 32) {
             std::vector<uint8_t> m32(static_cast<size_t>(nS) * 32);
             for (uint32_t s = 0; s < nS; ++s)
                 for (uint32_t q = 0; q < 32; ++q)
@@ -159,6 +192,48 @@ struct sfa_handle {
             for (size_t i = 0; i < m16.size(); ++i) m16[i] = static_cast<uint16_t>(A.maps[i]);
             CU(upload(&dmaps16, m16.data(), m16.size()));
             dev_bytes += m16.size() * 2;
+        }
+        // composition table comp[a][b] = id(f_a . f_b) = delta_s^(a, rep(b)) (Lemma 1)
+        if (has_comp()) {
+            const bool u8 = nS <= 256;
+            const size_t cells = static_cast<size_t>(nS) * nS;
+            std::vector<uint16_t> comp(cells);
+            for (uint32_t a = 0; a < nS; ++a)
+                for (uint32_t b = 0; b < nS; ++b) {
+                    uint32_t st = a;
+                    for (uint32_t k = A.rep_off[b]; k < A.rep_off[b + 1]; ++k)
+                        st = A.T[static_cast<size_t>(st) * C + A.cls[A.rep[k]]];
+                    comp[static_cast<size_t>(a) * nS + b] = static_cast<uint16_t>(st);
+                }
+            std::vector<uint8_t> bytes(cells * (u8 ? 1 : 2));
+            for (size_t i = 0; i < cells; ++i) {
+                if (u8) bytes[i] = static_cast<uint8_t>(comp[i]);
+                else std::memcpy(&bytes[2 * i], &comp[i], 2);
+            }
+            bytes.resize((bytes.size() + 15) & ~size_t(15), 0);
+            CU(upload(reinterpret_cast<uint8_t**>(&dcomp), bytes.data(), bytes.size()));
+            dev_bytes += bytes.size();
+            if (bytes.size() <= kAuxMax) {
+                CU(upload(&daux[0], reinterpret_cast<const uint32_t*>(bytes.data()), bytes.size() / 4));
+                aux_bytes[0] = static_cast<uint32_t>(bytes.size());
+            }
+        }
+        if (A.depth <= 15) {  // rep(s) in one 16-byte slot, |rep(s)| in byte 15
+            std::vector<uint8_t> slots(static_cast<size_t>(nS) * 16, 0);
+            for (uint32_t st = 0; st < nS; ++st) {
+                const uint32_t len = A.rep_off[st + 1] - A.rep_off[st];
+                std::memcpy(&slots[static_cast<size_t>(st) * 16], A.rep.data() + A.rep_off[st], len);
+                slots[static_cast<size_t>(st) * 16 + 15] = static_cast<uint8_t>(len);
+            }
+            CU(upload(reinterpret_cast<uint8_t**>(&drep16), slots.data(), slots.size()));
+        }
+        if (nD <= 32 && static_cast<size_t>(nS) * 32 <= kAuxMax) {
+            std::vector<uint8_t> m32(static_cast<size_t>(nS) * 32);
+            for (uint32_t st = 0; st < nS; ++st)
+                for (uint32_t q = 0; q < 32; ++q)
+                    m32[static_cast<size_t>(st) * 32 + q] = static_cast<uint8_t>(q < nD ? A.maps[static_cast<size_t>(st) * nD + q] : q);
+            CU(upload(&daux[1], reinterpret_cast<const uint32_t*>(m32.data()), m32.size() / 4));
+            aux_bytes[1] = static_cast<uint32_t>(m32.size());
         }
         CU(upload(&dimg0, A.img0.data(), A.img0.size()));
         CU(upload(&dfinal, A.dfa_final.data(), A.dfa_final.size()));
@@ -220,7 +295,7 @@ struct sfa_handle {
         cudaError_t e;
         if (direct) {
             sfa::DirectArgs a;
-            a.t = tables();
+            a.t = tables(mode);
             a.text = d_text;
             a.n = n;
             a.npieces = force_pieces ? force_pieces : std::max<uint64_t>(1, (n + kDirectPiece - 1) / kDirectPiece);
@@ -233,16 +308,18 @@ struct sfa_handle {
             e = sfa::launch_scan_direct(mode, vec(), a, stream);
         } else {
             sfa::ScanArgs a;
-            a.t = tables();
+            a.t = tables(mode);
             a.text = d_text;
             a.n = n;
             a.sc = scratch();
             a.q_in = q_in;
             a.result = d_result;
+            a.stamps = nullptr;
             sfa::TmaConfig cfg;
             if (!sfa::tma_choose(mode, a.t, smem_optin, &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
-            // box heights (rows_per_cta / NB) keep every TMA destination 128-B aligned
-            const uint64_t R = cfg.rows_per_cta, NB = cfg.nb * (128 / cfg.rowb), G = static_cast<uint64_t>(sm_count);
+            // box heights (rows_per_cta / nb) are multiples of 8 rows, so every TMA
+            // destination is aligned to its swizzle atom (8 rows x ROWB bytes)
+            const uint64_t R = cfg.rows_per_cta, NB = cfg.nb * 8, G = static_cast<uint64_t>(sm_count);
             uint64_t head = (256 - (reinterpret_cast<uintptr_t>(d_text) & 255)) & 255;
             head = std::min<uint64_t>(head, n);
             const uint64_t body = n - head;
@@ -259,21 +336,50 @@ struct sfa_handle {
             a.plan.ctas = rc ? static_cast<uint32_t>((rows + rc - 1) / rc) : 0;
             a.plan.tail_start = head + rows * L;
             if (rows == 0 || a.plan.ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "bad scan plan");
+            static const bool dbg = getenv("SFA_DEBUG_STAMPS") != nullptr;
+            if (dbg) CU(cudaMallocAsync(&a.stamps, 8 * sizeof(uint64_t) * a.plan.ctas, stream));
             e = sfa::launch_scan_tma(mode, vec(), a, cfg, stream);
+            if (dbg && e == cudaSuccess) {  // diagnostic: per-CTA phase times (ns) to stderr
+                std::vector<uint64_t> st(8ull * a.plan.ctas);
+                CU(cudaMemcpyAsync(st.data(), a.stamps, st.size() * 8, cudaMemcpyDeviceToHost, stream));
+                CU(cudaStreamSynchronize(stream));
+                CU(cudaFree(a.stamps));
+                uint64_t t0 = UINT64_MAX, tend = 0;
+                double ph[4] = {0, 0, 0, 0};
+                for (uint32_t b = 0; b < a.plan.ctas; ++b) t0 = std::min(t0, st[8 * b]);
+                for (uint32_t b = 0; b < a.plan.ctas; ++b) {
+                    for (int k = 0; k < 4; ++k) ph[k] += double(st[8 * b + k + 1] - st[8 * b + k]) / a.plan.ctas;
+                    tend = std::max(tend, st[8 * b + 4]);
+                }
+                uint64_t smax = 0;
+                for (uint32_t b = 0; b < a.plan.ctas; ++b) smax = std::max(smax, st[8 * b] - t0);
+                fprintf(stderr, "stamps: ctas=%u start-spread=%.2fus tables=%.2fus scan=%.2fus blockfold=%.2fus epi=%.2fus total=%.2fus L=%llu rc=%u\n",
+                        a.plan.ctas, smax / 1e3, ph[0] / 1e3, ph[1] / 1e3, ph[2] / 1e3, ph[3] / 1e3, (tend - t0) / 1e3,
+                        (unsigned long long)a.plan.L, a.plan.rows_per_cta);
+            }
         }
         if (e != cudaSuccess) return cuda_fail(e, "scan launch");
         return SFA_OK;
     }
 
-    // serialise the shared scratch across streams
+    // Serialise the shared scratch across streams.  Launches on the stream of
+    // the previous call are ordered by the stream itself (and may overlap
+    // through PDL, the kernels wait before touching scratch); a different
+    // stream first waits for everything enqueued on the previous one.
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
     int begin(cudaStream_t stream) {
         int rc = ensure_uploaded();
         if (rc) return rc;
-        CU(cudaStreamWaitEvent(stream, ev_done, 0));
+        if (has_last && stream != last_stream) {
+            CU(cudaEventRecord(ev_done, last_stream));
+            CU(cudaStreamWaitEvent(stream, ev_done, 0));
+        }
         return SFA_OK;
     }
     int end(cudaStream_t stream) {
-        CU(cudaEventRecord(ev_done, stream));
+        last_stream = stream;
+        has_last = true;
         return SFA_OK;
     }
 };
@@ -337,7 +443,7 @@ int sfa_info(const sfa_handle* h, sfa_info_t* info) {
     info->sfa_states = A.nS;
     info->classes = A.C;
     info->sfa_depth = A.depth;
-    info->compose_mode = h->vec() ? 0 : 1;
+    info->compose_mode = static_cast<uint32_t>(h->compose_mode());
     info->range_lo = h->lo;
     info->range_width = h->W;
     info->residency = 0;
@@ -367,6 +473,16 @@ int sfa_set_residency(sfa_handle* h, int mode) {
     rc = h->resolve(1, &m);
     if (rc) h->forced = prev;
     return rc;
+}
+
+int sfa_set_compose(sfa_handle* h, int mode) {
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (mode < SFA_COMPOSE_AUTO || mode > SFA_COMPOSE_REPLAY) return fail(SFA_ERR_INVALID_ARG, "bad compose mode");
+    if (mode == SFA_COMPOSE_VEC && h->A.nD > 32) return fail(SFA_ERR_CAPACITY, "VEC composition needs |D| <= 32");
+    if (mode == SFA_COMPOSE_TABLE && !h->has_comp()) return fail(SFA_ERR_CAPACITY, "composition table needs |S| <= 4096");
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->compose = mode;
+    return SFA_OK;
 }
 
 int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals) {
@@ -512,7 +628,7 @@ int sfa_match_batch(const sfa_handle* hc, const uint8_t* d_texts, const uint64_t
         h->seg_cap = need;
     }
     sfa::BatchArgs a;
-    a.t = h->tables();
+    a.t = h->tables(mode);
     a.texts = d_texts;
     a.off = d_offsets;
     a.count = count;

@@ -16,7 +16,9 @@
 //                VIADDMNMX + LEA + LDS (random banks: conflicts possible).
 //   StepGlobal   the u16 window table read through L1/L2 (any |S|).
 //
-// Interface:  init(lane) -> state of f_I;  step(state, byte) -> state;
+// Interface:  fill(t, tid, nthreads)  builds the smem table from t.Trange;
+//             params(t)  per-thread constants;
+//             init(lane) -> state of f_I;  step(state, byte) -> state;
 //             id(state, lane) -> SFA id;   from_id(id, lane) -> state.
 #pragma once
 
@@ -94,11 +96,30 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
-// TMA: 2-D tile global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t bar, int x, int y) {
+// TMA: 2-D tile global -> shared, completion counted on an mbarrier; `policy`
+// is an L2 cache policy (createpolicy), evict-first for the streamed text so
+// the table images stay L2-resident across launches.
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t bar, int x, int y,
+                                            uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-        ::"r"(dst), "l"(tmap), "r"(bar), "r"(x), "r"(y) : "memory");
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;"
+        ::"r"(dst), "l"(tmap), "r"(bar), "r"(x), "r"(y), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Programmatic dependent launch: let the next kernel of the stream start its
+// prologue now / wait until the previous kernel of the stream has completed
+// (and its memory is visible) before touching shared scratch.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// 1-D bulk copy global -> shared (bytes a multiple of 16), completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int x, int y) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tmap), "r"(x), "r"(y) : "memory");
@@ -116,6 +137,11 @@ __device__ __forceinline__ void bar_compute(uint32_t nthreads) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 constexpr unsigned kFull = 0xffffffffu;
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // column of a byte in the window table: min(byte - lo (mod 2^32), W - 1)
 __device__ __forceinline__ uint32_t window_col(uint32_t byte, uint32_t neg_lo, uint32_t wmax) {
@@ -136,23 +162,36 @@ struct StepPrivate {
     static __host__ __device__ uint32_t col_bytes(const DevTables& t) { return 128u * ((t.nS + 1) / 2); }
     static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.W) * col_bytes(t); }
     static __host__ __device__ bool supported(const DevTables& t) { return t.nS <= 1024; }
-    static __device__ __forceinline__ uint32_t enc(uint32_t s, uint32_t L) { return (s >> 1) * 128u + 4u * L + 2u * (s & 1u); }
+    static __host__ __device__ __forceinline__ uint32_t enc(uint32_t s, uint32_t L) { return (s >> 1) * 128u + 4u * L + 2u * (s & 1u); }
 
-    // the table must be at dsmem offset 0 (smem == dsmem)
-    __device__ void setup(const DevTables& t, uint8_t* smem, int tid, int nthreads) {
+    // Expands the compact window table t.Trange [nS x W] (global) into the 32
+    // bank-private copies: cell (s, j) of lane L is the u16 at
+    // j*X + (s>>1)*128 + 4L + 2(s&1).  Each warp reads 32 consecutive cells
+    // with one coalesced load per lane, then broadcasts them with shuffles and
+    // every lane writes its own copy.  Generic stores (see k_scan_tma: they
+    // keep the smem base foldable into the hot loop's LDS).
+    __device__ static void fill(const DevTables& t, int tid, int nthreads) {
+        const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5;
+        const uint32_t X = col_bytes(t), total = t.nS * t.W;
+        for (uint32_t base = w * 32; base < total; base += nw * 32) {
+            const uint32_t v = base + L < total ? __ldg(t.Trange + base + L) : 0u;
+            uint32_t s = base / t.W, j = base - s * t.W;
+            const uint32_t cnt = min(32u, total - base);
+            for (uint32_t i = 0; i < cnt; ++i) {
+                const uint32_t x = __shfl_sync(kFull, v, i);
+                *reinterpret_cast<uint16_t*>(dsmem + j * X + (s >> 1) * 128u + 4u * L + 2u * (s & 1u)) =
+                    static_cast<uint16_t>(enc(x, L));
+                if (++j == t.W) {
+                    j = 0;
+                    ++s;
+                }
+            }
+        }
+    }
+    __device__ void params(const DevTables& t) {
         X = col_bytes(t);
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
-        uint32_t* tbl = reinterpret_cast<uint32_t*>(smem);
-        const uint32_t words_per_col = X / 4, total = t.W * words_per_col;
-        for (uint32_t i = tid; i < total; i += nthreads) {
-            const uint32_t j = i / words_per_col, rem = i - j * words_per_col;
-            const uint32_t pair = rem >> 5, L = rem & 31;
-            const uint32_t s0 = 2 * pair, s1 = s0 + 1;
-            const uint32_t v0 = enc(t.Trange[s0 * t.W + j], L);
-            const uint32_t v1 = s1 < t.nS ? enc(t.Trange[s1 * t.W + j], L) : 0u;
-            tbl[i] = v0 | (v1 << 16);
-        }
     }
     __device__ __forceinline__ uint32_t init(uint32_t lane) const { return 4u * lane; }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
@@ -170,14 +209,16 @@ struct StepShared {
 
     static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.nS) * t.W * 4; }
     static __host__ __device__ bool supported(const DevTables& t) { return static_cast<uint64_t>(t.nS) * t.W * 4 < (1u << 24); }
-    // the table must be at dsmem offset 0 (smem == dsmem)
-    __device__ void setup(const DevTables& t, uint8_t* smem, int tid, int nthreads) {
+    __device__ static void fill(const DevTables& t, int tid, int nthreads) {
+        uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
+        const uint32_t row = 4 * t.W, total = t.nS * t.W;
+#pragma unroll 4
+        for (uint32_t i = tid; i < total; i += nthreads) tbl[i] = static_cast<uint32_t>(__ldg(t.Trange + i)) * row;
+    }
+    __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
         row = 4 * t.W;
-        uint32_t* T32 = reinterpret_cast<uint32_t*>(smem);
-        const uint32_t total = t.nS * t.W;
-        for (uint32_t i = tid; i < total; i += nthreads) T32[i] = static_cast<uint32_t>(t.Trange[i]) * row;
     }
     __device__ __forceinline__ uint32_t init(uint32_t) const { return 0; }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
@@ -195,7 +236,8 @@ struct StepGlobal {
 
     static __host__ __device__ size_t smem_bytes(const DevTables&) { return 0; }
     static __host__ __device__ bool supported(const DevTables&) { return true; }
-    __device__ void setup(const DevTables& t, uint8_t*, int, int) {
+    __device__ static void fill(const DevTables&, int, int) {}
+    __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
         W = t.W;
@@ -209,6 +251,21 @@ struct StepGlobal {
     __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return st / W; }
     __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return s * W; }
 };
+
+// Cooperative global -> smem copy of n16 16-byte words, 4 loads in flight per
+// thread before their stores.
+__device__ __forceinline__ void copy16(uint4* dst, const uint4* src, size_t n16, int tid, int nthreads) {
+    size_t i = tid;
+    for (; i + 3 * nthreads < n16; i += 4 * nthreads) {
+        const uint4 a = __ldg(src + i), b = __ldg(src + i + nthreads), c = __ldg(src + i + 2 * nthreads),
+                    d = __ldg(src + i + 3 * nthreads);
+        dst[i] = a;
+        dst[i + nthreads] = b;
+        dst[i + 2 * nthreads] = c;
+        dst[i + 3 * nthreads] = d;
+    }
+    for (; i < n16; i += nthreads) dst[i] = __ldg(src + i);
+}
 
 // 4 text bytes of one word, in text order (little-endian)
 template <class Step>
@@ -260,7 +317,7 @@ __device__ __forceinline__ uint32_t vec_fold_ids(const uint8_t* __restrict__ map
 #pragma unroll 8
     for (int l = 0; l < 32; ++l) {
         uint32_t s = __shfl_sync(kFull, s_lane, l);
-        g = __ldg(maps32 + s * 32 + g);
+        g = maps32[s * 32 + g];  // smem copy when small (DevTables::aux), else global
     }
     return g;
 }
@@ -270,6 +327,15 @@ __device__ __forceinline__ uint32_t vec_fold_ids(const uint8_t* __restrict__ map
 template <class Step>
 __device__ __forceinline__ uint32_t replay(const Step& S, const DevTables& t, uint32_t sa, uint32_t sb, uint32_t lane) {
     uint32_t st = S.from_id(sa, lane);
+    if (t.rep16) {  // depth <= 15: the word in one 16-byte slot, its length in byte 15
+        const uint4 w = __ldg(t.rep16 + sb);
+        const uint32_t len = w.w >> 24;
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (uint32_t k = 0; k < 15; ++k)
+            if (k < len) st = S.step(st, (ws[k >> 2] >> (8 * (k & 3))) & 0xffu);
+        return S.id(st, lane);
+    }
     const uint32_t e = t.rep_off[sb + 1];
     for (uint32_t k = t.rep_off[sb]; k < e; ++k) st = S.step(st, t.rep[k]);
     return S.id(st, lane);

@@ -1,20 +1,6 @@
-// kernels.cu -- sm_100a kernels of the SFA hot path (Alg. 5).
-//
-//   k_scan_tma     one long text.  One CTA per SM: kNW compute warps + 1 TMA
-//                  producer warp.  The 16-aligned body of the text is viewed as
-//                  a 2-D tensor [nchunks rows x L bytes]; every stage the
-//                  producer loads a 16-byte column slice of all of the CTA's
-//                  rows (TMA 2-D boxes, mbarrier ring), each compute thread owns
-//                  K rows (= K chunks of Alg. 5 lines 1-5, interleaved for ILP),
-//                  so every byte of HBM is read once and the smem reads of the
-//                  staged text are conflict-free.  Chunk states are composed
-//                  warp -> block -> grid (line 6); the last CTA to finish folds
-//                  the per-CTA partials (plus the head piece) and finalises
-//                  (line 7).  The last CTA also runs the ragged tail.
-//   k_scan_direct  small texts and the forced-chunking test knob: one piece
-//                  per thread (SPEC's chunk rule), same composition tree.
-//   k_batch_*      many texts (A5): a device-side plan, a work-stealing scan
-//                  over (text, segment) tasks and a per-text combine.
+// kernels.cu -- host side of the kernel layer: table sizes and images, the
+// TMA shape choice, and dispatch to the per-step launchers
+// (kernels_private.cu / kernels_shared.cu / kernels_global.cu).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -25,554 +11,15 @@
 
 #include "device.cuh"
 #include "kernels.hpp"
+#include "kernels_impl.cuh"
 
 namespace sfa {
 
-template <class Step>
-__host__ __device__ size_t table_bytes(const DevTables& t) {
-    return (Step::smem_bytes(t) + 15) & ~size_t(15);
-}
-
-// ------------------------------------------------------------------------------------------
-// Composition policy: vector form (|D| <= 32) or replay form (any |D|).
-// A "value" is one uint32 per lane: the lane's entry of the mapping vector
-// (VEC) or an SFA id replicated in every lane (replay).
-// ------------------------------------------------------------------------------------------
-template <class Step, bool VEC>
-struct Comp;
-
-template <class Step>
-struct Comp<Step, true> {
-    static constexpr int kSlot = 32;  // bytes per stored value
-    __device__ static uint32_t identity() { return lane_id(); }
-    __device__ static uint32_t fold_states(const Step&, const DevTables& t, uint32_t s) { return vec_fold_ids(t.maps32, s); }
-    __device__ static uint32_t combine(const Step&, const DevTables&, uint32_t a, uint32_t b) { return vec_compose(a, b); }
-    __device__ static void store(uint8_t* slot, uint32_t v) { slot[lane_id()] = static_cast<uint8_t>(v); }
-    __device__ static uint32_t load(const uint8_t* slot) { return slot[lane_id()]; }
-    __device__ static uint32_t load_global(const uint8_t* p) { return __ldcg(p + lane_id()); }
-    // fold `count` stored values in order into acc
-    __device__ static uint32_t fold_slots(const Step& S, const DevTables& t, const uint8_t* base, uint32_t count,
-                                          uint32_t acc, bool global) {
-        for (uint32_t u = 0; u < count; ++u) {
-            uint32_t v = global ? load_global(base + u * kSlot) : load(base + u * kSlot);
-            acc = combine(S, t, acc, v);
-        }
-        return acc;
-    }
-    // f_fin(q): lane q holds f_fin(q)
-    __device__ static uint32_t q_final(const DevTables&, uint32_t v, uint32_t q) { return __shfl_sync(kFull, v, q); }
-};
-
-template <class Step>
-struct Comp<Step, false> {
-    static constexpr int kSlot = 4;
-    __device__ static uint32_t identity() { return 0; }
-    __device__ static uint32_t fold_states(const Step& S, const DevTables& t, uint32_t s) {
-        return __shfl_sync(kFull, replay_fold(S, t, s), 0);
-    }
-    __device__ static uint32_t combine(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
-        return replay(S, t, a, b, lane_id());
-    }
-    __device__ static void store(uint8_t* slot, uint32_t v) {
-        if (lane_id() == 0) *reinterpret_cast<uint32_t*>(slot) = v;
-    }
-    __device__ static uint32_t load(const uint8_t* slot) { return *reinterpret_cast<const uint32_t*>(slot); }
-    __device__ static uint32_t fold_slots(const Step& S, const DevTables& t, const uint8_t* base, uint32_t count,
-                                          uint32_t acc, bool global) {
-        for (uint32_t c0 = 0; c0 < count; c0 += 32) {
-            uint32_t u = c0 + lane_id();
-            uint32_t x = 0;
-            if (u < count)
-                x = global ? __ldcg(reinterpret_cast<const unsigned int*>(base) + u)
-                           : reinterpret_cast<const uint32_t*>(base)[u];
-            uint32_t r = fold_states(S, t, x);
-            acc = combine(S, t, acc, r);
-        }
-        return acc;
-    }
-    __device__ static uint32_t q_final(const DevTables& t, uint32_t v, uint32_t q) {
-        return q == 0 ? t.img0[v] : t.maps16[static_cast<uint64_t>(v) * t.nD + q];
-    }
-};
-
-// ------------------------------------------------------------------------------------------
-// Grid-level epilogue shared by the scan kernels.  Every CTA has stored its
-// partial value at partials[blockIdx.x] (slots [gridDim.x, nslots) hold extra
-// pieces, e.g. the tail); the last CTA to arrive folds
-//     head . partials[0] . ... . partials[nslots-1]
-// in order and writes q_final = f_fin(q_in) and accept (Alg. 5 lines 6-7).
-//   warps [0, nwarps-1)  fold contiguous ranges of the partials
-//   warp  nwarps-1       the head piece [0, head) (one lane)
-// ------------------------------------------------------------------------------------------
-template <class Step, bool VEC>
-__device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& sc, sfa_result* result,
-                              const uint8_t* text, uint64_t head, uint32_t nslots, const uint32_t* q_in,
-                              int nwarps, uint8_t* red, uint32_t* flag) {
-    using CP = Comp<Step, VEC>;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nthreads = nwarps * 32;
-    if (warp == 0) {
-        __threadfence();
-        if (lane == 0) *flag = (atomicAdd(sc.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-    }
-    bar_compute(nthreads);
-    if (*flag == 0) return;
-    __threadfence();  // acquire the other CTAs' partials
-    const int nfold = nwarps - 1;
-    const uint32_t per = (nslots + nfold - 1) / nfold;
-    uint8_t* slot_head = red + nfold * CP::kSlot;
-    if (warp < nfold) {
-        uint32_t b0 = min(nslots, warp * per), b1 = min(nslots, b0 + per);
-        uint32_t acc = CP::fold_slots(S, t, sc.partials + b0 * CP::kSlot, b1 - b0, CP::identity(), true);
-        CP::store(red + warp * CP::kSlot, acc);
-    } else {  // head [0, head), split over the 32 lanes
-        const uint64_t per = (head + 31) / 32;
-        const uint64_t h0 = min(head, lane * per), h1 = min(head, h0 + per);
-        const uint32_t s = S.id(run_range(S, S.init(lane), text, h0, h1), lane);
-        CP::store(slot_head, CP::fold_states(S, t, s));
-    }
-    bar_compute(nthreads);
-    if (warp == 0) {
-        uint32_t acc = CP::load(slot_head);
-        acc = CP::fold_slots(S, t, red, nfold, acc, false);
-        const uint32_t q0 = q_in ? *q_in : 0u;
-        const uint32_t q = CP::q_final(t, acc, q0);
-        if (lane == 0) {
-            result->final_state = q;
-            result->accept = t.dfinal[q];
-            *sc.ticket = 0;  // ready for the next launch (stream-ordered)
-        }
-    }
-}
-
-// Fold one state per thread of `nwarps` warps, in thread order, into a CTA
-// value; valid in warp 0 (all lanes).  Uses red[0 .. nwarps) slots.
-template <class Step, bool VEC>
-__device__ uint32_t block_fold(const Step& S, const DevTables& t, uint32_t s, int nwarps, uint8_t* red) {
-    using CP = Comp<Step, VEC>;
-    const int warp = threadIdx.x >> 5;
-    CP::store(red + warp * CP::kSlot, CP::fold_states(S, t, s));
-    bar_compute(nwarps * 32);
-    uint32_t acc = CP::identity();
-    if (warp == 0) acc = CP::fold_slots(S, t, red, nwarps, acc, false);
-    bar_compute(nwarps * 32);
-    return acc;
-}
-
-template <bool VEC>
-__device__ __forceinline__ void store_partial(uint8_t* partials, uint32_t slot, uint32_t acc) {
-    if (VEC) partials[slot * 32 + lane_id()] = static_cast<uint8_t>(acc);
-    else if (lane_id() == 0) reinterpret_cast<uint32_t*>(partials)[slot] = acc;
-}
-
-// ------------------------------------------------------------------------------------------
-// k_scan_tma
-//
-// Shared memory (dynamic):  [table | red slots | flag | mbarriers | stage ring]
-// The table is first so its base is an immediate of every LDS.  A stage holds
-// ROWB bytes of each of the CTA's R rows (row-major, ROWB per row), loaded by
-// NB 2-D TMA boxes of [ROWB x BR]; the ring depth is chosen at launch from the
-// shared memory left after the table.  The producer also prefetches each
-// row's next 256-byte line into L2 once (a second tensor map with 256-B boxes)
-// so the TMA loads hit L2.
-// ------------------------------------------------------------------------------------------
-constexpr int kNW = 31;        // compute warps
-constexpr int kMaxRing = 8;    // max smem ring depth
-constexpr int kLine = 256;     // L2 prefetch granularity (bytes of a row)
-
-template <int K>
-__host__ __device__ constexpr int Sh_NB() { return (K * kNW * 32 + 255) / 256; }
-
-template <int K, int ROWB>
-struct TmaShape {
-    static constexpr int R = K * kNW * 32;            // rows (chunks) per CTA
-    static constexpr int NB = (R + 255) / 256;        // TMA boxes per stage (box dim <= 256)
-    static constexpr int BR = R / NB;                 // rows per box
-    static_assert(R % NB == 0, "rows must split evenly into boxes");
-    static_assert(ROWB % 16 == 0 && kLine % ROWB == 0, "row slice must be 16-B granular");
-    static constexpr uint32_t kStageBytes = R * ROWB;
-    static constexpr uint32_t kRedBytes = ((K * kNW + 2) * 32 + 15) & ~15u;
-    // bytes besides the table and the ring
-    static constexpr uint32_t kFixed = kRedBytes + 16 + 2 * kMaxRing * 8 + 128;
-};
-
-struct TmaMaps {
-    CUtensorMap load;      // box [ROWB x BR]
-    CUtensorMap pref;      // box [256 x BR], L2 prefetch only
-};
-
-template <class Step, int K, int ROWB, bool VEC>
-__global__ void __launch_bounds__((kNW + 1) * 32, 1)
-k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_t tbl_bytes, const uint32_t nring,
-           const uint32_t pf_lines) {
-    // rows of this CTA: [blockIdx.x * rc, +rc), loaded as NB boxes of br rows
-    const uint32_t rc = a.plan.rows_per_cta, br = rc / Sh_NB<K>();
-    using Sh = TmaShape<K, ROWB>;
-    using CP = Comp<Step, VEC>;
-    uint8_t* smem = dsmem;
-    uint8_t* tbl = smem;
-    uint8_t* red = smem + ((tbl_bytes + 15) & ~15u);
-    uint32_t* flag = reinterpret_cast<uint32_t*>(red + Sh::kRedBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + Sh::kRedBytes + 16);
-    const uint32_t ring0 = (smem_u32(bars + 2 * kMaxRing) + 127) & ~127u;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nstages = static_cast<uint32_t>(a.plan.L / ROWB);
-    const uint32_t full0 = smem_u32(bars), empty0 = full0 + kMaxRing * 8;
-    if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < nring; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, kNW);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-
-    if (warp == kNW) {  // ---- TMA producer ----
-        if (lane == 0) {
-            prefetch_tmap(&maps.load);
-            prefetch_tmap(&maps.pref);
-            const int y0 = blockIdx.x * rc;
-            const uint32_t nlines = static_cast<uint32_t>((a.plan.L + kLine - 1) / kLine);
-            for (uint32_t l = 0; l <= pf_lines && l < nlines; ++l)
-                for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&maps.pref, l * kLine, y0 + j * br);
-            constexpr uint32_t kStagesPerLine = kLine / ROWB;
-            uint32_t slot = 0, phase = 0;
-            for (uint32_t i = 0; i < nstages; ++i) {
-                if (i >= nring) mbar_wait(empty0 + 8 * slot, phase ^ 1);
-                mbar_expect_tx(full0 + 8 * slot, rc * ROWB);
-                const uint32_t dst = ring0 + slot * Sh::kStageBytes;
-                for (int j = 0; j < Sh::NB; ++j)
-                    tma_load_2d(dst + j * br * ROWB, &maps.load, full0 + 8 * slot, i * ROWB, y0 + j * br);
-                if (i % kStagesPerLine == 0) {  // entering line l: prefetch line l + pf_lines + 1
-                    const uint32_t l = i / kStagesPerLine + pf_lines + 1;
-                    if (l < nlines)
-                        for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&maps.pref, l * kLine, y0 + j * br);
-                }
-                if (++slot == nring) {
-                    slot = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-        return;
-    }
-
-    // ---- compute warps ----
-    Step S;
-    S.setup(a.t, tbl, threadIdx.x, kNW * 32);
-    bar_compute(kNW * 32);
-
-    // The last CTA also runs the ragged tail [tail_start, n) (< L + 16 bytes),
-    // split over its compute threads; its value goes to slot gridDim.x.
-    if (blockIdx.x == gridDim.x - 1) {
-        const uint64_t len = a.n - a.plan.tail_start;
-        const uint64_t per = (len + kNW * 32 - 1) / (kNW * 32);
-        const uint64_t p0 = min(a.n, a.plan.tail_start + threadIdx.x * per), p1 = min(a.n, p0 + per);
-        const uint32_t s = S.id(run_range(S, S.init(lane), a.text, p0, p1), lane);
-        const uint32_t acc = block_fold<Step, VEC>(S, a.t, s, kNW, red);
-        if (warp == 0) store_partial<VEC>(a.sc.partials, gridDim.x, acc);
-    }
-
-    uint32_t st[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) st[k] = S.init(lane);
-    const uint32_t row0 = warp * 32 + lane;
-    uint32_t rsrc[K];  // stage offset of each of this thread's rows (row 0 for idle threads)
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t r = k * kNW * 32 + row0;
-        rsrc[k] = (r < rc ? r : 0u) * ROWB;
-    }
-    uint32_t slot = 0, phase = 0;
-    for (uint32_t i = 0; i < nstages; ++i) {
-        mbar_wait(full0 + 8 * slot, phase);
-        const uint32_t src = ring0 + slot * Sh::kStageBytes;
-        uint4 v[K][ROWB / 16];
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-            for (int c = 0; c < ROWB / 16; ++c) v[k][c] = lds_v4(src + rsrc[k] + c * 16);
-#pragma unroll
-        for (int c = 0; c < ROWB / 16; ++c) {
-            const uint32_t* w[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) w[k] = reinterpret_cast<const uint32_t*>(&v[k][c]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<0>(w[k][q]));
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<1>(w[k][q]));
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<2>(w[k][q]));
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
-            }
-        }
-        // Release the slot only now: every lane has consumed its loaded bytes,
-        // so no LDS of this stage can still be in flight when the producer's
-        // next TMA write lands (an arrive right after issuing the LDS raced).
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * slot);
-        if (++slot == nring) {
-            slot = 0;
-            phase ^= 1;
-        }
-    }
-
-    // ---- composition: warp -> block (rows are ordered k-major, then warp, then lane) ----
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint32_t r = k * kNW * 32 + row0;
-        const uint32_t row = blockIdx.x * rc + r;
-        const uint32_t s = (r < rc && row < a.plan.nchunks) ? S.id(st[k], lane) : 0u;  // rows past the text: f_I
-        CP::store(red + (k * kNW + warp) * CP::kSlot, CP::fold_states(S, a.t, s));
-    }
-    bar_compute(kNW * 32);
-    if (warp == 0) {
-        uint32_t acc = CP::fold_slots(S, a.t, red, K * kNW, CP::identity(), false);
-        store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
-    }
-    bar_compute(kNW * 32);
-    grid_epilogue<Step, VEC>(S, a.t, a.sc, a.result, a.text, a.plan.head, gridDim.x + 1, a.q_in, kNW, red, flag);
-}
-
-// ------------------------------------------------------------------------------------------
-// k_scan_direct: piece g = [start(g), start(g+1)) by SPEC's rule (C6).
-// ------------------------------------------------------------------------------------------
-constexpr int kDirectWarps = 8;
-constexpr uint32_t kDirectRed = ((kDirectWarps + 2) * 32 + 15) & ~15u;
-
-__device__ __forceinline__ uint64_t piece_start(uint64_t g, uint64_t n, uint64_t p) {
-    const uint64_t q = n / p, r = n % p;
-    return g * q + (g < r ? g : r);
-}
-
-template <class Step, bool VEC>
-__global__ void __launch_bounds__(kDirectWarps * 32)
-k_scan_direct(const DirectArgs a) {
-    uint8_t* tbl = dsmem;  // table at offset 0
-    uint8_t* red = dsmem + ((table_bytes<Step>(a.t) + 15) & ~size_t(15));
-    uint32_t* flag = reinterpret_cast<uint32_t*>(red + kDirectRed);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Step S;
-    S.setup(a.t, tbl, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    uint32_t s = 0;
-    if (g < a.npieces) {
-        uint64_t b0 = piece_start(g, a.n, a.npieces), b1 = piece_start(g + 1, a.n, a.npieces);
-        s = S.id(run_range(S, S.init(lane), a.text, b0, b1), lane);
-        if (a.piece_ids) a.piece_ids[g] = s;
-    }
-    const uint32_t acc = block_fold<Step, VEC>(S, a.t, s, kDirectWarps, red);
-    if (warp == 0) store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
-    bar_compute(kDirectWarps * 32);
-    grid_epilogue<Step, VEC>(S, a.t, a.sc, a.result, a.text, 0, gridDim.x, a.q_in, kDirectWarps, red, flag);
-}
-
-// ------------------------------------------------------------------------------------------
-// Batch (A5).  Text i = texts[off[i], off[i+1]) is cut into segments of at most
-// seg bytes; a task is one segment, run by one warp (32 lane pieces).
-// ------------------------------------------------------------------------------------------
-constexpr int kBatchWarps = 16;
-
-// task_off[i] = number of tasks of texts < i (exclusive prefix), task_off[count] = total.
-__global__ void __launch_bounds__(1024) k_batch_plan(const uint64_t* __restrict__ off, uint64_t count,
-                                                      uint64_t seg, uint32_t* __restrict__ task_off,
-                                                      uint32_t* __restrict__ work) {
-    __shared__ uint32_t part[1024];
-    const uint32_t tid = threadIdx.x;
-    const uint64_t per = (count + 1023) / 1024;
-    const uint64_t i0 = min(count, tid * per), i1 = min(count, i0 + per);
-    uint32_t sum = 0;
-    for (uint64_t i = i0; i < i1; ++i) {
-        uint64_t a = off[i], b = off[i + 1];
-        uint64_t len = b > a ? b - a : 0;
-        sum += len == 0 ? 1u : static_cast<uint32_t>((len + seg - 1) / seg);
-    }
-    part[tid] = sum;
-    __syncthreads();
-    for (int d = 1; d < 1024; d <<= 1) {  // inclusive Hillis-Steele scan
-        uint32_t x = tid >= static_cast<uint32_t>(d) ? part[tid - d] : 0;
-        __syncthreads();
-        part[tid] += x;
-        __syncthreads();
-    }
-    uint32_t run = tid ? part[tid - 1] : 0;
-    for (uint64_t i = i0; i < i1; ++i) {
-        task_off[i] = run;
-        uint64_t a = off[i], b = off[i + 1];
-        uint64_t len = b > a ? b - a : 0;
-        run += len == 0 ? 1u : static_cast<uint32_t>((len + seg - 1) / seg);
-    }
-    if (tid == 1023) task_off[count] = part[1023];
-    if (tid == 0) *work = 0;
-}
-
-template <class Step, bool VEC>
-__global__ void __launch_bounds__(kBatchWarps * 32)
-k_batch_scan(const BatchArgs a) {
-    using CP = Comp<Step, VEC>;
-    uint8_t* tbl = dsmem;
-    const int lane = threadIdx.x & 31;
-    Step S;
-    S.setup(a.t, tbl, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const uint32_t total = a.task_off[a.count];
-    for (;;) {
-        uint32_t task = 0;
-        if (lane == 0) task = atomicAdd(a.work, 1u);
-        task = __shfl_sync(kFull, task, 0);
-        if (task >= total) break;
-        // text of this task: last i with task_off[i] <= task
-        uint64_t lo = 0, hi = a.count;  // invariant: task_off[lo] <= task < task_off[hi]
-        while (hi - lo > 1) {
-            uint64_t mid = (lo + hi) / 2;
-            if (a.task_off[mid] <= task) lo = mid;
-            else hi = mid;
-        }
-        const uint64_t i = lo;
-        const uint32_t j = task - a.task_off[i];
-        const uint32_t ntasks = a.task_off[i + 1] - a.task_off[i];
-        const uint64_t t0 = a.off[i], t1 = max(t0, a.off[i + 1]);
-        const uint64_t s0 = min(t1, t0 + j * a.seg), s1 = min(t1, s0 + a.seg);
-        const uint64_t per = (((s1 - s0) + 31) / 32 + 15) & ~uint64_t(15);
-        const uint64_t p0 = min(s1, s0 + lane * per), p1 = min(s1, p0 + per);
-        const uint32_t s = S.id(run_range(S, S.init(lane), a.texts, p0, p1), lane);
-        const uint32_t val = CP::fold_states(S, a.t, s);
-        if (ntasks == 1) {
-            const uint32_t q = CP::q_final(a.t, val, 0);
-            if (lane == 0) a.results[i] = sfa_result{q, a.t.dfinal[q]};
-        } else if (VEC) {
-            a.seg_parts[static_cast<uint64_t>(task) * CP::kSlot + lane] = static_cast<uint8_t>(val);
-        } else if (lane == 0) {
-            reinterpret_cast<uint32_t*>(a.seg_parts)[task] = val;
-        }
-    }
-}
-
-template <class Step, bool VEC>
-__global__ void __launch_bounds__(kBatchWarps * 32)
-k_batch_combine(const BatchArgs a) {
-    using CP = Comp<Step, VEC>;
-    Step S;
-    S.setup(a.t, dsmem, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t i = wid; i < a.count; i += nw) {
-        const uint32_t t0 = a.task_off[i], t1 = a.task_off[i + 1];
-        if (t1 - t0 <= 1) continue;
-        uint32_t acc = CP::fold_slots(S, a.t, a.seg_parts + static_cast<uint64_t>(t0) * CP::kSlot, t1 - t0,
-                                      CP::identity(), true);
-        const uint32_t q = CP::q_final(a.t, acc, 0);
-        if (lane == 0) a.results[i] = sfa_result{q, a.t.dfinal[q]};
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// Host launchers
-// ------------------------------------------------------------------------------------------
-namespace {
-
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encode_fn() {
-    static EncodeFn fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(p);
-    }
-    return fn;
-}
-
-
-template <class Step, int K, int ROWB, bool VEC>
-cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
-    using Sh = TmaShape<K, ROWB>;
-    auto kern = k_scan_tma<Step, K, ROWB, VEC>;
-    const uint32_t tbytes = static_cast<uint32_t>(table_bytes<Step>(a.t));
-    const size_t smem = tbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    EncodeFn enc = encode_fn();
-    if (!enc) return cudaErrorNotSupported;
-    TmaMaps maps;
-    cuuint64_t dims[2] = {a.plan.L, a.plan.nchunks};
-    cuuint64_t strides[1] = {a.plan.L};
-    const cuuint32_t br = a.plan.rows_per_cta / Sh::NB;
-    if (br == 0 || br > 256 || br * Sh::NB != a.plan.rows_per_cta || (br * ROWB) % 128) return cudaErrorInvalidValue;
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(ROWB), br};
-    cuuint32_t pbox[2] = {static_cast<cuuint32_t>(kLine), br};
-    cuuint32_t estr[2] = {1, 1};
-    void* base = const_cast<uint8_t*>(a.text + a.plan.head);
-    CUresult r = enc(&maps.load, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    r = enc(&maps.pref, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, pbox, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    kern<<<a.plan.ctas, (kNW + 1) * 32, smem, stream>>>(maps, a, tbytes, cfg.nring, cfg.pf_lines);
-    return cudaGetLastError();
-}
-
-template <class Step, bool VEC>
-cudaError_t tma_launch(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
-    switch (cfg.K * 1000 + cfg.rowb) {
-        case 1016: return tma_launch_t<Step, 1, 16, VEC>(a, cfg, stream);
-        case 1032: return tma_launch_t<Step, 1, 32, VEC>(a, cfg, stream);
-        case 2016: return tma_launch_t<Step, 2, 16, VEC>(a, cfg, stream);
-        case 2032: return tma_launch_t<Step, 2, 32, VEC>(a, cfg, stream);
-    }
-    return cudaErrorInvalidValue;
-}
-
-template <class Step, bool VEC>
-cudaError_t direct_launch(const DirectArgs& a, cudaStream_t stream) {
-    auto kern = k_scan_direct<Step, VEC>;
-    const size_t smem = kDirectRed + 16 + table_bytes<Step>(a.t);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    const uint64_t ctas = (a.npieces + kDirectWarps * 32 - 1) / (kDirectWarps * 32);
-    kern<<<static_cast<unsigned>(ctas), kDirectWarps * 32, smem, stream>>>(a);
-    return cudaGetLastError();
-}
-
-template <class Step, bool VEC>
-cudaError_t batch_launch(const BatchArgs& a, int sm_count, cudaStream_t stream) {
-    const size_t smem = table_bytes<Step>(a.t);
-    auto scan = k_batch_scan<Step, VEC>;
-    auto comb = k_batch_combine<Step, VEC>;
-    cudaError_t e = cudaFuncSetAttribute(scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(comb, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan, kBatchWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    k_batch_plan<<<1, 1024, 0, stream>>>(a.off, a.count, a.seg, a.task_off, a.work);
-    scan<<<sm_count * per_sm, kBatchWarps * 32, smem, stream>>>(a);
-    comb<<<sm_count, kBatchWarps * 32, smem, stream>>>(a);
-    return cudaGetLastError();
-}
-
-}  // namespace
-
 size_t table_smem_bytes(Res mode, const DevTables& t) {
     switch (mode) {
-        case Res::Private: return StepPrivate::supported(t) ? table_bytes<StepPrivate>(t) : SIZE_MAX / 2;
-        case Res::Shared: return StepShared::supported(t) ? table_bytes<StepShared>(t) : SIZE_MAX / 2;
-        default: return table_bytes<StepGlobal>(t);
+        case Res::Private: return StepPrivate::supported(t) ? table_bytes<StepPrivate>(t) + t.aux_bytes : SIZE_MAX / 2;
+        case Res::Shared: return StepShared::supported(t) ? table_bytes<StepShared>(t) + t.aux_bytes : SIZE_MAX / 2;
+        default: return table_bytes<StepGlobal>(t) + t.aux_bytes;
     }
 }
 size_t direct_smem_bytes(Res mode, const DevTables& t) { return kDirectRed + 16 + table_smem_bytes(mode, t); }
@@ -581,31 +28,41 @@ uint32_t direct_threads_per_cta() { return kDirectWarps * 32; }
 static int Sh_NB_host(int K) { return K == 1 ? Sh_NB<1>() : Sh_NB<2>(); }
 
 // (K, ROWB) candidates in order of preference; the ring takes what is left.
+// SFA_TMA_CONFIG="K,ROWB,ring[,pf[,promo]]" forces a shape (diagnostic sweeps
+// and tests): ring 0 = as deep as fits, pf = L2 prefetch distance in 256-B
+// lines (-1 = none), promo = L2 promotion bytes of the load map (0/64/128/256).
 bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out) {
     const size_t tb = table_smem_bytes(mode, t);
     if (tb > smem_optin) return false;
-    static const int cand[][2] = {{1, 32}, {2, 32}, {2, 16}, {1, 16}};
-    const char* env = getenv("SFA_TMA_CONFIG");  // "K,ROWB,ring" (diagnostic sweeps)
-    int fk = 0, fr = 0, fn = 0;
-    if (env) sscanf(env, "%d,%d,%d", &fk, &fr, &fn);
+    static const int cand[][2] = {{1, 32}, {2, 32}, {1, 64}, {2, 16}, {1, 16}};
+    const char* env = getenv("SFA_TMA_CONFIG");
+    int fk = 0, fr = 0, fn = 0, fpf = -2, fpromo = -1;
+    if (env) sscanf(env, "%d,%d,%d,%d,%d", &fk, &fr, &fn, &fpf, &fpromo);
+    const bool forced = fk && (fk == 1 || fk == 2) && (fr == 16 || fr == 32 || fr == 64);
     for (int pass = 0; pass < 2; ++pass) {
-        for (auto& c : cand) {
-            const int K = c[0], rowb = c[1];
-            if (fk && (K != fk || rowb != fr)) continue;
+        for (size_t ci = 0; ci < sizeof(cand) / sizeof(cand[0]); ++ci) {
+            int K = cand[ci][0], rowb = cand[ci][1];
+            if (forced) {
+                if (ci) break;
+                K = fk;
+                rowb = fr;
+            }
             const size_t R = static_cast<size_t>(K) * kNW * 32;
             const size_t stage = R * rowb;
-            const size_t fixed = (((K * kNW + 2) * 32 + 15) & ~15u) + 16 + 2 * kMaxRing * 8 + 128;
+            const size_t fixed = (((K * kNW + 2) * 32 + 15) & ~15u) + 16 + (2 * kMaxRing + 1) * 8 + 1024;
             if (tb + fixed + 2 * stage > smem_optin) continue;
             uint32_t ring = static_cast<uint32_t>(std::min<size_t>(kMaxRing, (smem_optin - tb - fixed) / stage));
             if (fn) ring = std::min<uint32_t>(ring, static_cast<uint32_t>(fn));
-            if (pass == 0 && ring < 3 && !fk) continue;
+            if (pass == 0 && ring < 3 && !forced) continue;
             out->K = K;
             out->rowb = rowb;
             out->nring = ring;
             out->rows_per_cta = static_cast<uint32_t>(R);
             out->nb = Sh_NB_host(K);
-            // prefetch about 256 KiB of each SM's rows ahead of the loads
-            out->pf_lines = static_cast<uint32_t>(std::max<size_t>(1, (256u << 10) / (R * kLine)));
+            // No L2 prefetch by default: with ~1000 rows per SM, lines fetched
+            // ahead of the TMA loads were evicted before use (1.6x DRAM reads).
+            out->pf_lines = fpf >= -1 ? fpf : -1;
+            out->promo = fpromo >= 0 ? fpromo : 0;
             return true;
         }
     }
@@ -614,28 +71,25 @@ bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out)
 
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
     switch (mode) {
-        case Res::Private: return vec ? tma_launch<StepPrivate, true>(a, cfg, stream) : tma_launch<StepPrivate, false>(a, cfg, stream);
-        case Res::Shared: return vec ? tma_launch<StepShared, true>(a, cfg, stream) : tma_launch<StepShared, false>(a, cfg, stream);
-        default: return vec ? tma_launch<StepGlobal, true>(a, cfg, stream) : tma_launch<StepGlobal, false>(a, cfg, stream);
+        case Res::Private: return StepLaunch<StepPrivate>::scan_tma(vec, a, cfg, stream);
+        case Res::Shared: return StepLaunch<StepShared>::scan_tma(vec, a, cfg, stream);
+        default: return StepLaunch<StepGlobal>::scan_tma(vec, a, cfg, stream);
     }
 }
 
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream) {
     switch (mode) {
-        case Res::Private: return vec ? direct_launch<StepPrivate, true>(a, stream) : direct_launch<StepPrivate, false>(a, stream);
-        case Res::Shared: return vec ? direct_launch<StepShared, true>(a, stream) : direct_launch<StepShared, false>(a, stream);
-        default: return vec ? direct_launch<StepGlobal, true>(a, stream) : direct_launch<StepGlobal, false>(a, stream);
+        case Res::Private: return StepLaunch<StepPrivate>::scan_direct(vec, a, stream);
+        case Res::Shared: return StepLaunch<StepShared>::scan_direct(vec, a, stream);
+        default: return StepLaunch<StepGlobal>::scan_direct(vec, a, stream);
     }
 }
 
 cudaError_t launch_batch(Res mode, bool vec, const BatchArgs& a, int sm_count, cudaStream_t stream) {
     switch (mode) {
-        case Res::Private:
-            return vec ? batch_launch<StepPrivate, true>(a, sm_count, stream) : batch_launch<StepPrivate, false>(a, sm_count, stream);
-        case Res::Shared:
-            return vec ? batch_launch<StepShared, true>(a, sm_count, stream) : batch_launch<StepShared, false>(a, sm_count, stream);
-        default:
-            return vec ? batch_launch<StepGlobal, true>(a, sm_count, stream) : batch_launch<StepGlobal, false>(a, sm_count, stream);
+        case Res::Private: return StepLaunch<StepPrivate>::batch(vec, a, sm_count, stream);
+        case Res::Shared: return StepLaunch<StepShared>::batch(vec, a, sm_count, stream);
+        default: return StepLaunch<StepGlobal>::batch(vec, a, sm_count, stream);
     }
 }
 

@@ -23,6 +23,7 @@ struct ScanArgs {
     Scratch sc;
     const uint32_t* q_in;
     sfa_result* result;
+    uint64_t* stamps;     // diagnostic (SFA_DEBUG_STAMPS): 8 %globaltimer stamps per CTA, else NULL
 };
 
 struct DirectArgs {
@@ -53,7 +54,9 @@ struct BatchArgs {
 // distance in 256-byte lines.
 struct TmaConfig {
     int K = 1, rowb = 16;
-    uint32_t nring = 2, rows_per_cta = 0, pf_lines = 1;
+    uint32_t nring = 2, rows_per_cta = 0;
+    int pf_lines = 1;     // L2 prefetch distance in 256-B lines (-1: no prefetch)
+    int promo = 256;      // L2 promotion of the TMA loads (bytes; 0 = none)
     uint32_t nb = 4;   // TMA boxes per stage: rows_per_cta of a launch must be a multiple
 };
 
@@ -62,6 +65,14 @@ size_t table_smem_bytes(Res mode, const DevTables& t);   // SIZE_MAX/2 if the la
 uint32_t direct_threads_per_cta();
 // false if `mode` cannot run the TMA scan within smem_optin bytes
 bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out);
+
+// Per-step-policy launchers, specialised in kernels_<step>.cu.
+template <class Step>
+struct StepLaunch {
+    static cudaError_t scan_tma(bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s);
+    static cudaError_t scan_direct(bool vec, const DirectArgs& a, cudaStream_t s);
+    static cudaError_t batch(bool vec, const BatchArgs& a, int sm_count, cudaStream_t s);
+};
 
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);

@@ -3,6 +3,8 @@
 
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "../../include/sfa.h"
 
 namespace sfa {
@@ -18,6 +20,14 @@ struct DevTables {
     const uint8_t* dfinal = nullptr;    // nD       q in F_d
     const uint32_t* rep_off = nullptr;  // nS + 1
     const uint8_t* rep = nullptr;       // representative words (bytes)
+    // composition (kernels.cu Comp): table comp[a * nS + b] = id(f_a . f_b), u8 if comp_u8 else
+    // u16 (nullptr: Lemma-1 replay); rep16[s] = rep(s) in bytes 0..14, |rep(s)| in byte 15 (depth <= 15)
+    const void* comp = nullptr;
+    uint32_t comp_u8 = 0;
+    const uint4* rep16 = nullptr;
+    // aux smem image copied after the step table: [comp table if aux_comp][maps32 at aux_maps_off if aux_maps]
+    const uint32_t* aux = nullptr;
+    uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;
     uint32_t lo = 0, W = 0;             // byte window: columns lo..lo+W-2, column W-1 = every other byte
 };

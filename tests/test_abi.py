@@ -158,16 +158,18 @@ def test_errors_and_capacity():
 
 def test_info_and_byte_window():
     """A1: the column window of each config (kernel section)."""
-    for (rx, alpha), lo, w, vec in [(CFG1, ord("a"), 4, 0), (CFG2, ord("0"), 11, 0), (CFG4, ord("a"), 3, 1)]:
+    T = P.COMPOSE_TABLE
+    for (rx, alpha), lo, w, cm in [(CFG1, ord("a"), 4, T), (CFG2, ord("0"), 11, T), (CFG4, ord("a"), 3, T)]:
         h = P.sfa_compile(rx, alpha)
         info = P.sfa_info(h)
         P.sfa_free(h)
         assert (info["range_lo"], info["range_width"]) == (lo, w), rx
-        assert info["compose_mode"] == vec
+        assert info["compose_mode"] == cm
     h = P.sfa_compile(W.cfg3_regex(), None)
     info = P.sfa_info(h)
     P.sfa_free(h)
-    assert (info["range_lo"], info["range_width"], info["compose_mode"]) == (ord("a"), 27, 1)
+    # |S| ~ 20k > 4096: no composition table, |D| > 32: no vectors -> Lemma-1 replay
+    assert (info["range_lo"], info["range_width"], info["compose_mode"]) == (ord("a"), 27, P.COMPOSE_REPLAY)
     assert 1 <= info["sfa_depth"] <= 16
 
 
@@ -192,3 +194,27 @@ def test_window_columns_cover_every_byte():
         other = [b for b, c in enumerate(cols) if c == w - 1 and not (0 <= b - lo < w - 1)]
         for b in other:
             assert (table[:, b] == table[:, other[0]]).all(), (rx, b)
+
+
+def test_set_compose_capacity():
+    """sfa_set_compose refuses modes the automaton cannot use (no device needed)."""
+    h = P.sfa_compile(*CFG4)          # |D| = 513 > 32
+    with pytest.raises(P.SFAError) as e:
+        P.sfa_set_compose(h, P.COMPOSE_VEC)
+    assert e.value.code == P.SFA_ERR_CAPACITY
+    P.sfa_set_compose(h, P.COMPOSE_REPLAY)
+    assert P.sfa_info(h)["compose_mode"] == P.COMPOSE_REPLAY
+    with pytest.raises(P.SFAError) as e:
+        P.sfa_set_compose(h, 7)
+    assert e.value.code == P.SFA_ERR_INVALID_ARG
+    P.sfa_free(h)
+    h = P.sfa_compile(W.cfg3_regex(), None)   # |S| ~ 20k > 4096
+    with pytest.raises(P.SFAError) as e:
+        P.sfa_set_compose(h, P.COMPOSE_TABLE)
+    assert e.value.code == P.SFA_ERR_CAPACITY
+    P.sfa_free(h)
+    h = P.sfa_compile(*CFG2)
+    for m in (P.COMPOSE_VEC, P.COMPOSE_TABLE, P.COMPOSE_REPLAY, P.COMPOSE_AUTO):
+        P.sfa_set_compose(h, m)
+    assert P.sfa_info(h)["compose_mode"] == P.COMPOSE_TABLE
+    P.sfa_free(h)

@@ -318,7 +318,8 @@ def test_match_host_replay_mode(torch_cuda):
 
 
 # --------------------------------------------------------------------------- every TMA pipeline shape
-@pytest.mark.parametrize("shape", ["1,16,0", "1,32,0", "2,16,0", "2,32,0", "1,16,2", "2,16,2", "1,32,3"])
+@pytest.mark.parametrize("shape", ["1,16,0", "1,32,0", "2,16,0", "2,32,0", "1,64,0", "1,16,2", "2,16,2",
+                                   "1,32,3", "1,32,0,-1,256", "1,64,0,0,128", "2,32,0,-1,0"])
 def test_every_tma_shape(torch_cuda, shape, monkeypatch):
     """k_scan_tma for each (K chunks/thread, bytes/row/stage, ring depth) the
     launcher can pick (SFA_TMA_CONFIG forces one), on texts spanning several
@@ -333,3 +334,34 @@ def test_every_tma_shape(torch_cuda, shape, monkeypatch):
             t = text[:n]
             for pad in (0, 5):
                 check_text(torch, sfa, d, t, pad)
+
+
+# --------------------------------------------------------------------------- every composition mode
+@pytest.mark.parametrize("rx,alpha,modes", [(*CFG1, (P.COMPOSE_VEC, P.COMPOSE_TABLE, P.COMPOSE_REPLAY)),
+                                            (*CFG2, (P.COMPOSE_VEC, P.COMPOSE_TABLE, P.COMPOSE_REPLAY)),
+                                            (*CFG4, (P.COMPOSE_TABLE, P.COMPOSE_REPLAY))])
+def test_every_compose_mode(torch_cuda, rx, alpha, modes):
+    """A3 by shuffled mapping vectors, by the composition table and by Lemma-1
+    replay: the same exact result on the direct and TMA scans, the forced
+    chunkings (per-chunk ids included) and batches."""
+    torch = torch_cuda
+    d = oracle_pair(rx, alpha)
+    gen = {CFG1: W.cfg1_random, CFG2: lambda n: W.cfg2_accepted(n // 10), CFG4: W.cfg4_text}[(rx, alpha)]
+    text = gen(6_000_011)
+    for m in modes:
+        sfa = P.SFA(rx, alpha)
+        sfa.set_compose(m)
+        for n in (text.size, 5_000_003, 70_001, 13):
+            check_text(torch, sfa, d, text[:n], pad=3)
+        _, v = dev(torch, text[:100_003])
+        q, acc, ids = sfa.match_chunked(v, 777)
+        assert (q, acc) == d.run(text[:100_003])
+        o_ids, _, _ = O.OracleSFA(d).run_chunked(text[:100_003], spec_bounds(100_003, 777))
+        assert ids.tolist() == o_ids.tolist(), m
+        texts, off = W.ragged_batch(11, 40, 200_000, alpha)
+        res = torch.zeros(80, dtype=torch.int32, device="cuda")
+        sfa.match_batch(torch.from_numpy(texts).cuda(), torch.from_numpy(off.astype(np.int64)).cuda(), 40, res)
+        torch.cuda.synchronize()
+        got = res.cpu().numpy().view(np.uint32).reshape(40, 2)
+        qo, ao = d.run_batch(texts, off)
+        assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all(), m
