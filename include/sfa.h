@@ -182,6 +182,15 @@ SFA_API int sfa_match_chunked(const sfa_handle* h, const uint8_t* d_text, size_t
 /* Forces a residency mode (SFA_RES_*); CAPACITY if it does not fit. */
 SFA_API int sfa_set_residency(sfa_handle* h, int mode);
 
+/* HOT residency: re-ranks the SFA states by their visit frequency on a
+ * sample of text (the first min(n, 8 MiB) bytes of d_sample, device memory,
+ * caller-owned; copied to the host on `stream`), so the most visited rows sit
+ * in shared memory.  Blocking: waits for earlier work of the handle, then
+ * rewrites the HOT tables.  n == 0 restores the static ranking.  Without a
+ * call, the first HOT match of the handle tunes on its own text (environment
+ * SFA_HOT_AUTOTUNE=0 disables that).  Results never depend on the ranking. */
+SFA_API int sfa_tune_residency(sfa_handle* h, const uint8_t* d_sample, size_t n, sfa_stream_t stream);
+
 /* Forces a composition mode (SFA_COMPOSE_*); CAPACITY if the handle cannot
  * use it (VEC needs |D| <= 32, TABLE |S| <= 4096).  Results do not depend on
  * it (composition is exact); only the epilogue cost does. */

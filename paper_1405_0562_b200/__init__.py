@@ -56,6 +56,7 @@ class sfa_info_t(C.Structure):
 
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
+           "sfa_tune_residency",
            "sfa_export_dfa", "sfa_export_sfa")
 
 _lib = None
@@ -81,6 +82,7 @@ def lib() -> C.CDLL:
         L.sfa_match_chunked.argtypes = [vp, vp, C.c_size_t, C.c_uint32, vp, u32p, C.POINTER(C.c_int), u32p]
         L.sfa_set_residency.argtypes = [vp, C.c_int]
         L.sfa_set_compose.argtypes = [vp, C.c_int]
+        L.sfa_tune_residency.argtypes = [vp, vp, C.c_size_t, vp]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
         for f in EXPORTS:
@@ -193,6 +195,15 @@ def sfa_set_residency(h: int, mode: int):
     _check(lib().sfa_set_residency(h, mode))
 
 
+def sfa_tune_residency(h: int, d_sample=None, n: int | None = None, stream=None):
+    """HOT residency: re-rank rows by visit frequency on a device text sample (None: static ranking)."""
+    if d_sample is None:
+        _check(lib().sfa_tune_residency(h, None, 0, _stream(stream)))
+        return
+    n = _nbytes(d_sample) if n is None else n
+    _check(lib().sfa_tune_residency(h, _dptr(d_sample), n, _stream(stream)))
+
+
 def sfa_set_compose(h: int, mode: int):
     _check(lib().sfa_set_compose(h, mode))
 
@@ -260,6 +271,9 @@ class SFA:
 
     def set_compose(self, mode: int):
         sfa_set_compose(self.h, mode)
+
+    def tune_residency(self, d_sample=None, stream=None):
+        sfa_tune_residency(self.h, d_sample, None, stream)
 
     def export_dfa(self):
         return sfa_export_dfa(self.h)

@@ -74,6 +74,9 @@ struct sfa_handle {
     uint32_t* drep_off = nullptr;
     uint8_t* drep = nullptr;
     void* dcomp = nullptr;                    // composition table (u8 if nS <= 256, else u16)
+    uint16_t* dTdev = nullptr;                // HOT: window table renumbered by visit frequency
+    uint16_t* dperm = nullptr;                // HOT: canonical -> device id
+    uint16_t* diperm = nullptr;               // HOT: device -> canonical id
     uint4* drep16 = nullptr;                  // rep(s) slots (depth <= 15)
     uint32_t* daux[2] = {nullptr, nullptr};   // aux smem images: [0] comp (TABLE), [1] maps32 (VEC)
     uint32_t aux_bytes[2] = {0, 0};
@@ -102,7 +105,7 @@ struct sfa_handle {
         for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
                         (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
                         (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1],
-                        (void*)dcomp, (void*)drep16, (void*)daux[0],
+                        (void*)dcomp, (void*)dTdev, (void*)dperm, (void*)diperm, (void*)drep16, (void*)daux[0],
                         (void*)daux[1]})
             if (p) cudaFree(p);
         if (hres) cudaFreeHost(hres);
@@ -125,7 +128,7 @@ struct sfa_handle {
     bool vec() const { return compose_mode() == SFA_COMPOSE_VEC; }
 
     // device tables as seen by a kernel (aux = the composition mode's smem image)
-    sfa::DevTables tables(sfa::Res = sfa::Res::Global) const {
+    sfa::DevTables tables(sfa::Res mode = sfa::Res::Global, int kind = 0) const {
         sfa::DevTables t;
         const int cm = compose_mode();
         t.comp = cm == SFA_COMPOSE_TABLE ? dcomp : nullptr;
@@ -155,7 +158,99 @@ struct sfa_handle {
         t.nD = A.nD;
         t.lo = lo;
         t.W = W;
+        t.Tdev = dTdev;
+        t.perm = dperm;
+        t.iperm = diperm;
+        t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin) : 0;
         return t;
+    }
+
+    // HOT residency: rank SFA states by visit frequency.  Static part: a
+    // random walk drawing every window column (byte class of the table)
+    // uniformly, restarting from f_I every 2048 steps (chunks start from f_I,
+    // Alg. 5 line 2).  Profile part (sample != NULL): the SFA run over
+    // 2048-byte chunks of a sample of real text, weighted 16x.  Device ids =
+    // ranks, so the hot rows are a prefix of the renumbered table.
+    void hot_ranking(std::vector<uint32_t>& perm, const uint8_t* sample, size_t ns) const {
+        const uint32_t nS = A.nS;
+        std::vector<uint64_t> cnt(nS, 0);
+        std::vector<uint32_t> colcls(W);
+        for (uint32_t j = 0; j + 1 < W; ++j) colcls[j] = A.cls[lo + j];
+        colcls[W - 1] = other;
+        uint64_t x = 0x9e3779b97f4a7c15ull;
+        for (int walk = 0; walk < 2048; ++walk) {
+            uint32_t st = 0;
+            ++cnt[st];
+            for (int k = 0; k < 2048; ++k) {
+                x ^= x << 13;
+                x ^= x >> 7;
+                x ^= x << 17;
+                st = A.T[static_cast<size_t>(st) * A.C + colcls[(x >> 11) % W]];
+                ++cnt[st];
+            }
+        }
+        for (size_t c0 = 0; sample && c0 < ns; c0 += 2048) {
+            uint32_t st = 0;
+            for (size_t i = c0; i < std::min(ns, c0 + 2048); ++i) {
+                st = A.T[static_cast<size_t>(st) * A.C + A.cls[sample[i]]];
+                cnt[st] += 16;
+            }
+        }
+        std::vector<uint32_t> order(nS);
+        for (uint32_t i = 0; i < nS; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
+        perm.assign(nS, 0);
+        for (uint32_t r = 0; r < nS; ++r) perm[order[r]] = r;
+    }
+
+    // (Re)builds the HOT tables from a ranking and writes them to the device
+    // buffers (allocated on first use).  Synchronous.
+    int upload_hot(const uint8_t* sample, size_t ns) {
+        const uint32_t nS = A.nS;
+        std::vector<uint32_t> perm;
+        hot_ranking(perm, sample, ns);
+        std::vector<uint16_t> p16(nS), ip16(nS), Td((static_cast<size_t>(nS) * W + 7) & ~size_t(7), 0);
+        for (uint32_t st = 0; st < nS; ++st) {
+            p16[st] = static_cast<uint16_t>(perm[st]);
+            ip16[perm[st]] = static_cast<uint16_t>(st);
+        }
+        for (uint32_t st = 0; st < nS; ++st)
+            for (uint32_t j = 0; j < W; ++j) {
+                const uint32_t c = j + 1 < W ? A.cls[lo + j] : other;
+                Td[static_cast<size_t>(perm[st]) * W + j] = p16[A.T[static_cast<size_t>(st) * A.C + c]];
+            }
+        if (!dTdev) {
+            CU(cudaMalloc(&dTdev, Td.size() * 2));
+            CU(cudaMalloc(&dperm, nS * 2));
+            CU(cudaMalloc(&diperm, nS * 2));
+        }
+        CU(cudaMemcpy(dTdev, Td.data(), Td.size() * 2, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dperm, p16.data(), nS * 2, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(diperm, ip16.data(), nS * 2, cudaMemcpyHostToDevice));
+        return SFA_OK;
+    }
+
+    // Profile-guided HOT ranking from (a prefix of) a device text, once per
+    // handle unless forced.  Waits for all earlier work of the handle (the
+    // tables are rewritten in place).  Results never depend on the ranking.
+    bool hot_tuned = false;
+    static bool auto_tune() {
+        static const bool on = [] {
+            const char* e = getenv("SFA_HOT_AUTOTUNE");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+    int tune_hot(const uint8_t* d_text, size_t n, cudaStream_t stream) {
+        const size_t ns = std::min<size_t>(n, 8u << 20);
+        std::vector<uint8_t> sample(ns);
+        if (has_last) CU(cudaStreamSynchronize(last_stream));
+        CU(cudaMemcpyAsync(sample.data(), d_text, ns, cudaMemcpyDeviceToHost, stream));
+        CU(cudaStreamSynchronize(stream));
+        int rc = upload_hot(sample.data(), ns);
+        if (rc) return rc;
+        hot_tuned = true;
+        return SFA_OK;
     }
 
     // Lazy upload: sfa_compile works without a GPU (host tests); the first
@@ -235,6 +330,12 @@ struct sfa_handle {
             CU(upload(&daux[1], reinterpret_cast<const uint32_t*>(m32.data()), m32.size() / 4));
             aux_bytes[1] = static_cast<uint32_t>(m32.size());
         }
+        // HOT residency tables (AUTO uses them when neither smem layout holds the whole table)
+        {
+            const int rc = upload_hot(nullptr, 0);
+            if (rc) return rc;
+            dev_bytes += static_cast<uint64_t>(nS) * W * 2 + 4ull * nS;
+        }
         CU(upload(&dimg0, A.img0.data(), A.img0.size()));
         CU(upload(&dfinal, A.dfa_final.data(), A.dfa_final.size()));
         CU(upload(&drep_off, A.rep_off.data(), A.rep_off.size()));
@@ -254,7 +355,8 @@ struct sfa_handle {
 
     // does `mode` fit for this launch kind?
     bool fits(sfa::Res mode, int kind /*0 tma, 1 direct, 2 batch*/) const {
-        const sfa::DevTables t = tables();
+        const sfa::DevTables t = tables(mode, kind);
+        if (mode == sfa::Res::Hot && t.hotH == 0) return false;
         if (kind == 0) {
             sfa::TmaConfig c;
             return sfa::tma_choose(mode, t, smem_optin, &c);
@@ -264,12 +366,12 @@ struct sfa_handle {
     }
     int resolve(int kind, sfa::Res* out) const {
         if (forced != SFA_RES_AUTO) {
-            sfa::Res m = forced == SFA_RES_HOT_L2 ? sfa::Res::Global : static_cast<sfa::Res>(forced);
+            const sfa::Res m = static_cast<sfa::Res>(forced);
             if (!fits(m, kind)) return fail(SFA_ERR_CAPACITY, "forced residency does not fit in shared memory");
             *out = m;
             return SFA_OK;
         }
-        for (sfa::Res m : {sfa::Res::Private, sfa::Res::Shared, sfa::Res::Global})
+        for (sfa::Res m : {sfa::Res::Private, sfa::Res::Shared, sfa::Res::Hot, sfa::Res::Global})
             if (fits(m, kind)) {
                 *out = m;
                 return SFA_OK;
@@ -292,10 +394,14 @@ struct sfa_handle {
         sfa::Res mode;
         int rc = resolve(direct ? 1 : 0, &mode);
         if (rc) return rc;
+        if (mode == sfa::Res::Hot && !hot_tuned && auto_tune()) {
+            rc = tune_hot(d_text, n, stream);
+            if (rc) return rc;
+        }
         cudaError_t e;
         if (direct) {
             sfa::DirectArgs a;
-            a.t = tables(mode);
+            a.t = tables(mode, 1);
             a.text = d_text;
             a.n = n;
             a.npieces = force_pieces ? force_pieces : std::max<uint64_t>(1, (n + kDirectPiece - 1) / kDirectPiece);
@@ -308,7 +414,7 @@ struct sfa_handle {
             e = sfa::launch_scan_direct(mode, vec(), a, stream);
         } else {
             sfa::ScanArgs a;
-            a.t = tables(mode);
+            a.t = tables(mode, 0);
             a.text = d_text;
             a.n = n;
             a.sc = scratch();
@@ -475,6 +581,21 @@ int sfa_set_residency(sfa_handle* h, int mode) {
     return rc;
 }
 
+int sfa_tune_residency(sfa_handle* h, const uint8_t* d_sample, size_t n, sfa_stream_t stream) {
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (!d_sample && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_sample is NULL with n > 0");
+    std::lock_guard<std::mutex> lk(h->mu);
+    int rc = h->ensure_uploaded();
+    if (rc) return rc;
+    if (n == 0) {  // back to the static ranking
+        if (h->has_last) CU(cudaStreamSynchronize(h->last_stream));
+        rc = h->upload_hot(nullptr, 0);
+        if (!rc) h->hot_tuned = true;
+        return rc;
+    }
+    return h->tune_hot(d_sample, n, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int sfa_set_compose(sfa_handle* h, int mode) {
     if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
     if (mode < SFA_COMPOSE_AUTO || mode > SFA_COMPOSE_REPLAY) return fail(SFA_ERR_INVALID_ARG, "bad compose mode");
@@ -627,8 +748,14 @@ int sfa_match_batch(const sfa_handle* hc, const uint8_t* d_texts, const uint64_t
         CU(cudaMalloc(&h->seg_parts, need));
         h->seg_cap = need;
     }
+    if (mode == sfa::Res::Hot && !h->hot_tuned && h->auto_tune() && total_bytes > 0) {
+        uint64_t first = 0;
+        CU(cudaMemcpy(&first, d_offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        rc = h->tune_hot(d_texts + first, total_bytes, s);
+        if (rc) return rc;
+    }
     sfa::BatchArgs a;
-    a.t = h->tables(mode);
+    a.t = h->tables(mode, 2);
     a.texts = d_texts;
     a.off = d_offsets;
     a.count = count;

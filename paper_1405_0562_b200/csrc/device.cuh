@@ -148,6 +148,21 @@ __device__ __forceinline__ uint32_t window_col(uint32_t byte, uint32_t neg_lo, u
     return __viaddmin_u32(byte, neg_lo, wmax);
 }
 
+// Cooperative global -> smem copy of n16 16-byte words, 4 loads in flight per
+// thread before their stores.
+__device__ __forceinline__ void copy16(uint4* dst, const uint4* src, size_t n16, int tid, int nthreads) {
+    size_t i = tid;
+    for (; i + 3 * nthreads < n16; i += 4 * nthreads) {
+        const uint4 a = __ldg(src + i), b = __ldg(src + i + nthreads), c = __ldg(src + i + 2 * nthreads),
+                    d = __ldg(src + i + 3 * nthreads);
+        dst[i] = a;
+        dst[i + nthreads] = b;
+        dst[i + 2 * nthreads] = c;
+        dst[i + 3 * nthreads] = d;
+    }
+    for (; i < n16; i += nthreads) dst[i] = __ldg(src + i);
+}
+
 // ------------------------------------------------------------------------------------------
 // Step policies
 // ------------------------------------------------------------------------------------------
@@ -252,20 +267,48 @@ struct StepGlobal {
     __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return s * W; }
 };
 
-// Cooperative global -> smem copy of n16 16-byte words, 4 loads in flight per
-// thread before their stores.
-__device__ __forceinline__ void copy16(uint4* dst, const uint4* src, size_t n16, int tid, int nthreads) {
-    size_t i = tid;
-    for (; i + 3 * nthreads < n16; i += 4 * nthreads) {
-        const uint4 a = __ldg(src + i), b = __ldg(src + i + nthreads), c = __ldg(src + i + 2 * nthreads),
-                    d = __ldg(src + i + 3 * nthreads);
-        dst[i] = a;
-        dst[i + nthreads] = b;
-        dst[i + 2 * nthreads] = c;
-        dst[i + 3 * nthreads] = d;
+struct StepHot {
+    // HOT residency (A6): SFA states renumbered by expected visit frequency
+    // (host ranking, DevTables::perm / iperm); rows [0, H) of the renumbered
+    // u16 window table DevTables::Tdev sit in smem, the other rows are read
+    // from global memory (L2).  state = device id.
+    uint32_t neg_lo, wmax, W, H, init_dev, sbase;
+    const uint16_t* Tdev;
+    const uint16_t* perm;
+    const uint16_t* iperm;
+
+    static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.hotH) * t.W * 2; }
+    static __host__ __device__ bool supported(const DevTables& t) { return t.Tdev != nullptr && t.hotH > 0; }
+    __device__ static void fill(const DevTables& t, int tid, int nthreads) {  // the hot rows are Tdev's prefix
+        copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.Tdev), (smem_bytes(t) + 15) / 16, tid,
+               nthreads);
     }
-    for (; i < n16; i += nthreads) dst[i] = __ldg(src + i);
-}
+    __device__ void params(const DevTables& t) {
+        neg_lo = 0u - t.lo;
+        wmax = t.W - 1;
+        W = t.W;
+        H = t.hotH;
+        Tdev = t.Tdev;
+        perm = t.perm;
+        iperm = t.iperm;
+        init_dev = __ldg(t.perm);  // f_I (canonical id 0)
+        sbase = smem_u32(dsmem);
+    }
+    __device__ __forceinline__ uint32_t init(uint32_t) const { return init_dev; }
+    // One predicated LDS (hot row) and one predicated LDG (cold row): no
+    // branch, no reconvergence; only the lanes whose state is cold touch L2.
+    __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
+        const uint32_t idx = st * W + window_col(byte, neg_lo, wmax);
+        uint32_t r;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t"
+            "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
+            : "=r"(r) : "r"(st), "r"(H), "r"(sbase + 2 * idx), "l"(Tdev + idx) : "memory");
+        return r;
+    }
+    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return __ldg(iperm + st); }
+    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return __ldg(perm + s); }
+};
 
 // 4 text bytes of one word, in text order (little-endian)
 template <class Step>

@@ -19,9 +19,27 @@ size_t table_smem_bytes(Res mode, const DevTables& t) {
     switch (mode) {
         case Res::Private: return StepPrivate::supported(t) ? table_bytes<StepPrivate>(t) + t.aux_bytes : SIZE_MAX / 2;
         case Res::Shared: return StepShared::supported(t) ? table_bytes<StepShared>(t) + t.aux_bytes : SIZE_MAX / 2;
+        case Res::Hot: return StepHot::supported(t) ? table_bytes<StepHot>(t) + t.aux_bytes : SIZE_MAX / 2;
         default: return table_bytes<StepGlobal>(t) + t.aux_bytes;
     }
 }
+// HOT residency: the number of renumbered rows that fit in smem next to what
+// the launch kind needs (kind 0: the TMA scan with K=1, 32-byte stages and a
+// 2-deep ring; 1: k_scan_direct; 2: the batch kernels), capped at nS.
+uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin) {
+    size_t other = t.aux_bytes + 16;
+    if (kind == 0) {
+        using Sh = TmaShape<1, 32>;
+        other += Sh::kFixed + 2 * Sh::kStageBytes;
+    } else if (kind == 1) {
+        other += kDirectRed + 16;
+    }
+    if (other >= smem_optin) return 0;
+    size_t rows = (smem_optin - other) / (2 * static_cast<size_t>(t.W));
+    if (const char* e = getenv("SFA_HOT_ROWS")) rows = std::min<size_t>(rows, std::max(1l, atol(e)));  // tests: force cold rows
+    return static_cast<uint32_t>(std::min<size_t>(rows, t.nS));
+}
+
 size_t direct_smem_bytes(Res mode, const DevTables& t) { return kDirectRed + 16 + table_smem_bytes(mode, t); }
 uint32_t direct_threads_per_cta() { return kDirectWarps * 32; }
 
@@ -73,6 +91,7 @@ cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConf
     switch (mode) {
         case Res::Private: return StepLaunch<StepPrivate>::scan_tma(vec, a, cfg, stream);
         case Res::Shared: return StepLaunch<StepShared>::scan_tma(vec, a, cfg, stream);
+        case Res::Hot: return StepLaunch<StepHot>::scan_tma(vec, a, cfg, stream);
         default: return StepLaunch<StepGlobal>::scan_tma(vec, a, cfg, stream);
     }
 }
@@ -81,6 +100,7 @@ cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStre
     switch (mode) {
         case Res::Private: return StepLaunch<StepPrivate>::scan_direct(vec, a, stream);
         case Res::Shared: return StepLaunch<StepShared>::scan_direct(vec, a, stream);
+        case Res::Hot: return StepLaunch<StepHot>::scan_direct(vec, a, stream);
         default: return StepLaunch<StepGlobal>::scan_direct(vec, a, stream);
     }
 }
@@ -89,6 +109,7 @@ cudaError_t launch_batch(Res mode, bool vec, const BatchArgs& a, int sm_count, c
     switch (mode) {
         case Res::Private: return StepLaunch<StepPrivate>::batch(vec, a, sm_count, stream);
         case Res::Shared: return StepLaunch<StepShared>::batch(vec, a, sm_count, stream);
+        case Res::Hot: return StepLaunch<StepHot>::batch(vec, a, sm_count, stream);
         default: return StepLaunch<StepGlobal>::batch(vec, a, sm_count, stream);
     }
 }

@@ -60,6 +60,7 @@ struct TmaConfig {
     uint32_t nb = 4;   // TMA boxes per stage: rows_per_cta of a launch must be a multiple
 };
 
+uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin);
 size_t direct_smem_bytes(Res mode, const DevTables& t);
 size_t table_smem_bytes(Res mode, const DevTables& t);   // SIZE_MAX/2 if the layout cannot hold t
 uint32_t direct_threads_per_cta();

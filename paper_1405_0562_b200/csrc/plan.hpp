@@ -26,6 +26,12 @@ struct DevTables {
     uint32_t comp_u8 = 0;
     const uint4* rep16 = nullptr;
     // aux smem image copied after the step table: [comp table if aux_comp][maps32 at aux_maps_off if aux_maps]
+    // HOT residency: renumbered window table (u16 device ids, nS x W, padded to 16 B), canonical <-> device
+    // id permutations, and the number of rows H kept in smem for this launch
+    const uint16_t* Tdev = nullptr;
+    const uint16_t* perm = nullptr;    // canonical -> device
+    const uint16_t* iperm = nullptr;   // device -> canonical
+    uint32_t hotH = 0;
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;

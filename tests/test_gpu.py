@@ -225,11 +225,17 @@ def test_batch_count_zero_is_noop(torch_cuda):
 
 
 # --------------------------------------------------------------------------- residency modes
-@pytest.mark.parametrize("rx,alpha,modes", [(*CFG1, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_L2)),
-                                            (*CFG2, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_L2)),
-                                            (*CFG4, (P.RES_SMEM_SHARED, P.RES_L2)),
-                                            (W.cfg3_regex(), None, (P.RES_L2,))])
-def test_every_residency_mode(torch_cuda, rx, alpha, modes):
+@pytest.mark.parametrize("hot_rows", [None, "7"])
+@pytest.mark.parametrize("rx,alpha,modes", [(*CFG1, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
+                                            (*CFG2, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
+                                            (*CFG4, (P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
+                                            (W.cfg3_regex(), None, (P.RES_HOT_L2, P.RES_L2))])
+def test_every_residency_mode(torch_cuda, rx, alpha, modes, hot_rows, monkeypatch):
+    """A6: every table placement gives the oracle's result; hot_rows='7'
+    keeps only 7 renumbered rows in smem so nearly every HOT lookup takes the
+    global (L2) path."""
+    if hot_rows:
+        monkeypatch.setenv("SFA_HOT_ROWS", hot_rows)
     torch = torch_cuda
     d = oracle_pair(rx, alpha)
     sfa = P.SFA(rx, alpha)
@@ -365,3 +371,23 @@ def test_every_compose_mode(torch_cuda, rx, alpha, modes):
         got = res.cpu().numpy().view(np.uint32).reshape(40, 2)
         qo, ao = d.run_batch(texts, off)
         assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all(), m
+
+
+def test_tune_residency_keeps_results(torch_cuda):
+    """The HOT ranking (static, profiled on a sample, auto-tuned) only moves
+    rows between smem and L2: results stay the oracle's."""
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    d = oracle_pair(rx, None)
+    text = W.cfg3_text(9 << 20, plant=True)
+    sfa = P.SFA(rx, None)
+    sfa.set_residency(P.RES_HOT_L2)
+    buf, v = dev(torch, text)
+    for sample in (None, v[:1 << 20], v):
+        sfa.tune_residency(sample)
+        for n in (text.size, 4_194_319, 300_001):
+            check_text(torch, sfa, d, text[:n], 1)
+    rng = np.random.default_rng(12)
+    junk = torch.from_numpy(rng.integers(0, 256, size=1 << 20, dtype=np.uint8)).cuda()
+    sfa.tune_residency(junk)          # a misleading sample: slower, never wrong
+    check_text(torch, sfa, d, text, 0)
