@@ -74,6 +74,7 @@ struct sfa_handle {
     uint32_t* drep_off = nullptr;
     uint8_t* drep = nullptr;
     void* dcomp = nullptr;                    // composition table (u8 if nS <= 256, else u16)
+    uint32_t* dpairs = nullptr;               // PRIVATE: pair words (device.cuh StepPrivate)
     uint16_t* dTdev = nullptr;                // HOT: window table renumbered by visit frequency
     uint16_t* dperm = nullptr;                // HOT: canonical -> device id
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
@@ -105,7 +106,7 @@ struct sfa_handle {
         for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
                         (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
                         (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1],
-                        (void*)dcomp, (void*)dTdev, (void*)dperm, (void*)diperm, (void*)drep16, (void*)daux[0],
+                        (void*)dcomp, (void*)dpairs, (void*)dTdev, (void*)dperm, (void*)diperm, (void*)drep16, (void*)daux[0],
                         (void*)daux[1]})
             if (p) cudaFree(p);
         if (hres) cudaFreeHost(hres);
@@ -158,6 +159,7 @@ struct sfa_handle {
         t.nD = A.nD;
         t.lo = lo;
         t.W = W;
+        t.pairs = dpairs;
         t.Tdev = dTdev;
         t.perm = dperm;
         t.iperm = diperm;
@@ -273,7 +275,17 @@ struct sfa_handle {
             R16[static_cast<size_t>(s) * W + W - 1] = T16[static_cast<size_t>(s) * C + other];
         }
         CU(upload(&dT, T16.data(), T16.size()));
-        CU(upload(&dTrange, R16.data(), R16.size()));
+        if (nS <= 1024) {  // PRIVATE pair words (padded to 16 bytes: bulk-copied)
+            std::vector<uint32_t> pw(static_cast<size_t>(W) * ((nS + 1) / 2));
+            sfa::build_private_pairs(R16.data(), nS, W, pw.data());
+            pw.resize((pw.size() + 3) & ~size_t(3), 0);
+            CU(upload(&dpairs, pw.data(), pw.size()));
+        }
+        {  // padded to 16 bytes: the TMA kernel bulk-copies it
+            std::vector<uint16_t> padded(R16);
+            padded.resize((padded.size() + 7) & ~size_t(7), 0);
+            CU(upload(&dTrange, padded.data(), padded.size()));
+        }
         CU(upload(&dcls, A.cls, 256));
         if (nD <= 32) {
             std::vector<uint8_t> m32(static_cast<size_t>(nS) * 32);
@@ -421,6 +433,8 @@ struct sfa_handle {
             a.q_in = q_in;
             a.result = d_result;
             a.stamps = nullptr;
+            static const uint32_t diag = getenv("SFA_DIAG_FLAGS") ? static_cast<uint32_t>(atoi(getenv("SFA_DIAG_FLAGS"))) : 0u;
+            a.diag = diag;
             sfa::TmaConfig cfg;
             if (!sfa::tma_choose(mode, a.t, smem_optin, &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
             // box heights (rows_per_cta / nb) are multiples of 8 rows, so every TMA
@@ -456,6 +470,20 @@ struct sfa_handle {
                 for (uint32_t b = 0; b < a.plan.ctas; ++b) {
                     for (int k = 0; k < 4; ++k) ph[k] += double(st[8 * b + k + 1] - st[8 * b + k]) / a.plan.ctas;
                     tend = std::max(tend, st[8 * b + 4]);
+                }
+                double f5 = 0, f6 = 0;
+                for (uint32_t b = 0; b < a.plan.ctas; ++b) {
+                    f5 += double(st[8 * b + 5]) / a.plan.ctas;
+                    f6 += double(st[8 * b + 6]) / a.plan.ctas;
+                }
+                fprintf(stderr, "stamps: fill(thread0)=%.0f cyc of which staging wait=%.0f cyc\n", f5, f6);
+                if (a.diag & 2) {
+                    double cold = 0, warm = 0;
+                    for (uint32_t b = 0; b < a.plan.ctas; ++b) {
+                        cold += double(st[8 * b + 5] >> 32) / a.plan.ctas;
+                        warm += double(st[8 * b + 5] & 0xffffffffull) / a.plan.ctas;
+                    }
+                    fprintf(stderr, "stamps: first build %.0f cyc, second (warm) build %.0f cyc\n", cold, warm);
                 }
                 uint64_t smax = 0;
                 for (uint32_t b = 0; b < a.plan.ctas; ++b) smax = std::max(smax, st[8 * b] - t0);

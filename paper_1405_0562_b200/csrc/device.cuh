@@ -167,6 +167,9 @@ __device__ __forceinline__ void copy16(uint4* dst, const uint4* src, size_t n16,
 // Step policies
 // ------------------------------------------------------------------------------------------
 struct StepPrivate {
+    static constexpr bool kStaged = true;  // TMA kernel: bulk-copy the pair words, expand in smem
+    static __host__ __device__ uint32_t staged_bytes(const DevTables& t) { return ((t.nS + 1) / 2 * t.W * 4 + 15) & ~15u; }
+    static __host__ __device__ const void* staged_src(const DevTables& t) { return t.pairs; }
     // Lane L's copy lives in bank L.  Cell (s, j) of lane L is the u16 at byte
     //   j*X + (s>>1)*128 + 4L + 2(s&1)          (X = 128 * ceil(nS/2))
     // and holds enc(delta_s(s, j), L) = (s'>>1)*128 + 4L + 2(s'&1), the
@@ -179,29 +182,35 @@ struct StepPrivate {
     static __host__ __device__ bool supported(const DevTables& t) { return t.nS <= 1024; }
     static __host__ __device__ __forceinline__ uint32_t enc(uint32_t s, uint32_t L) { return (s >> 1) * 128u + 4u * L + 2u * (s & 1u); }
 
-    // Expands the compact window table t.Trange [nS x W] (global) into the 32
-    // bank-private copies: cell (s, j) of lane L is the u16 at
-    // j*X + (s>>1)*128 + 4L + 2(s&1).  Each warp reads 32 consecutive cells
-    // with one coalesced load per lane, then broadcasts them with shuffles and
-    // every lane writes its own copy.  Generic stores (see k_scan_tma: they
-    // keep the smem base foldable into the hot loop's LDS).
-    __device__ static void fill(const DevTables& t, int tid, int nthreads) {
+    // The 32 bank-private copies from the lane-independent pair words
+    // t.pairs[j * npairs + p] = (a(s0') | a(s1') << 16), a(s') = (s'>>1)*128 +
+    // 2(s'&1), s0'/s1' = delta_s(2p / 2p+1, column j) (built on the host):
+    // word (j, p, L) at j*X + 128p + 4L = pairs[j*npairs + p] + 4L*0x10001.
+    // One warp per 128-byte line: a broadcast load, an add, a store.
+    // `src_s`: shared-window address of an smem copy of t.pairs (the TMA
+    // kernel stages it), else 0 (read t.pairs from global).  Generic stores
+    // (see k_scan_tma: they keep the smem base foldable into the hot loop).
+    __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t src_s) {
         const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5;
-        const uint32_t X = col_bytes(t), total = t.nS * t.W;
-        for (uint32_t base = w * 32; base < total; base += nw * 32) {
-            const uint32_t v = base + L < total ? __ldg(t.Trange + base + L) : 0u;
-            uint32_t s = base / t.W, j = base - s * t.W;
-            const uint32_t cnt = min(32u, total - base);
-            for (uint32_t i = 0; i < cnt; ++i) {
-                const uint32_t x = __shfl_sync(kFull, v, i);
-                *reinterpret_cast<uint16_t*>(dsmem + j * X + (s >> 1) * 128u + 4u * L + 2u * (s & 1u)) =
-                    static_cast<uint16_t>(enc(x, L));
-                if (++j == t.W) {
-                    j = 0;
-                    ++s;
-                }
-            }
+        const uint32_t npairs = (t.nS + 1) / 2, units = npairs * t.W, add = L * 0x40004u;
+        uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
+        // unit u = j * npairs + p lives at line j*X/128 + p = u (X = 128 * npairs)
+#pragma unroll 4
+        for (uint32_t u = w; u < units; u += nw) {
+            const uint32_t a = src_s ? lds_u32(src_s + 4 * u) : __ldg(t.pairs + u);
+            tbl[u * 32 + L] = a + add;
         }
+    }
+    // host: the pair words of Trange [nS x W]
+    static __host__ void build_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t* pairs) {
+        const uint32_t npairs = (nS + 1) / 2;
+        for (uint32_t j = 0; j < W; ++j)
+            for (uint32_t p = 0; p < npairs; ++p) {
+                const uint32_t s0 = Trange[(2 * p) * W + j];
+                const uint32_t s1 = 2 * p + 1 < nS ? Trange[(2 * p + 1) * W + j] : 0u;
+                const uint32_t a0 = enc(s0, 0), a1 = 2 * p + 1 < nS ? enc(s1, 0) : 0u;
+                pairs[j * npairs + p] = a0 | (a1 << 16);
+            }
     }
     __device__ void params(const DevTables& t) {
         X = col_bytes(t);
@@ -217,18 +226,24 @@ struct StepPrivate {
     __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t lane) const { return enc(s, lane); }
 };
 
+
 struct StepShared {
+    static constexpr bool kStaged = true;  // TMA kernel: bulk-copy the compact table, expand in smem
+    // bytes the TMA kernel stages (16-B padded: Trange is allocated padded) and their source
+    static __host__ __device__ uint32_t staged_bytes(const DevTables& t) { return (t.nS * t.W * 2 + 15) & ~15u; }
+    static __host__ __device__ const void* staged_src(const DevTables& t) { return t.Trange; }
     // one copy of the window table, u32 entries premultiplied to byte offsets:
     // state = 4*W*s (offset of row s), cell (s, j) holds 4*W*delta_s(s, j).
     uint32_t neg_lo, wmax, row;
 
     static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.nS) * t.W * 4; }
     static __host__ __device__ bool supported(const DevTables& t) { return static_cast<uint64_t>(t.nS) * t.W * 4 < (1u << 24); }
-    __device__ static void fill(const DevTables& t, int tid, int nthreads) {
+    __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t src_s) {
         uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
         const uint32_t row = 4 * t.W, total = t.nS * t.W;
 #pragma unroll 4
-        for (uint32_t i = tid; i < total; i += nthreads) tbl[i] = static_cast<uint32_t>(__ldg(t.Trange + i)) * row;
+        for (uint32_t i = tid; i < total; i += nthreads)
+            tbl[i] = (src_s ? lds_u16(src_s + 2 * i) : static_cast<uint32_t>(__ldg(t.Trange + i))) * row;
     }
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
@@ -245,13 +260,16 @@ struct StepShared {
 };
 
 struct StepGlobal {
+    static constexpr bool kStaged = false;
+    static __host__ __device__ uint32_t staged_bytes(const DevTables&) { return 0; }
+    static __host__ __device__ const void* staged_src(const DevTables&) { return nullptr; }
     // the u16 window table through L1/L2: state = s*W (element offset of row s)
     uint32_t neg_lo, wmax, W;
     const uint16_t* T;
 
     static __host__ __device__ size_t smem_bytes(const DevTables&) { return 0; }
     static __host__ __device__ bool supported(const DevTables&) { return true; }
-    __device__ static void fill(const DevTables&, int, int) {}
+    __device__ static void fill(const DevTables&, int, int, uint32_t) {}
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
@@ -268,6 +286,9 @@ struct StepGlobal {
 };
 
 struct StepHot {
+    static constexpr bool kStaged = false;
+    static __host__ __device__ uint32_t staged_bytes(const DevTables&) { return 0; }
+    static __host__ __device__ const void* staged_src(const DevTables&) { return nullptr; }
     // HOT residency (A6): SFA states renumbered by expected visit frequency
     // (host ranking, DevTables::perm / iperm); rows [0, H) of the renumbered
     // u16 window table DevTables::Tdev sit in smem, the other rows are read
@@ -279,7 +300,7 @@ struct StepHot {
 
     static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.hotH) * t.W * 2; }
     static __host__ __device__ bool supported(const DevTables& t) { return t.Tdev != nullptr && t.hotH > 0; }
-    __device__ static void fill(const DevTables& t, int tid, int nthreads) {  // the hot rows are Tdev's prefix
+    __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t) {  // hot rows = Tdev's prefix
         copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.Tdev), (smem_bytes(t) + 15) / 16, tid,
                nthreads);
     }

@@ -26,6 +26,10 @@ size_t table_smem_bytes(Res mode, const DevTables& t) {
 // HOT residency: the number of renumbered rows that fit in smem next to what
 // the launch kind needs (kind 0: the TMA scan with K=1, 32-byte stages and a
 // 2-deep ring; 1: k_scan_direct; 2: the batch kernels), capped at nS.
+void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t* pairs) {
+    StepPrivate::build_pairs(Trange, nS, W, pairs);
+}
+
 uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin) {
     size_t other = t.aux_bytes + 16;
     if (kind == 0) {
@@ -49,8 +53,21 @@ static int Sh_NB_host(int K) { return K == 1 ? Sh_NB<1>() : Sh_NB<2>(); }
 // SFA_TMA_CONFIG="K,ROWB,ring[,pf[,promo]]" forces a shape (diagnostic sweeps
 // and tests): ring 0 = as deep as fits, pf = L2 prefetch distance in 256-B
 // lines (-1 = none), promo = L2 promotion bytes of the load map (0/64/128/256).
+static bool tma_choose_once(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out, bool staged);
+
+// Prefers staging the compact table in smem (one bulk copy) when it fits
+// next to the table and a ring; else the table is built from global memory.
 bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out) {
-    const size_t tb = table_smem_bytes(mode, t);
+    return tma_choose_once(mode, t, smem_optin, out, true) || tma_choose_once(mode, t, smem_optin, out, false);
+}
+
+static bool tma_choose_once(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out, bool staged) {
+    size_t tb = table_smem_bytes(mode, t);
+    size_t sb = 0;
+    if (staged && mode == Res::Private) sb = StepPrivate::staged_bytes(t);
+    if (staged && mode == Res::Shared) sb = StepShared::staged_bytes(t);
+    if (staged && sb == 0) return false;
+    tb += sb;
     if (tb > smem_optin) return false;
     static const int cand[][2] = {{1, 32}, {2, 32}, {1, 64}, {2, 16}, {1, 16}};
     const char* env = getenv("SFA_TMA_CONFIG");
@@ -67,7 +84,7 @@ bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out)
             }
             const size_t R = static_cast<size_t>(K) * kNW * 32;
             const size_t stage = R * rowb;
-            const size_t fixed = (((K * kNW + 2) * 32 + 15) & ~15u) + 16 + (2 * kMaxRing + 1) * 8 + 1024;
+            const size_t fixed = (((K * kNW + 2) * 32 + 15) & ~15u) + 16 + (2 * kMaxRing + 3) * 8 + 1024;
             if (tb + fixed + 2 * stage > smem_optin) continue;
             uint32_t ring = static_cast<uint32_t>(std::min<size_t>(kMaxRing, (smem_optin - tb - fixed) / stage));
             if (fn) ring = std::min<uint32_t>(ring, static_cast<uint32_t>(fn));
@@ -81,6 +98,7 @@ bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out)
             // ahead of the TMA loads were evicted before use (1.6x DRAM reads).
             out->pf_lines = fpf >= -1 ? fpf : -1;
             out->promo = fpromo >= 0 ? fpromo : 0;
+            out->staged = staged;
             return true;
         }
     }

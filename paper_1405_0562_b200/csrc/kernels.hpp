@@ -24,6 +24,7 @@ struct ScanArgs {
     const uint32_t* q_in;
     sfa_result* result;
     uint64_t* stamps;     // diagnostic (SFA_DEBUG_STAMPS): 8 %globaltimer stamps per CTA, else NULL
+    uint32_t diag;        // diagnostic (SFA_DIAG_FLAGS, results invalid): 1 = skip the table build
 };
 
 struct DirectArgs {
@@ -57,10 +58,13 @@ struct TmaConfig {
     uint32_t nring = 2, rows_per_cta = 0;
     int pf_lines = 1;     // L2 prefetch distance in 256-B lines (-1: no prefetch)
     int promo = 256;      // L2 promotion of the TMA loads (bytes; 0 = none)
+    bool staged = false;  // bulk-copy the step's compact table into smem before building it
     uint32_t nb = 4;   // TMA boxes per stage: rows_per_cta of a launch must be a multiple
 };
 
 uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin);
+// Host: the PRIVATE layout's lane-independent pair words (W * ceil(nS/2) u32).
+void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t* pairs);
 size_t direct_smem_bytes(Res mode, const DevTables& t);
 size_t table_smem_bytes(Res mode, const DevTables& t);   // SIZE_MAX/2 if the layout cannot hold t
 uint32_t direct_threads_per_cta();

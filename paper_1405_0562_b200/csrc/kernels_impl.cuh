@@ -129,8 +129,9 @@ struct Comp<Step, false> {
 // bulk-copies it), cooperatively by `nthreads` threads; `t` is rebound to the
 // smem copies.
 template <class Step>
-__device__ __forceinline__ void load_tables(DevTables& t, int tid, int nthreads, bool aux_async = false) {
-    Step::fill(t, tid, nthreads);
+__device__ __forceinline__ void load_tables(DevTables& t, int tid, int nthreads, bool aux_async = false,
+                                            uint32_t compact_s = 0) {
+    Step::fill(t, tid, nthreads, compact_s);
     const uint32_t tb = static_cast<uint32_t>((Step::smem_bytes(t) + 15) & ~size_t(15));
     if (t.aux_bytes) {
         if (!aux_async)
@@ -236,7 +237,7 @@ struct TmaShape {
     static constexpr uint32_t kStageBytes = R * ROWB;
     static constexpr uint32_t kRedBytes = ((K * kNW + 2) * 32 + 15) & ~15u;
     // bytes besides the table and the ring
-    static constexpr uint32_t kFixed = kRedBytes + 16 + (2 * kMaxRing + 1) * 8 + 1024;
+    static constexpr uint32_t kFixed = kRedBytes + 16 + (2 * kMaxRing + 3) * 8 + 1024;
     // physical offset of logical stage offset `o` (rows of ROWB bytes)
     __host__ __device__ static constexpr uint32_t swz(uint32_t o) { return o ^ (((o >> 7) & kSwzMask) << 4); }
 };
@@ -248,17 +249,21 @@ struct TmaMaps {
 
 template <class Step, int K, int ROWB, bool VEC>
 __global__ void __launch_bounds__((kNW + 1) * 32, 1)
-k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_t tbl_bytes, const uint32_t nring,
-           const int pf_lines) {
+k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_t tbl_bytes, const uint32_t stage_bytes,
+           const uint32_t nring, const int pf_lines) {
     // rows of this CTA: [blockIdx.x * rc, +rc), loaded as NB boxes of br rows
     const uint32_t rc = a.plan.rows_per_cta, br = rc / Sh_NB<K>();
     using Sh = TmaShape<K, ROWB>;
     using CP = Comp<Step, VEC>;
-    uint8_t* red = dsmem + ((tbl_bytes + 15) & ~15u);
+    // [step table + aux (tbl_bytes) | compact table staging (stage_bytes) | red | flag | bars | ring]
+    uint8_t* const staging = dsmem + ((tbl_bytes + 15) & ~15u);
+    uint8_t* red = staging + stage_bytes;
     uint32_t* flag = reinterpret_cast<uint32_t*>(red + Sh::kRedBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(red + Sh::kRedBytes + 16);
-    const uint32_t abar = smem_u32(bars + 2 * kMaxRing);  // aux image landed
-    const uint32_t ring0 = (smem_u32(bars + 2 * kMaxRing + 1) + 1023) & ~1023u;
+    const uint32_t abar = smem_u32(bars + 2 * kMaxRing);      // aux image landed
+    const uint32_t cbar = smem_u32(bars + 2 * kMaxRing + 1);  // compact table landed
+    const uint32_t rbar = smem_u32(bars + 2 * kMaxRing + 2);  // compute warps built their table part
+    const uint32_t ring0 = (smem_u32(bars + 2 * kMaxRing + 3) + 1023) & ~1023u;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nstages = static_cast<uint32_t>(a.plan.L / ROWB);
@@ -270,6 +275,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
             mbar_init(empty0 + 8 * s, kNW);
         }
         mbar_init(abar, 1);
+        mbar_init(cbar, 1);
+        mbar_init(rbar, kNW);
         fence_barrier_init();
     }
     __syncthreads();
@@ -279,7 +286,10 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
             prefetch_tmap(&maps.load);
             prefetch_tmap(&maps.pref);
             const uint64_t policy = policy_evict_first();
-
+            if (stage_bytes) {  // the compact table, expanded in smem by the compute warps
+                mbar_expect_tx(cbar, stage_bytes);
+                bulk_g2s(smem_u32(staging), Step::staged_src(a.t), stage_bytes, cbar);
+            }
             if (a.t.aux_bytes) {  // composition aux image: needed only at the fold
                 const uint32_t tb = static_cast<uint32_t>((Step::smem_bytes(a.t) + 15) & ~size_t(15));
                 mbar_expect_tx(abar, a.t.aux_bytes);
@@ -292,6 +302,10 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
             constexpr uint32_t kStagesPerLine = kLine / ROWB;
             uint32_t slot = 0, phase = 0;
             for (uint32_t i = 0; i < nstages; ++i) {
+                // Only the first stage is requested before the compute warps
+                // have built the table: their table reads would otherwise
+                // queue behind the whole ring fill (~20 MB device-wide).
+                if (i == 1) mbar_wait(rbar, 0);
                 if (i >= nring) mbar_wait(empty0 + 8 * slot, phase ^ 1);
                 mbar_expect_tx(full0 + 8 * slot, rc * ROWB);
                 const uint32_t dst = ring0 + slot * Sh::kStageBytes;
@@ -321,9 +335,25 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     // copy through generic stores (not a bulk copy): with it ptxas keeps the
     // smem base in a uniform register and folds it into every LDS.U16 of the
     // hot loop ([R+UR]), one IADD per byte less.
-    load_tables<Step>(t, threadIdx.x, kNW * 32, true);
+    const long long c0 = clock64();
+    if (stage_bytes) mbar_wait(cbar, 0);
+    const long long cw = clock64();
+    if (!(a.diag & 1))
+        load_tables<Step>(t, threadIdx.x, kNW * 32, true, stage_bytes ? smem_u32(staging) : 0u);
+    long long c1 = clock64();
+    if (a.diag & 2) {  // diagnostic: time a second, warm build
+        const long long c2 = clock64();
+        load_tables<Step>(t, threadIdx.x, kNW * 32, true, stage_bytes ? smem_u32(staging) : 0u);
+        c1 = c0 + (clock64() - c2) + ((c2 - c0) << 32);  // stamp[5]: cold cycles << 32 | warm cycles
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(rbar);
     bar_compute(kNW * 32);
-    if (stamp) stamp[1] = globaltimer();
+    if (stamp) {
+        stamp[1] = globaltimer();
+        stamp[5] = static_cast<uint64_t>(c1 - c0);           // thread 0's own fill, SM cycles
+        stamp[6] = static_cast<uint64_t>(cw - c0);           // wait for the staged compact table
+    }
 
     // The last CTA also runs the ragged tail [tail_start, n) (< L + 16 bytes),
     // split over its compute threads; its value goes to slot gridDim.x (stored
@@ -598,7 +628,8 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s
     using Sh = TmaShape<K, ROWB>;
     auto kern = k_scan_tma<Step, K, ROWB, VEC>;
     const uint32_t tbytes = static_cast<uint32_t>(table_bytes<Step>(a.t) + a.t.aux_bytes);
-    const size_t smem = tbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
+    const uint32_t sbytes = cfg.staged ? Step::staged_bytes(a.t) : 0u;
+    const size_t smem = tbytes + sbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     EncodeFn enc = encode_fn();
@@ -632,7 +663,7 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    return launch_pdl(kern, a.plan.ctas, (kNW + 1) * 32, smem, stream, maps, a, tbytes, cfg.nring, cfg.pf_lines);
+    return launch_pdl(kern, a.plan.ctas, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring, cfg.pf_lines);
 }
 
 template <class Step, bool VEC>

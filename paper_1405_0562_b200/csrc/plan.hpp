@@ -14,6 +14,7 @@ struct DevTables {
     const uint16_t* T = nullptr;        // nS * C   next SFA id per (state, class)
     const uint8_t* cls = nullptr;       // 256      byte -> class
     const uint16_t* Trange = nullptr;   // nS * W   next SFA id per (state, window column)
+    const uint32_t* pairs = nullptr;    // PRIVATE: W * ceil(nS/2) lane-independent pair words (device.cuh)
     const uint8_t* maps32 = nullptr;    // nS * 32  f_s(q) for |D| <= 32 (identity-padded)
     const uint16_t* maps16 = nullptr;   // nS * nD  f_s(q) (any |D|; used to apply f_fin to q_in != q0)
     const uint32_t* img0 = nullptr;     // nS       f_s(q0)
