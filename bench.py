@@ -397,7 +397,11 @@ def main():
     info = sfa.info()
     sm_hz = (clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    smem_peak = nsm * 32 * sm_hz / 1e9       # GB/s of text at one conflict-free LDS wavefront per byte
+    # shared-memory ceilings: one conflict-free LDS wavefront per 32
+    # lookups (1 lookup per text byte) -> 32 B/clk/SM; with the staged text
+    # (TMA write + LDS.128 read, 1/128 wavefront each per byte) -> 21.33 B/clk/SM
+    smem_peak = nsm * 32 * sm_hz / 1e9
+    smem_dp_peak = nsm * (1.0 / (1 / 32 + 2 / 128)) * sm_hz / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -411,8 +415,10 @@ def main():
                      "frac": per_rank_gbs / peak, "traffic": ncu_traffic(cfg),
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "kernel": "k_scan_tma (one launch per step; achieved = text bytes / launch time)",
-                     "smem_lookup_peak_gbs": smem_peak,
-                     "frac_of_min_roofline": per_rank_gbs / min(peak, smem_peak)},
+                     "smem_lookup_peak_gbs": smem_peak, "smem_datapath_peak_gbs": smem_dp_peak,
+                     "sm_mhz_for_smem_peaks": sm_hz / 1e6,
+                     "frac_of_min_roofline": per_rank_gbs / min(peak, smem_peak),
+                     "frac_of_min_datapath": per_rank_gbs / min(peak, smem_dp_peak)},
         "clocks": clocks,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(text.size), "d2h_bytes_per_step": 8,
                 "api": "sfa_match_host (pinned host text, 64 MiB slices copied and matched in a pipeline)"},

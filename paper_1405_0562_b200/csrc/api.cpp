@@ -485,6 +485,17 @@ struct sfa_handle {
                     }
                     fprintf(stderr, "stamps: first build %.0f cyc, second (warm) build %.0f cyc\n", cold, warm);
                 }
+                {
+                    uint64_t e0 = UINT64_MAX, e1 = 0, m0 = UINT64_MAX, m1 = 0;
+                    for (uint32_t b = 0; b < a.plan.ctas; ++b) {
+                        e0 = std::min(e0, st[8 * b + 2]);
+                        e1 = std::max(e1, st[8 * b + 2]);
+                        m0 = std::min(m0, st[8 * b + 1]);
+                        m1 = std::max(m1, st[8 * b + 1]);
+                    }
+                    fprintf(stderr, "stamps: scan-start spread %.2fus, scan-end spread %.2fus\n", (m1 - m0) / 1e3,
+                            (e1 - e0) / 1e3);
+                }
                 uint64_t smax = 0;
                 for (uint32_t b = 0; b < a.plan.ctas; ++b) smax = std::max(smax, st[8 * b] - t0);
                 fprintf(stderr, "stamps: ctas=%u start-spread=%.2fus tables=%.2fus scan=%.2fus blockfold=%.2fus epi=%.2fus total=%.2fus L=%llu rc=%u\n",
