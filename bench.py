@@ -245,6 +245,66 @@ def extra_config(torch, P, cfg, stream, steps, warmup, peak):
             "sfa_states": info["sfa_states"], "dfa_states": info["dfa_states"]}
 
 
+def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, peak_kind):
+    """--shard: ONE text split over the ranks (strong scaling).  Per step every
+    rank runs sfa_match_map on its shard, the ranks all-gather the |D|-entry
+    mappings (NCCL) and fold them in text order (sfa_combine_maps)."""
+    from paper_1405_0562_b200 import parallel as PL
+    a, b = PL.shard_bounds(text.size, world, rank)
+    nD = sfa.info()["dfa_states"]
+    with torch.cuda.stream(stream):
+        dshard = torch.from_numpy(text[a:b]).cuda()
+        local_map = torch.empty(nD, dtype=torch.int32, device="cuda")
+        res = torch.zeros(2, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+
+    def step():
+        with torch.cuda.stream(stream):
+            sfa.match_map(dshard, local_map, stream)
+            if world > 1:
+                maps = PL.gather_maps(local_map)
+            else:
+                maps = local_map.view(1, -1)
+            sfa.combine_maps(maps, maps.shape[0], res, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    q, acc = res.cpu().tolist()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    gbs = text.size / (ms_per_step * 1e-3) / 1e9
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic (seeded, DESIGN.md input recipe)",
+        "config": {"workload": CONFIG_NAMES[args.config], "bytes_per_step": int(text.size),
+                   "parallelism": f"text sharded over {world} ranks; |D|-entry map all-gather (NCCL)",
+                   "result": [q, bool(acc)]},
+        "roofline": {"bound": "hbm", "achieved": gbs / world, "peak": peak, "unit": "GB/s",
+                     "frac": gbs / world / peak, "traffic": None, "peak_kind": f"{peak_kind} copy bandwidth (per GPU)"},
+        "clocks": clk.summary(), "gpu_launches": 2 * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def bench_batch(args, torch, P, sfa, rx, alpha, batch, stream, world, rank, local, peak, peak_kind, peaks):
     """Config 5 as the timed workload: one step = sfa_match_batch over the whole batch."""
     texts, off = batch
@@ -306,6 +366,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-bytes", type=int, default=64 << 20)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="split ONE text over the ranks (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -328,6 +389,8 @@ def main():
     stream = torch.cuda.Stream()
     if cfg == 5:
         return bench_batch(args, torch, P, sfa, rx, alpha, text, stream, world, rank, local, peak, peak_kind, peaks)
+    if args.shard:
+        return bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, peak_kind)
     with torch.cuda.stream(stream):
         dtext = torch.from_numpy(text).cuda()
         res = torch.zeros(2, dtype=torch.int32, device="cuda")

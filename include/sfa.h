@@ -159,6 +159,26 @@ SFA_API int sfa_match_batch(const sfa_handle* h, const uint8_t* d_texts, const u
                     size_t count, sfa_stream_t stream, sfa_result* d_results);
 
 /*
+ * Sharded matching (one text split over several GPUs / streams; Theorem 3,
+ * PAPER.md:469-479, and Lemma 1).
+ *
+ * sfa_match_map -- like sfa_match_async, but writes the text's whole SFA
+ * state as its mapping: d_map[q] = f_text(q) = delta^_d(q, text) for every
+ * DFA state q (|D| = sfa_info().dfa_states u32 entries, device, caller-owned).
+ * Async, stream-ordered.  n == 0 writes the identity (f_I).  CAPACITY if the
+ * handle keeps no mapping table (|S| * |D| > 2^29).
+ *
+ * sfa_combine_maps -- the reduction over `count` shard mappings in text
+ * order (d_maps: count * |D| u32, device; e.g. an all-gather of every rank's
+ * sfa_match_map): q = q0; q = d_maps[r * |D| + q] for r = 0..count-1, the
+ * sequential reduction of Alg. 5 (right column); writes
+ * (q, [q in F_d]) to d_result (device).  Async, stream-ordered.
+ */
+SFA_API int sfa_match_map(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_stream_t stream, uint32_t* d_map);
+SFA_API int sfa_combine_maps(const sfa_handle* h, const uint32_t* d_maps, size_t count, sfa_stream_t stream,
+                     sfa_result* d_result);
+
+/*
  * sfa_match_host -- end-to-end call on a HOST buffer (pinned or pageable):
  * the text is copied to the device in slices on `stream` while earlier slices
  * are matched (each slice yields one SFA state; slices compose by Lemma 1,

@@ -56,7 +56,7 @@ class sfa_info_t(C.Structure):
 
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
-           "sfa_tune_residency",
+           "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps",
            "sfa_export_dfa", "sfa_export_sfa")
 
 _lib = None
@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
         L.sfa_set_residency.argtypes = [vp, C.c_int]
         L.sfa_set_compose.argtypes = [vp, C.c_int]
         L.sfa_tune_residency.argtypes = [vp, vp, C.c_size_t, vp]
+        L.sfa_match_map.argtypes = [vp, vp, C.c_size_t, vp, vp]
+        L.sfa_combine_maps.argtypes = [vp, vp, C.c_size_t, vp, vp]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
         for f in EXPORTS:
@@ -166,6 +168,17 @@ def sfa_match_batch(h: int, d_texts, d_offsets, count: int, d_results, stream=No
     if count == 0:
         return
     _check(lib().sfa_match_batch(h, _dptr(d_texts), _dptr(d_offsets), count, _stream(stream), _dptr(d_results)))
+
+
+def sfa_match_map(h: int, d_text, d_map, n: int | None = None, stream=None):
+    """Stream-ordered: d_map (device, |D| x uint32) <- f_text(q) for every DFA state q."""
+    n = _nbytes(d_text) if n is None else n
+    _check(lib().sfa_match_map(h, _dptr(d_text) if n else None, n, _stream(stream), _dptr(d_map)))
+
+
+def sfa_combine_maps(h: int, d_maps, count: int, d_result, stream=None):
+    """Stream-ordered: d_result (device, 2 x uint32) <- (q, accept) after the shard maps in order."""
+    _check(lib().sfa_combine_maps(h, _dptr(d_maps) if count else None, count, _stream(stream), _dptr(d_result)))
 
 
 def sfa_match_host(h: int, h_text, stream=None):
@@ -259,6 +272,12 @@ class SFA:
 
     def match_batch(self, d_texts, d_offsets, count, d_results, stream=None):
         return sfa_match_batch(self.h, d_texts, d_offsets, count, d_results, stream)
+
+    def match_map(self, d_text, d_map, stream=None):
+        return sfa_match_map(self.h, d_text, d_map, None, stream)
+
+    def combine_maps(self, d_maps, count, d_result, stream=None):
+        return sfa_combine_maps(self.h, d_maps, count, d_result, stream)
 
     def match_host(self, h_text, stream=None):
         return sfa_match_host(self.h, h_text, stream)

@@ -401,7 +401,7 @@ struct sfa_handle {
 
     // One text on the device -> result (device), stream-ordered.
     int launch_one(const uint8_t* d_text, uint64_t n, cudaStream_t stream, const uint32_t* q_in, sfa_result* d_result,
-                   uint64_t force_pieces = 0, uint32_t* piece_ids = nullptr) {
+                   uint64_t force_pieces = 0, uint32_t* piece_ids = nullptr, uint32_t* map_out = nullptr) {
         const bool direct = force_pieces > 0 || n < kTmaMin;
         sfa::Res mode;
         int rc = resolve(direct ? 1 : 0, &mode);
@@ -421,6 +421,7 @@ struct sfa_handle {
             a.q_in = q_in;
             a.result = d_result;
             a.piece_ids = piece_ids;
+            a.map_out = map_out;
             const uint64_t ctas = (a.npieces + sfa::direct_threads_per_cta() - 1) / sfa::direct_threads_per_cta();
             if (ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "too many chunks");
             e = sfa::launch_scan_direct(mode, vec(), a, stream);
@@ -433,6 +434,7 @@ struct sfa_handle {
             a.q_in = q_in;
             a.result = d_result;
             a.stamps = nullptr;
+            a.map_out = map_out;
             static const uint32_t diag = getenv("SFA_DIAG_FLAGS") ? static_cast<uint32_t>(atoi(getenv("SFA_DIAG_FLAGS"))) : 0u;
             a.diag = diag;
             sfa::TmaConfig cfg;
@@ -742,6 +744,41 @@ int sfa_match_chunked(const sfa_handle* hc, const uint8_t* d_text, size_t n, uin
     *final_state = h->hres[0].final_state;
     *accept = static_cast<int>(h->hres[0].accept);
     return SFA_OK;
+}
+
+int sfa_match_map(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_stream_t stream, uint32_t* d_map) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !d_map) return fail(SFA_ERR_INVALID_ARG, "NULL handle or map");
+    if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    if (!h->vec() && !h->dmaps16) return fail(SFA_ERR_CAPACITY, "mapping table too large for sfa_match_map");
+    if (n == 0) {  // f_eps = identity
+        std::vector<uint32_t> id(h->A.nD);
+        for (uint32_t q = 0; q < h->A.nD; ++q) id[q] = q;
+        CU(cudaMemcpyAsync(d_map, id.data(), id.size() * 4, cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));
+        return h->end(s);
+    }
+    rc = h->launch_one(d_text, n, s, nullptr, nullptr, 0, nullptr, d_map);
+    if (rc) return rc;
+    return h->end(s);
+}
+
+int sfa_combine_maps(const sfa_handle* hc, const uint32_t* d_maps, size_t count, sfa_stream_t stream,
+                     sfa_result* d_result) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !d_result || (count > 0 && !d_maps)) return fail(SFA_ERR_INVALID_ARG, "NULL argument");
+    if (count > 0xffffffffull) return fail(SFA_ERR_INVALID_ARG, "count too large");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    cudaError_t e = sfa::launch_combine_maps(d_maps, static_cast<uint32_t>(count), h->A.nD, h->dfinal, d_result, s);
+    if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+    return h->end(s);
 }
 
 int sfa_match_batch(const sfa_handle* hc, const uint8_t* d_texts, const uint64_t* d_offsets, size_t count,

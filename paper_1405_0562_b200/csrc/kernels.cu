@@ -105,6 +105,20 @@ static bool tma_choose_once(Res mode, const DevTables& t, size_t smem_optin, Tma
     return false;
 }
 
+__global__ void k_combine_maps(const uint32_t* __restrict__ maps, uint32_t count, uint32_t nD,
+                               const uint8_t* __restrict__ dfinal, sfa_result* result) {
+    uint32_t q = 0;  // q0 (C3)
+    for (uint32_t r = 0; r < count; ++r) q = maps[static_cast<size_t>(r) * nD + q];
+    result->final_state = q;
+    result->accept = dfinal[q];
+}
+
+cudaError_t launch_combine_maps(const uint32_t* maps, uint32_t count, uint32_t nD, const uint8_t* dfinal,
+                                sfa_result* result, cudaStream_t stream) {
+    k_combine_maps<<<1, 1, 0, stream>>>(maps, count, nD, dfinal, result);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
     switch (mode) {
         case Res::Private: return StepLaunch<StepPrivate>::scan_tma(vec, a, cfg, stream);

@@ -25,6 +25,7 @@ struct ScanArgs {
     sfa_result* result;
     uint64_t* stamps;     // diagnostic (SFA_DEBUG_STAMPS): 8 %globaltimer stamps per CTA, else NULL
     uint32_t diag;        // diagnostic (SFA_DIAG_FLAGS, results invalid): 1 = skip the table build
+    uint32_t* map_out;    // optional: f_fin(q) for every DFA state q (nD u32, device)
 };
 
 struct DirectArgs {
@@ -36,6 +37,7 @@ struct DirectArgs {
     const uint32_t* q_in;
     sfa_result* result;
     uint32_t* piece_ids;  // optional, npieces entries (device SFA ids)
+    uint32_t* map_out;    // optional: f_fin(q) for every DFA state q (nD u32, device)
 };
 
 struct BatchArgs {
@@ -78,6 +80,11 @@ struct StepLaunch {
     static cudaError_t scan_direct(bool vec, const DirectArgs& a, cudaStream_t s);
     static cudaError_t batch(bool vec, const BatchArgs& a, int sm_count, cudaStream_t s);
 };
+
+// Sequential reduction over shard mappings (Alg. 5, right column):
+// q = q0 = 0; q = maps[r * nD + q] for r = 0..count-1; result = (q, dfinal[q]).
+cudaError_t launch_combine_maps(const uint32_t* maps, uint32_t count, uint32_t nD, const uint8_t* dfinal,
+                                sfa_result* result, cudaStream_t stream);
 
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);

@@ -145,7 +145,7 @@ __device__ __forceinline__ void load_tables(DevTables& t, int tid, int nthreads,
 template <class Step, bool VEC>
 __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& sc, sfa_result* result,
                               const uint8_t* text, uint64_t head, uint32_t nslots, const uint32_t* q_in,
-                              int nwarps, uint8_t* red, uint32_t* flag) {
+                              int nwarps, uint8_t* red, uint32_t* flag, uint32_t* map_out) {
     using CP = Comp<Step, VEC>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nthreads = nwarps * 32;
@@ -175,9 +175,17 @@ __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& 
         acc = CP::fold_slots(S, t, red, nfold, acc, false);
         const uint32_t q0 = q_in ? *q_in : 0u;
         const uint32_t q = CP::q_final(t, acc, q0);
+        if (map_out)  // the whole mapping f_fin (sfa_match_map: shards of a text compose by Lemma 1)
+            for (uint32_t b = 0; b < t.nD; b += 32) {
+                const uint32_t qq = b + lane;
+                const uint32_t v = CP::q_final(t, acc, qq < t.nD ? qq : 0u);
+                if (qq < t.nD) map_out[qq] = v;
+            }
         if (lane == 0) {
-            result->final_state = q;
-            result->accept = t.dfinal[q];
+            if (result) {
+                result->final_state = q;
+                result->accept = t.dfinal[q];
+            }
             *sc.ticket = 0;  // ready for the next launch (stream-ordered)
         }
     }
@@ -437,7 +445,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     }
     bar_compute(kNW * 32);
     if (stamp) stamp[3] = globaltimer();
-    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, a.plan.head, gridDim.x + 1, a.q_in, kNW, red, flag);
+    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, a.plan.head, gridDim.x + 1, a.q_in, kNW, red, flag,
+                             a.map_out);
     if (stamp) stamp[4] = globaltimer();
 }
 
@@ -475,7 +484,7 @@ k_scan_direct(const DirectArgs a) {
     const uint32_t acc = block_fold<Step, VEC>(S, t, s, kDirectWarps, red);
     if (warp == 0) store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
     bar_compute(kDirectWarps * 32);
-    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, 0, gridDim.x, a.q_in, kDirectWarps, red, flag);
+    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, 0, gridDim.x, a.q_in, kDirectWarps, red, flag, a.map_out);
 }
 
 // ------------------------------------------------------------------------------------------
