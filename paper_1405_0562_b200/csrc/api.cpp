@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -78,6 +79,12 @@ struct sfa_handle {
     uint16_t* dTdev = nullptr;                // HOT: window table renumbered by visit frequency
     uint16_t* dperm = nullptr;                // HOT: canonical -> device id
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
+    uint16_t *dfam = nullptr, *dfg = nullptr, *dftab = nullptr, *ddwin = nullptr;  // FACTORED step tables
+    uint32_t dwin_bytes = 0, nfam = 0;
+    bool factor_on = [] {  // SFA_FACTOR=0 disables the factored step (A/B measurements, tests)
+        const char* e = getenv("SFA_FACTOR");
+        return !(e && e[0] == '0');
+    }();
     uint4* drep16 = nullptr;                  // rep(s) slots (depth <= 15)
     uint32_t* daux[2] = {nullptr, nullptr};   // aux smem images: [0] comp (TABLE), [1] maps32 (VEC)
     uint32_t aux_bytes[2] = {0, 0};
@@ -106,7 +113,7 @@ struct sfa_handle {
         for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
                         (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
                         (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1],
-                        (void*)dcomp, (void*)dpairs, (void*)dTdev, (void*)dperm, (void*)diperm, (void*)drep16, (void*)daux[0],
+                        (void*)dcomp, (void*)dpairs, (void*)dTdev, (void*)dfam, (void*)dfg, (void*)dftab, (void*)ddwin, (void*)dperm, (void*)diperm, (void*)drep16, (void*)daux[0],
                         (void*)daux[1]})
             if (p) cudaFree(p);
         if (hres) cudaFreeHost(hres);
@@ -163,6 +170,13 @@ struct sfa_handle {
         t.Tdev = dTdev;
         t.perm = dperm;
         t.iperm = diperm;
+        if (mode == sfa::Res::Hot && dfam && factor_on) {
+            t.fact_fam = dfam;
+            t.fact_g = dfg;
+            t.fact_tab = dftab;
+            t.dwin = ddwin;
+            t.dwin_bytes = dwin_bytes;
+        }
         t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin) : 0;
         return t;
     }
@@ -229,6 +243,89 @@ struct sfa_handle {
         CU(cudaMemcpy(dTdev, Td.data(), Td.size() * 2, cudaMemcpyHostToDevice));
         CU(cudaMemcpy(dperm, p16.data(), nS * 2, cudaMemcpyHostToDevice));
         CU(cudaMemcpy(diperm, ip16.data(), nS * 2, cudaMemcpyHostToDevice));
+        return SFA_OK;
+    }
+
+    // FACTORED step tables.  A DFA state a is absorbing if
+    // delta(a, b) = a for every byte.  An SFA state s is factorable if all q
+    // with f_s(q) not absorbing share one image g_s; its family is f_s with
+    // those q marked.  fact_tab[family][g] = the SFA state (family, g).  Built
+    // when most states are factorable and the tables are small.
+    int upload_fact() {
+        const uint32_t nS = A.nS, nD = A.nD;
+        if (static_cast<uint64_t>(nD) * W * 2 > 32768) return SFA_OK;
+        std::vector<uint8_t> absorbing(nD, 1);
+        for (uint32_t q = 0; q < nD; ++q)
+            for (int b = 0; b < 256 && absorbing[q]; ++b)
+                if (A.dfa[static_cast<size_t>(q) * 256 + b] != q) absorbing[q] = 0;
+        uint32_t abs0 = UINT32_MAX;
+        for (uint32_t q = 0; q < nD; ++q)
+            if (absorbing[q]) {
+                abs0 = q;
+                break;
+            }
+        std::vector<uint16_t> fam(nS, 0xffff), g(nS, 0);
+        std::map<std::vector<uint16_t>, uint32_t> fams;
+        uint32_t nfact = 0;
+        for (uint32_t st = 0; st < nS; ++st) {
+            const uint32_t* m = &A.maps[static_cast<size_t>(st) * nD];
+            uint32_t gg = UINT32_MAX;
+            bool ok = true;
+            std::vector<uint16_t> key(nD);
+            for (uint32_t q = 0; q < nD && ok; ++q) {
+                if (absorbing[m[q]]) {
+                    key[q] = static_cast<uint16_t>(m[q]);
+                } else {
+                    key[q] = 0xffff;
+                    if (gg == UINT32_MAX) gg = m[q];
+                    else if (gg != m[q]) ok = false;
+                }
+            }
+            if (!ok) continue;
+            if (gg == UINT32_MAX) {  // frozen: every image absorbing
+                if (abs0 == UINT32_MAX) continue;
+                gg = abs0;
+            }
+            auto it = fams.emplace(key, static_cast<uint32_t>(fams.size())).first;
+            fam[st] = static_cast<uint16_t>(it->second);
+            g[st] = static_cast<uint16_t>(gg);
+            ++nfact;
+        }
+        if (nfact * 2 < nS || fams.size() >= 0xffff || static_cast<uint64_t>(fams.size()) * nD > (8u << 20)) return SFA_OK;
+        std::vector<uint16_t> tab(fams.size() * static_cast<size_t>(nD), 0xffff);
+        for (uint32_t st = 0; st < nS; ++st)
+            if (fam[st] != 0xffff) tab[static_cast<size_t>(fam[st]) * nD + g[st]] = static_cast<uint16_t>(st);
+        // g reaching an absorbing state a freezes the mapping: (family, a) is the
+        // frozen state whose mapping is the family's with the marked q sent to a
+        for (const auto& kv : fams) {
+            bool marked = false;
+            for (uint16_t x : kv.first) marked |= x == 0xffff;
+            if (!marked) continue;
+            for (uint32_t a = 0; a < nD; ++a) {
+                if (!absorbing[a]) continue;
+                std::vector<uint16_t> k2(kv.first);
+                for (uint16_t& x : k2)
+                    if (x == 0xffff) x = static_cast<uint16_t>(a);
+                auto f2 = fams.find(k2);
+                if (f2 != fams.end())
+                    tab[static_cast<size_t>(kv.second) * nD + a] = tab[static_cast<size_t>(f2->second) * nD + abs0];
+            }
+        }
+        // DFA window table, entries premultiplied by 2W (StepDfa)
+        const uint32_t ob = lo + W - 1 < 256 ? lo + W - 1 : lo - 1;  // a byte outside the window (class `other`)
+        std::vector<uint16_t> dw((static_cast<size_t>(nD) * W + 7) & ~size_t(7), 0);
+        for (uint32_t q = 0; q < nD; ++q)
+            for (uint32_t j = 0; j < W; ++j) {
+                const uint32_t b = j + 1 < W ? lo + j : ob;
+                dw[static_cast<size_t>(q) * W + j] = static_cast<uint16_t>(A.dfa[static_cast<size_t>(q) * 256 + b] * 2 * W);
+            }
+        CU(upload(&dfam, fam.data(), fam.size()));
+        CU(upload(&dfg, g.data(), g.size()));
+        CU(upload(&dftab, tab.data(), tab.size()));
+        CU(upload(&ddwin, dw.data(), dw.size()));
+        dwin_bytes = static_cast<uint32_t>(dw.size() * 2);
+        nfam = static_cast<uint32_t>(fams.size());
+        dev_bytes += fam.size() * 4 + tab.size() * 2 + dw.size() * 2;
         return SFA_OK;
     }
 
@@ -344,7 +441,9 @@ struct sfa_handle {
         }
         // HOT residency tables (AUTO uses them when neither smem layout holds the whole table)
         {
-            const int rc = upload_hot(nullptr, 0);
+            int rc = upload_hot(nullptr, 0);
+            if (rc) return rc;
+            rc = upload_fact();
             if (rc) return rc;
             dev_bytes += static_cast<uint64_t>(nS) * W * 2 + 4ull * nS;
         }

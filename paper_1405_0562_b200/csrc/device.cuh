@@ -167,6 +167,7 @@ __device__ __forceinline__ void copy16(uint4* dst, const uint4* src, size_t n16,
 // Step policies
 // ------------------------------------------------------------------------------------------
 struct StepPrivate {
+    static constexpr bool kFactor = false;
     static constexpr bool kStaged = true;  // TMA kernel: bulk-copy the pair words, expand in smem
     static __host__ __device__ uint32_t staged_bytes(const DevTables& t) { return ((t.nS + 1) / 2 * t.W * 4 + 15) & ~15u; }
     static __host__ __device__ const void* staged_src(const DevTables& t) { return t.pairs; }
@@ -228,6 +229,7 @@ struct StepPrivate {
 
 
 struct StepShared {
+    static constexpr bool kFactor = false;
     static constexpr bool kStaged = true;  // TMA kernel: bulk-copy the compact table, expand in smem
     // bytes the TMA kernel stages (16-B padded: Trange is allocated padded) and their source
     static __host__ __device__ uint32_t staged_bytes(const DevTables& t) { return (t.nS * t.W * 2 + 15) & ~15u; }
@@ -260,6 +262,7 @@ struct StepShared {
 };
 
 struct StepGlobal {
+    static constexpr bool kFactor = false;
     static constexpr bool kStaged = false;
     static __host__ __device__ uint32_t staged_bytes(const DevTables&) { return 0; }
     static __host__ __device__ const void* staged_src(const DevTables&) { return nullptr; }
@@ -298,11 +301,15 @@ struct StepHot {
     const uint16_t* perm;
     const uint16_t* iperm;
 
-    static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.hotH) * t.W * 2; }
+    static constexpr bool kFactor = true;  // kernels may switch warps to the factored step (StepDfa)
+    static __host__ __device__ size_t hot_bytes(const DevTables& t) { return (static_cast<size_t>(t.hotH) * t.W * 2 + 15) & ~size_t(15); }
+    static __host__ __device__ size_t smem_bytes(const DevTables& t) { return hot_bytes(t) + t.dwin_bytes; }
     static __host__ __device__ bool supported(const DevTables& t) { return t.Tdev != nullptr && t.hotH > 0; }
     __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t) {  // hot rows = Tdev's prefix
-        copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.Tdev), (smem_bytes(t) + 15) / 16, tid,
-               nthreads);
+        copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.Tdev), hot_bytes(t) / 16, tid, nthreads);
+        if (t.dwin_bytes)
+            copy16(reinterpret_cast<uint4*>(dsmem + hot_bytes(t)), reinterpret_cast<const uint4*>(t.dwin), t.dwin_bytes / 16,
+                   tid, nthreads);
     }
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
@@ -330,6 +337,35 @@ struct StepHot {
     __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return __ldg(iperm + st); }
     __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t) const { return __ldg(perm + s); }
 };
+
+// The factored SFA step.  If every q that f does not send to an absorbing DFA
+// state goes to one state g, then f . delta^c (Def. 3) keeps the
+// absorbing part and sends those q to delta(g, c): the SFA state is (family,
+// g) and one transition is one lookup in the DFA window table (smem, after the
+// hot rows).  state = 2W * g.  Entered per warp once all its lanes' states are
+// factorable (k_scan_tma, k_batch_scan); converted back to the canonical SFA
+// id through DevTables::fact_tab at the end of the chunk.
+struct StepDfa {
+    uint32_t neg_lo, wmax, off;
+    __device__ void params(const DevTables& t) {
+        neg_lo = 0u - t.lo;
+        wmax = t.W - 1;
+        off = static_cast<uint32_t>(StepHot::hot_bytes(t));
+    }
+    __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
+        return ld_tbl_u16(off + st + 2 * window_col(byte, neg_lo, wmax));
+    }
+};
+
+// SFA id -> factored state (2W * g) and family; false if s is not factorable
+__device__ __forceinline__ bool fact_from_id(const DevTables& t, uint32_t s, uint32_t& fam, uint32_t& g2w) {
+    fam = __ldg(t.fact_fam + s);
+    g2w = static_cast<uint32_t>(__ldg(t.fact_g + s)) * 2u * t.W;
+    return fam != 0xffffu;
+}
+__device__ __forceinline__ uint32_t fact_to_id(const DevTables& t, uint32_t fam, uint32_t g2w) {
+    return __ldg(t.fact_tab + fam * t.nD + g2w / (2u * t.W));
+}
 
 // 4 text bytes of one word, in text order (little-endian)
 template <class Step>

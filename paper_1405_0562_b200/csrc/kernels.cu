@@ -31,7 +31,7 @@ void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32
 }
 
 uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin) {
-    size_t other = t.aux_bytes + 16;
+    size_t other = t.aux_bytes + t.dwin_bytes + 32;
     if (kind == 0) {
         using Sh = TmaShape<1, 32>;
         other += Sh::kFixed + 2 * Sh::kStageBytes;

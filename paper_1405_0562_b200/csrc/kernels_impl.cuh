@@ -255,6 +255,54 @@ struct TmaMaps {
     CUtensorMap pref;      // box [256 x BR], L2 prefetch only
 };
 
+// The consumer side of the stage ring: full/empty mbarriers, slot, phase.
+struct Ring {
+    uint32_t full0, empty0, base, n, slot, phase;
+};
+
+// Stages [i0, i1) of the K rows of this thread through `S` (Alg. 5 lines 3-5):
+// wait for the stage, read each row's ROWB bytes (swizzled LDS.128), step the
+// K chains byte by byte (interleaved for ILP), release the slot.
+template <int K, int ROWB, class Sh, class StepT>
+__device__ __forceinline__ void scan_stages(const StepT& S, uint32_t (&st)[K], const uint32_t (&rsrc)[K][ROWB / 16],
+                                            Ring& ring, uint32_t i0, uint32_t i1, uint32_t lane) {
+    for (uint32_t i = i0; i < i1; ++i) {
+        mbar_wait(ring.full0 + 8 * ring.slot, ring.phase);
+        const uint32_t src = ring.base + ring.slot * Sh::kStageBytes;
+        uint4 v[K][ROWB / 16];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int c = 0; c < ROWB / 16; ++c) v[k][c] = lds_v4(src + rsrc[k][c]);
+#pragma unroll
+        for (int c = 0; c < ROWB / 16; ++c) {
+            const uint32_t* w[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) w[k] = reinterpret_cast<const uint32_t*>(&v[k][c]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<0>(w[k][q]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<1>(w[k][q]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<2>(w[k][q]));
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
+            }
+        }
+        // Release the slot only now: every lane has consumed its loaded bytes,
+        // so no LDS of this stage can still be in flight when the producer's
+        // next TMA write lands (an arrive right after issuing the LDS raced).
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ring.empty0 + 8 * ring.slot);
+        if (++ring.slot == ring.n) {
+            ring.slot = 0;
+            ring.phase ^= 1;
+        }
+    }
+}
+
 template <class Step, int K, int ROWB, bool VEC>
 __global__ void __launch_bounds__((kNW + 1) * 32, 1)
 k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_t tbl_bytes, const uint32_t stage_bytes,
@@ -387,41 +435,33 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
 #pragma unroll
         for (int c = 0; c < ROWB / 16; ++c) rsrc[k][c] = Sh::swz((r < rc ? r : 0u) * ROWB + c * 16);
     }
-    uint32_t slot = 0, phase = 0;
-    for (uint32_t i = 0; i < nstages; ++i) {
-        mbar_wait(full0 + 8 * slot, phase);
-        const uint32_t src = ring0 + slot * Sh::kStageBytes;
-        uint4 v[K][ROWB / 16];
+    Ring ring{full0, empty0, ring0, nring, 0, 0};
+    uint32_t fact_ids[K];  // canonical ids of factored chunks (valid when `factored`)
+    bool factored = false;
+    if constexpr (Step::kFactor) {
+        // Stage 0 with the SFA table; then, if every lane's state is
+        // factorable (<= 1 non-absorbing image), the rest with the DFA step.
+        scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages < 1 ? nstages : 1u, lane);
+        if (t.fact_fam && nstages > 1) {
+            uint32_t fam[K], g[K];
+            bool ok = true;
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+            for (int k = 0; k < K; ++k) ok &= fact_from_id(t, S.id(st[k], lane), fam[k], g[k]);
+            if (__all_sync(kFull, ok)) {
+                StepDfa D;
+                D.params(t);
+                scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, 1, nstages, lane);
 #pragma unroll
-            for (int c = 0; c < ROWB / 16; ++c) v[k][c] = lds_v4(src + rsrc[k][c]);
-#pragma unroll
-        for (int c = 0; c < ROWB / 16; ++c) {
-            const uint32_t* w[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) w[k] = reinterpret_cast<const uint32_t*>(&v[k][c]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<0>(w[k][q]));
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<1>(w[k][q]));
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<2>(w[k][q]));
-#pragma unroll
-                for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
+                for (int k = 0; k < K; ++k) fact_ids[k] = fact_to_id(t, fam[k], g[k]);
+                factored = true;
+            } else {
+                scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 1, nstages, lane);
             }
+        } else if (nstages > 1) {
+            scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 1, nstages, lane);
         }
-        // Release the slot only now: every lane has consumed its loaded bytes,
-        // so no LDS of this stage can still be in flight when the producer's
-        // next TMA write lands (an arrive right after issuing the LDS raced).
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * slot);
-        if (++slot == nring) {
-            slot = 0;
-            phase ^= 1;
-        }
+    } else {
+        scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages, lane);
     }
 
     if (stamp) stamp[2] = globaltimer();
@@ -431,7 +471,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     for (int k = 0; k < K; ++k) {
         const uint32_t r = k * kNW * 32 + row0;
         const uint32_t row = blockIdx.x * rc + r;
-        const uint32_t s = (r < rc && row < a.plan.nchunks) ? S.id(st[k], lane) : 0u;  // rows past the text: f_I
+        const uint32_t sid = factored ? fact_ids[k] : S.id(st[k], lane);
+        const uint32_t s = (r < rc && row < a.plan.nchunks) ? sid : 0u;  // rows past the text: f_I
         CP::store(red + (k * kNW + warp) * CP::kSlot, CP::fold_states(S, t, s));
     }
     bar_compute(kNW * 32);
@@ -556,7 +597,22 @@ k_batch_scan(const BatchArgs a) {
         const uint64_t s0 = min(t1, t0 + j * a.seg), s1 = min(t1, s0 + a.seg);
         const uint64_t per = (((s1 - s0) + 31) / 32 + 15) & ~uint64_t(15);
         const uint64_t p0 = min(s1, s0 + lane * per), p1 = min(s1, p0 + per);
-        const uint32_t s = S.id(run_range(S, S.init(lane), a.texts, p0, p1), lane);
+        uint32_t s;
+        if constexpr (Step::kFactor) {  // 32 bytes through the SFA table, then the factored step if all lanes allow
+            const uint64_t pm = min(p1, p0 + 32);
+            const uint32_t s0 = run_range(S, S.init(lane), a.texts, p0, pm);
+            uint32_t fam = 0, g = 0;
+            const bool ok = t.fact_fam && fact_from_id(t, S.id(s0, lane), fam, g);
+            if (__all_sync(kFull, ok)) {
+                StepDfa D;
+                D.params(t);
+                s = fact_to_id(t, fam, run_range(D, g, a.texts, pm, p1));
+            } else {
+                s = S.id(run_range(S, s0, a.texts, pm, p1), lane);
+            }
+        } else {
+            s = S.id(run_range(S, S.init(lane), a.texts, p0, p1), lane);
+        }
         const uint32_t val = CP::fold_states(S, t, s);
         if (ntasks == 1) {
             const uint32_t q = CP::q_final(t, val, 0);

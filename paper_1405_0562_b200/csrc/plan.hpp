@@ -33,6 +33,15 @@ struct DevTables {
     const uint16_t* perm = nullptr;    // canonical -> device
     const uint16_t* iperm = nullptr;   // device -> canonical
     uint32_t hotH = 0;
+    // FACTORED step (HOT residency): SFA states whose mapping has at most one
+    // non-absorbing image g are (family, g); fact_fam / fact_g by canonical id (0xFFFF: not
+    // factorable), fact_tab[fam * nD + g] = canonical id, dwin = the DFA window table
+    // (u16 entries premultiplied by 2W), copied into smem after the hot rows.
+    const uint16_t* fact_fam = nullptr;
+    const uint16_t* fact_g = nullptr;
+    const uint16_t* fact_tab = nullptr;
+    const uint16_t* dwin = nullptr;
+    uint32_t dwin_bytes = 0;
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;

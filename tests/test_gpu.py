@@ -225,17 +225,19 @@ def test_batch_count_zero_is_noop(torch_cuda):
 
 
 # --------------------------------------------------------------------------- residency modes
+@pytest.mark.parametrize("factor", ["1", "0"])
 @pytest.mark.parametrize("hot_rows", [None, "7"])
 @pytest.mark.parametrize("rx,alpha,modes", [(*CFG1, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
                                             (*CFG2, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
                                             (*CFG4, (P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
                                             (W.cfg3_regex(), None, (P.RES_HOT_L2, P.RES_L2))])
-def test_every_residency_mode(torch_cuda, rx, alpha, modes, hot_rows, monkeypatch):
+def test_every_residency_mode(torch_cuda, rx, alpha, modes, hot_rows, factor, monkeypatch):
     """A6: every table placement gives the oracle's result; hot_rows='7'
     keeps only 7 renumbered rows in smem so nearly every HOT lookup takes the
     global (L2) path."""
     if hot_rows:
         monkeypatch.setenv("SFA_HOT_ROWS", hot_rows)
+    monkeypatch.setenv("SFA_FACTOR", factor)   # read when the handle is created below
     torch = torch_cuda
     d = oracle_pair(rx, alpha)
     sfa = P.SFA(rx, alpha)
@@ -391,3 +393,40 @@ def test_tune_residency_keeps_results(torch_cuda):
     junk = torch.from_numpy(rng.integers(0, 256, size=1 << 20, dtype=np.uint8)).cuda()
     sfa.tune_residency(junk)          # a misleading sample: slower, never wrong
     check_text(torch, sfa, d, text, 0)
+
+
+def test_factored_step_contains_match_boundaries(torch_cuda):
+    """FACTORED step (HOT residency): a word completed anywhere -- inside a
+    chunk's first 32 bytes (SFA-table phase), just after it, across chunk
+    boundaries, at the very end -- freezes the mapping into the accepting sink
+    (the (family, absorbing g) entries of fact_tab)."""
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    d = oracle_pair(rx, None)
+    sfa = P.SFA(rx, None)
+    base = W.cfg3_text(6 << 20, plant=False)
+    assert d.run(base)[1] is False
+    word = np.frombuffer(W.cfg3_words()[5], np.uint8)
+    rng = np.random.default_rng(21)
+    for off in [0, 3, 29, 31, 32, 33, 255, 4096, 7424 - 2, base.size - word.size] + rng.integers(0, base.size - 8, 12).tolist():
+        t = base.copy()
+        t[off:off + word.size] = word
+        exp = d.run(t)
+        assert exp[1] is True
+        check_text(torch, sfa, d, t, 0)
+    texts, offs = [], [0]
+    for i in range(64):
+        t = base[i * 65536:(i + 1) * 65536].copy()
+        if i % 3 == 0:
+            o = int(rng.integers(0, 65536 - 8))
+            t[o:o + word.size] = word
+        texts.append(t)
+        offs.append(offs[-1] + t.size)
+    cat = np.concatenate(texts)
+    off = np.array(offs, np.uint64)
+    res = torch.zeros(128, dtype=torch.int32, device="cuda")
+    sfa.match_batch(torch.from_numpy(cat).cuda(), torch.from_numpy(off.astype(np.int64)).cuda(), 64, res)
+    torch.cuda.synchronize()
+    got = res.cpu().numpy().view(np.uint32).reshape(64, 2)
+    qo, ao = d.run_batch(cat, off)
+    assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all()
