@@ -42,6 +42,7 @@ constexpr uint64_t kSlice = 64ull << 20;       // sfa_match_host slice
 constexpr uint64_t kBatchSeg = 64ull << 10;    // bytes per batch task
 constexpr uint32_t kCompMaxStates = 4096;      // composition table up to |S|^2 = 16M entries
 constexpr size_t kAuxMax = 16u << 10;          // comp / maps32 copied into smem up to this size
+constexpr uint64_t kDfaMax = 132u << 10;       // FACTORED: the DFA table copies take at most this much smem
 
 template <class T>
 cudaError_t upload(T** dst, const T* src, size_t count) {
@@ -80,7 +81,7 @@ struct sfa_handle {
     uint16_t* dperm = nullptr;                // HOT: canonical -> device id
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
     uint16_t *dfam = nullptr, *dfg = nullptr, *dftab = nullptr, *ddwin = nullptr;  // FACTORED step tables
-    uint32_t dwin_bytes = 0, nfam = 0;
+    uint32_t dwin_bytes = 0, nfam = 0, dwin_R = 0, dwin_X = 0;
     bool factor_on = [] {  // SFA_FACTOR=0 disables the factored step (A/B measurements, tests)
         const char* e = getenv("SFA_FACTOR");
         return !(e && e[0] == '0');
@@ -176,6 +177,8 @@ struct sfa_handle {
             t.fact_tab = dftab;
             t.dwin = ddwin;
             t.dwin_bytes = dwin_bytes;
+            t.dwin_R = dwin_R;
+            t.dwin_X = dwin_X;
         }
         t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin) : 0;
         return t;
@@ -311,19 +314,36 @@ struct sfa_handle {
                     tab[static_cast<size_t>(kv.second) * nD + a] = tab[static_cast<size_t>(f2->second) * nD + abs0];
             }
         }
-        // DFA window table, entries premultiplied by 2W (StepDfa)
+        // compact DFA window table (next state ids); in smem as R lane-group copies,
+        // R the largest of 32, 16, ..., 1 whose copies take <= 80 KB (StepDfa)
         const uint32_t ob = lo + W - 1 < 256 ? lo + W - 1 : lo - 1;  // a byte outside the window (class `other`)
         std::vector<uint16_t> dw((static_cast<size_t>(nD) * W + 7) & ~size_t(7), 0);
         for (uint32_t q = 0; q < nD; ++q)
             for (uint32_t j = 0; j < W; ++j) {
                 const uint32_t b = j + 1 < W ? lo + j : ob;
-                dw[static_cast<size_t>(q) * W + j] = static_cast<uint16_t>(A.dfa[static_cast<size_t>(q) * 256 + b] * 2 * W);
+                dw[static_cast<size_t>(q) * W + j] = static_cast<uint16_t>(A.dfa[static_cast<size_t>(q) * 256 + b]);
             }
+        uint32_t R = 32, X = 0;
+        const char* re = getenv("SFA_DFA_COPIES");  // diagnostic: force R
+        const uint32_t Rmax = re ? static_cast<uint32_t>(atoi(re)) : 32u;
+        for (; R >= 1; R /= 2) {
+            X = sfa::dfa_X(nD, R);
+            if (R <= Rmax && static_cast<uint64_t>(X) * W <= (kDfaMax) && X <= 65535u) break;
+        }
+        if (R == 0) return SFA_OK;
+        dwin_R = R;
+        dwin_X = X;
         CU(upload(&dfam, fam.data(), fam.size()));
         CU(upload(&dfg, g.data(), g.size()));
         CU(upload(&dftab, tab.data(), tab.size()));
-        CU(upload(&ddwin, dw.data(), dw.size()));
-        dwin_bytes = static_cast<uint32_t>(dw.size() * 2);
+        dwin_bytes = (X * W + 15) & ~15u;
+        std::vector<uint16_t> img(dwin_bytes / 2, 0);
+        for (uint32_t j = 0; j < W; ++j)
+            for (uint32_t q = 0; q < nD; ++q)
+                for (uint32_t c = 0; c < R; ++c)
+                    img[(j * X + sfa::dfa_enc(q, c, R)) / 2] =
+                        static_cast<uint16_t>(sfa::dfa_enc(dw[static_cast<size_t>(q) * W + j], c, R));
+        CU(upload(&ddwin, img.data(), img.size()));
         nfam = static_cast<uint32_t>(fams.size());
         dev_bytes += fam.size() * 4 + tab.size() * 2 + dw.size() * 2;
         return SFA_OK;
@@ -596,6 +616,12 @@ struct sfa_handle {
                     }
                     fprintf(stderr, "stamps: scan-start spread %.2fus, scan-end spread %.2fus\n", (m1 - m0) / 1e3,
                             (e1 - e0) / 1e3);
+                    std::vector<std::pair<double, uint32_t>> dur;
+                    for (uint32_t b = 0; b < a.plan.ctas; ++b) dur.push_back({(st[8 * b + 2] - st[8 * b + 1]) / 1e3, b});
+                    std::sort(dur.begin(), dur.end());
+                    fprintf(stderr, "stamps: scan us min %.1f (cta %u) median %.1f max %.1f (cta %u) 2nd %.1f (cta %u)\n",
+                            dur.front().first, dur.front().second, dur[dur.size() / 2].first, dur.back().first,
+                            dur.back().second, dur[dur.size() - 2].first, dur[dur.size() - 2].second);
                 }
                 uint64_t smax = 0;
                 for (uint32_t b = 0; b < a.plan.ctas; ++b) smax = std::max(smax, st[8 * b] - t0);

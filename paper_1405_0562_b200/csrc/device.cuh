@@ -302,14 +302,15 @@ struct StepHot {
     const uint16_t* iperm;
 
     static constexpr bool kFactor = true;  // kernels may switch warps to the factored step (StepDfa)
+    // smem: [DFA table copies (t.dwin_bytes, StepDfa) | hot rows]
     static __host__ __device__ size_t hot_bytes(const DevTables& t) { return (static_cast<size_t>(t.hotH) * t.W * 2 + 15) & ~size_t(15); }
     static __host__ __device__ size_t smem_bytes(const DevTables& t) { return hot_bytes(t) + t.dwin_bytes; }
     static __host__ __device__ bool supported(const DevTables& t) { return t.Tdev != nullptr && t.hotH > 0; }
     __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t) {  // hot rows = Tdev's prefix
-        copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.Tdev), hot_bytes(t) / 16, tid, nthreads);
-        if (t.dwin_bytes)
-            copy16(reinterpret_cast<uint4*>(dsmem + hot_bytes(t)), reinterpret_cast<const uint4*>(t.dwin), t.dwin_bytes / 16,
-                   tid, nthreads);
+        copy16(reinterpret_cast<uint4*>(dsmem + t.dwin_bytes), reinterpret_cast<const uint4*>(t.Tdev), hot_bytes(t) / 16,
+               tid, nthreads);
+        if (t.dwin_bytes)  // the DFA window table's smem image (dwin_R lane-group copies, built on the host)
+            copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.dwin), t.dwin_bytes / 16, tid, nthreads);
     }
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
@@ -320,7 +321,7 @@ struct StepHot {
         perm = t.perm;
         iperm = t.iperm;
         init_dev = __ldg(t.perm);  // f_I (canonical id 0)
-        sbase = smem_u32(dsmem);
+        sbase = smem_u32(dsmem) + t.dwin_bytes;
     }
     __device__ __forceinline__ uint32_t init(uint32_t) const { return init_dev; }
     // One predicated LDS (hot row) and one predicated LDG (cold row): no
@@ -346,25 +347,27 @@ struct StepHot {
 // factorable (k_scan_tma, k_batch_scan); converted back to the canonical SFA
 // id through DevTables::fact_tab at the end of the chunk.
 struct StepDfa {
-    uint32_t neg_lo, wmax, off;
+    // state = dfa_enc(g, lane % R): the column-0 offset of DFA state g in the
+    // lane's copy; one step = PRMT + VIADDMNMX + IMAD + LDS, as StepPrivate.
+    uint32_t neg_lo, wmax, X;
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
-        off = static_cast<uint32_t>(StepHot::hot_bytes(t));
+        X = t.dwin_X;
     }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
-        return ld_tbl_u16(off + st + 2 * window_col(byte, neg_lo, wmax));
+        return ld_tbl_u16(window_col(byte, neg_lo, wmax) * X + st);
     }
 };
 
-// SFA id -> factored state (2W * g) and family; false if s is not factorable
-__device__ __forceinline__ bool fact_from_id(const DevTables& t, uint32_t s, uint32_t& fam, uint32_t& g2w) {
+// SFA id -> factored state and family; false if s is not factorable
+__device__ __forceinline__ bool fact_from_id(const DevTables& t, uint32_t s, uint32_t& fam, uint32_t& st) {
     fam = __ldg(t.fact_fam + s);
-    g2w = static_cast<uint32_t>(__ldg(t.fact_g + s)) * 2u * t.W;
+    st = dfa_enc(__ldg(t.fact_g + s), lane_id() % t.dwin_R, t.dwin_R);
     return fam != 0xffffu;
 }
-__device__ __forceinline__ uint32_t fact_to_id(const DevTables& t, uint32_t fam, uint32_t g2w) {
-    return __ldg(t.fact_tab + fam * t.nD + g2w / (2u * t.W));
+__device__ __forceinline__ uint32_t fact_to_id(const DevTables& t, uint32_t fam, uint32_t st) {
+    return __ldg(t.fact_tab + fam * t.nD + dfa_dec(st, lane_id() % t.dwin_R, t.dwin_R));
 }
 
 // 4 text bytes of one word, in text order (little-endian)

@@ -439,10 +439,16 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     uint32_t fact_ids[K];  // canonical ids of factored chunks (valid when `factored`)
     bool factored = false;
     if constexpr (Step::kFactor) {
-        // Stage 0 with the SFA table; then, if every lane's state is
-        // factorable (<= 1 non-absorbing image), the rest with the DFA step.
-        scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages < 1 ? nstages : 1u, lane);
-        if (t.fact_fam && nstages > 1) {
+        // Stages through the SFA table until every lane's state is factorable
+        // (<= 1 non-absorbing image; the image count never grows along a
+        // walk), checked after stages 1, 2, 4, 8, ...; the rest with the
+        // factored DFA step.
+        uint32_t i = 0, next_check = 1;
+        while (i < nstages) {
+            scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, i, i + 1, lane);
+            ++i;
+            if (!t.fact_fam || i != next_check || i == nstages) continue;
+            next_check *= 2;
             uint32_t fam[K], g[K];
             bool ok = true;
 #pragma unroll
@@ -450,15 +456,12 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
             if (__all_sync(kFull, ok)) {
                 StepDfa D;
                 D.params(t);
-                scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, 1, nstages, lane);
+                scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i, nstages, lane);
 #pragma unroll
                 for (int k = 0; k < K; ++k) fact_ids[k] = fact_to_id(t, fam[k], g[k]);
                 factored = true;
-            } else {
-                scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 1, nstages, lane);
+                break;
             }
-        } else if (nstages > 1) {
-            scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 1, nstages, lane);
         }
     } else {
         scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages, lane);

@@ -36,17 +36,37 @@ struct DevTables {
     // FACTORED step (HOT residency): SFA states whose mapping has at most one
     // non-absorbing image g are (family, g); fact_fam / fact_g by canonical id (0xFFFF: not
     // factorable), fact_tab[fam * nD + g] = canonical id, dwin = the DFA window table
-    // (u16 entries premultiplied by 2W), copied into smem after the hot rows.
+    // copied into smem (before the hot rows) as dwin_R copies, lane L using copy L % dwin_R.
     const uint16_t* fact_fam = nullptr;
     const uint16_t* fact_g = nullptr;
     const uint16_t* fact_tab = nullptr;
-    const uint16_t* dwin = nullptr;
-    uint32_t dwin_bytes = 0;
+    const uint16_t* dwin = nullptr;     // smem image of the DFA window table: dwin_R lane-group copies
+    uint32_t dwin_bytes = 0;            // (StepDfa, dfa_enc), copied to smem offset 0
+    uint32_t dwin_R = 0, dwin_X = 0;
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;
     uint32_t lo = 0, W = 0;             // byte window: columns lo..lo+W-2, column W-1 = every other byte
 };
+
+// R lane-group copies of a u16 table (R | 32; lane L uses copy L % R, which
+// owns the banks c, c+R, c+2R, ... -- 32/R banks).  Entry (g, column j) of
+// copy c lives at j*X + dfa_enc(g, c, R):
+//   dfa_enc(g, c, R) = (g / spl) * 128 + 4 * (c + R * ((g % spl) / 2)) + 2 * (g & 1),  spl = 64 / R,
+// and X = 128 * ceil(nD / spl) + 4R, so consecutive columns of one state
+// rotate through the copy's banks (lanes of one copy at the same state but on
+// different bytes do not conflict).  R = 32 is a bank-private layout.
+__host__ __device__ __forceinline__ uint32_t dfa_enc(uint32_t g, uint32_t c, uint32_t R) {
+    const uint32_t spl = 64u / R, k = g % spl;
+    return (g / spl) * 128u + 4u * (c + R * (k >> 1)) + 2u * (k & 1u);
+}
+__host__ __device__ __forceinline__ uint32_t dfa_dec(uint32_t e, uint32_t c, uint32_t R) {
+    const uint32_t spl = 64u / R, w = (e & 127u) >> 2;
+    return (e >> 7) * spl + 2u * ((w - c) / R) + ((e >> 1) & 1u);
+}
+__host__ __device__ __forceinline__ uint32_t dfa_X(uint32_t nD, uint32_t R) {
+    return 128u * ((nD + 64u / R - 1) / (64u / R)) + 4u * R;
+}
 
 // Residency modes that have a kernel (sfa_residency without AUTO).
 enum class Res : int { Private = SFA_RES_SMEM_PRIVATE, Shared = SFA_RES_SMEM_SHARED, Hot = SFA_RES_HOT_L2, Global = SFA_RES_L2 };
