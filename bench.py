@@ -314,18 +314,34 @@ def bench_batch(args, torch, P, sfa, rx, alpha, batch, stream, world, rank, loca
         do = torch.from_numpy(off.astype(np.int64)).cuda()
         res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
+    length = int(off[1] - off[0])
+    assert (np.diff(off) == length).all()
+    # the offsets API (sfa_match_batch) as a secondary number
     for _ in range(args.warmup):
         sfa.match_batch(dt, do, count, res, stream)
     torch.cuda.synchronize()
+    ok_off = res.clone()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(max(1, args.steps // 2)):
+        sfa.match_batch(dt, do, count, res, stream)
+    e1.record(stream)
+    e1.synchronize()
+    offsets_gbs = texts.size / (e0.elapsed_time(e1) / max(1, args.steps // 2) * 1e-3) / 1e9
+    # timed: equal texts through sfa_match_batch_uniform (the TMA scan, per-text fold)
+    for _ in range(args.warmup):
+        sfa.match_batch_uniform(dt, length, count, res, stream)
+    torch.cuda.synchronize()
+    if not torch.equal(ok_off, res):
+        raise SystemExit("uniform batch results differ from the offsets path")
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         time.sleep(0.3)
         e0.record(stream)
         for _ in range(args.steps):
-            sfa.match_batch(dt, do, count, res, stream)
+            sfa.match_batch_uniform(dt, length, count, res, stream)
         e1.record(stream)
         e1.synchronize()
     ms = e0.elapsed_time(e1)
@@ -345,11 +361,13 @@ def bench_batch(args, torch, P, sfa, rx, alpha, batch, stream, world, rank, loca
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded, DESIGN.md input recipe)",
         "config": {"workload": CONFIG_NAMES[5], "bytes_per_step": int(texts.size), "texts": count,
                    "accepted": accepts, "l2": "4 GiB input > 126 MB L2: no flush needed",
+                   "api": "sfa_match_batch_uniform (TMA scan, per-text fold)",
+                   "offsets_api_gbs": offsets_gbs,
                    "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
                    "parallelism": f"replicas x{world}"},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": ncu_traffic(5), "peak_kind": f"{peak_kind} copy bandwidth"},
-        "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(), "gpu_launches": args.steps,
     }
     print(json.dumps(line), flush=True)
 

@@ -159,6 +159,16 @@ SFA_API int sfa_match_batch(const sfa_handle* h, const uint8_t* d_texts, const u
                     size_t count, sfa_stream_t stream, sfa_result* d_results);
 
 /*
+ * sfa_match_batch_uniform -- `count` texts of `len` bytes each, back to back
+ * at d_texts (device; text i = d_texts[i*len : (i+1)*len)).  Same results as
+ * sfa_match_batch with offsets i*len; async, stream-ordered.  When d_texts is
+ * 16-byte aligned and len a multiple of 256, the texts go through the TMA
+ * scan as a [rows x len/m] tensor (m rows per text) with a per-text fold.
+ */
+SFA_API int sfa_match_batch_uniform(const sfa_handle* h, const uint8_t* d_texts, size_t len, size_t count,
+                            sfa_stream_t stream, sfa_result* d_results);
+
+/*
  * Sharded matching (one text split over several GPUs / streams; Theorem 3,
  * PAPER.md:469-479, and Lemma 1).
  *

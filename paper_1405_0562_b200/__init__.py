@@ -56,7 +56,7 @@ class sfa_info_t(C.Structure):
 
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
-           "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps",
+           "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform",
            "sfa_export_dfa", "sfa_export_sfa")
 
 _lib = None
@@ -84,6 +84,7 @@ def lib() -> C.CDLL:
         L.sfa_set_compose.argtypes = [vp, C.c_int]
         L.sfa_tune_residency.argtypes = [vp, vp, C.c_size_t, vp]
         L.sfa_match_map.argtypes = [vp, vp, C.c_size_t, vp, vp]
+        L.sfa_match_batch_uniform.argtypes = [vp, vp, C.c_size_t, C.c_size_t, vp, vp]
         L.sfa_combine_maps.argtypes = [vp, vp, C.c_size_t, vp, vp]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
@@ -181,6 +182,13 @@ def sfa_combine_maps(h: int, d_maps, count: int, d_result, stream=None):
     _check(lib().sfa_combine_maps(h, _dptr(d_maps) if count else None, count, _stream(stream), _dptr(d_result)))
 
 
+def sfa_match_batch_uniform(h: int, d_texts, length: int, count: int, d_results, stream=None):
+    """Stream-ordered: count back-to-back texts of `length` bytes -> d_results (device, count x 2 uint32)."""
+    if count == 0:
+        return
+    _check(lib().sfa_match_batch_uniform(h, _dptr(d_texts), length, count, _stream(stream), _dptr(d_results)))
+
+
 def sfa_match_host(h: int, h_text, stream=None):
     """End to end from host memory (numpy array or pinned CPU tensor): -> (final_state, accept)."""
     if isinstance(h_text, np.ndarray):
@@ -272,6 +280,9 @@ class SFA:
 
     def match_batch(self, d_texts, d_offsets, count, d_results, stream=None):
         return sfa_match_batch(self.h, d_texts, d_offsets, count, d_results, stream)
+
+    def match_batch_uniform(self, d_texts, length, count, d_results, stream=None):
+        return sfa_match_batch_uniform(self.h, d_texts, length, count, d_results, stream)
 
     def match_map(self, d_text, d_map, stream=None):
         return sfa_match_map(self.h, d_text, d_map, None, stream)

@@ -554,6 +554,8 @@ struct sfa_handle {
             a.result = d_result;
             a.stamps = nullptr;
             a.map_out = map_out;
+            a.seg_m = 0;
+            a.results = nullptr;
             static const uint32_t diag = getenv("SFA_DIAG_FLAGS") ? static_cast<uint32_t>(atoi(getenv("SFA_DIAG_FLAGS"))) : 0u;
             a.diag = diag;
             sfa::TmaConfig cfg;
@@ -968,6 +970,80 @@ int sfa_match_batch(const sfa_handle* hc, const uint8_t* d_texts, const uint64_t
     cudaError_t e = sfa::launch_batch(mode, h->vec(), a, h->sm_count, s);
     if (e != cudaSuccess) return cuda_fail(e, "batch launch");
     return h->end(s);
+}
+
+// A batch of `count` back-to-back texts of `len` bytes each through the TMA scan:
+// the texts are a 2-D tensor [count * m rows x len/m bytes], m rows per text
+// (m | 32, so one text's rows are consecutive lanes of one warp) and the
+// kernel folds each text's m row states with a segmented shuffle tree.
+int sfa_match_batch_uniform(const sfa_handle* hc, const uint8_t* d_texts, size_t len, size_t count, sfa_stream_t stream,
+                            sfa_result* d_results) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || (count && !d_results)) return fail(SFA_ERR_INVALID_ARG, "NULL handle or results");
+    if (count == 0) return SFA_OK;
+    if (!d_texts && len > 0) return fail(SFA_ERR_INVALID_ARG, "d_texts is NULL");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    {
+        std::lock_guard<std::mutex> lk(h->mu);
+        int rc = h->begin(s);
+        if (rc) return rc;
+        sfa::Res mode;
+        rc = h->resolve(0, &mode);
+        if (rc) return rc;
+        sfa::TmaConfig cfg;
+        const sfa::DevTables t0 = h->tables(mode, 0);
+        const bool aligned = (reinterpret_cast<uintptr_t>(d_texts) & 15) == 0;
+        if (!h->vec() && aligned && len >= 512 && sfa::tma_choose(mode, t0, h->smem_optin, &cfg)) {
+            if (mode == sfa::Res::Hot && !h->hot_tuned && h->auto_tune()) {
+                rc = h->tune_hot(d_texts, len * count, s);
+                if (rc) return rc;
+            }
+            const uint64_t G = static_cast<uint64_t>(h->sm_count), R = cfg.rows_per_cta;
+            // largest m <= 32 (power of 2) with len/m a multiple of the stage width and of 256
+            uint32_t m = 32;
+            while (m > 1 && (len % (static_cast<uint64_t>(m) * 256) != 0 || count * m > G * R)) m /= 2;
+            const uint64_t L = len / m;
+            if (len % 256 == 0 && L % static_cast<uint64_t>(cfg.rowb) == 0) {
+                const uint64_t per_launch = std::max<uint64_t>(1, (G * R) / m);  // texts per launch
+                for (uint64_t c0 = 0; c0 < count; c0 += per_launch) {
+                    const uint64_t cnt = std::min<uint64_t>(per_launch, count - c0);
+                    sfa::ScanArgs a{};
+                    a.t = h->tables(mode, 0);
+                    a.text = d_texts + c0 * len;
+                    a.n = cnt * len;
+                    a.sc = h->scratch();
+                    a.q_in = nullptr;
+                    a.result = nullptr;
+                    a.stamps = nullptr;
+                    a.map_out = nullptr;
+                    a.diag = 0;
+                    a.seg_m = m;
+                    a.results = d_results + c0;
+                    const uint64_t rows = cnt * m, NB = cfg.nb * 8;
+                    const uint64_t rc_ = NB * ((rows + G * NB - 1) / (G * NB));
+                    a.plan.head = 0;
+                    a.plan.L = L;
+                    a.plan.nchunks = static_cast<uint32_t>(rows);
+                    a.plan.rows_per_cta = static_cast<uint32_t>(rc_);
+                    a.plan.ctas = static_cast<uint32_t>((rows + rc_ - 1) / rc_);
+                    a.plan.tail_start = a.n;
+                    cudaError_t e = sfa::launch_scan_tma(mode, false, a, cfg, s);
+                    if (e != cudaSuccess) return cuda_fail(e, "uniform batch launch");
+                }
+                return h->end(s);
+            }
+        }
+    }
+    // general path: explicit offsets
+    std::vector<uint64_t> off(count + 1);
+    for (size_t i = 0; i <= count; ++i) off[i] = i * len;
+    uint64_t* d_off = nullptr;
+    CU(cudaMallocAsync(&d_off, off.size() * 8, s));
+    CU(cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s));
+    int rc = sfa_match_batch(hc, d_texts, d_off, count, stream, d_results);
+    CU(cudaFreeAsync(d_off, s));
+    CU(cudaStreamSynchronize(s));  // `off` is host memory of this frame
+    return rc;
 }
 
 int sfa_match_host(const sfa_handle* hc, const uint8_t* h_text, size_t n, sfa_stream_t stream, uint32_t* final_state,

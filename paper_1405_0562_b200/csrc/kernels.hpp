@@ -26,6 +26,8 @@ struct ScanArgs {
     uint64_t* stamps;     // diagnostic (SFA_DEBUG_STAMPS): 8 %globaltimer stamps per CTA, else NULL
     uint32_t diag;        // diagnostic (SFA_DIAG_FLAGS, results invalid): 1 = skip the table build
     uint32_t* map_out;    // optional: f_fin(q) for every DFA state q (nD u32, device)
+    uint32_t seg_m;       // 0: one text.  > 0: a batch of equal texts, each seg_m consecutive rows
+    sfa_result* results;  // seg_m > 0: per-text results
 };
 
 struct DirectArgs {

@@ -469,6 +469,27 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
 
     if (stamp) stamp[2] = globaltimer();
     if (t.aux_bytes) mbar_wait(abar, 0);
+    if constexpr (!VEC) {
+        if (a.seg_m) {  // batch of equal texts: text = seg_m consecutive rows (lanes); per-text fold, no grid fold
+            const uint32_t m = a.seg_m;
+            pdl_wait();   // results may be reused by the previous launch on the stream
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t r = k * kNW * 32 + row0;
+                const uint32_t row = blockIdx.x * rc + r;
+                uint32_t sv = factored ? fact_ids[k] : S.id(st[k], lane);
+                for (uint32_t d = 1; d < m; d <<= 1) {  // segmented shuffle tree (m | 32, texts never straddle warps)
+                    const uint32_t o = __shfl_down_sync(kFull, sv, d);
+                    if ((lane & (2 * d - 1)) == 0) sv = Comp<Step, false>::combine(S, t, sv, o);
+                }
+                if (lane % m == 0 && r < rc && row < a.plan.nchunks) {
+                    const uint32_t q = t.img0[sv];
+                    a.results[row / m] = sfa_result{q, t.dfinal[q]};
+                }
+            }
+            return;
+        }
+    }
     // ---- composition: warp -> block (rows are ordered k-major, then warp, then lane) ----
 #pragma unroll
     for (int k = 0; k < K; ++k) {

@@ -430,3 +430,43 @@ def test_factored_step_contains_match_boundaries(torch_cuda):
     got = res.cpu().numpy().view(np.uint32).reshape(64, 2)
     qo, ao = d.run_batch(cat, off)
     assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all()
+
+
+@pytest.mark.parametrize("rx,alpha,compose", [(W.cfg3_regex(), None, None), (*CFG2, None), (*CFG4, None),
+                                               (*CFG1, None), (*CFG1, P.COMPOSE_VEC), (*CFG2, P.COMPOSE_REPLAY)])
+def test_batch_uniform(torch_cuda, rx, alpha, compose):
+    """sfa_match_batch_uniform: equal texts through the TMA scan with a per-text
+    segmented fold (or the offsets path for VEC / unaligned / odd lengths)."""
+    torch = torch_cuda
+    d = oracle_pair(rx, alpha)
+    sfa = P.SFA(rx, alpha)
+    if compose:
+        sfa.set_compose(compose)
+    al = np.frombuffer(alpha if alpha else b"abcdefghijklmnopqrstuvwxyz", np.uint8)
+    rng = np.random.default_rng(31)
+    for length, count, pad in [(65536, 300, 0), (4096, 5000, 0), (768, 20000, 0), (65536, 3, 0), (1000, 77, 0),
+                               (4096, 64, 8)]:
+        if rx == CFG2[0]:
+            body = W.cfg2_accepted(length * count // 10 + 1)[:length * count]
+            body = body.copy()
+            flips = rng.integers(0, body.size, size=count // 3)
+            body[flips] = np.uint8(ord("7"))
+        elif rx == CFG1[0]:
+            body = np.tile(W.cfg1_accepted(length // 2)[:length], count)[:length * count].copy()
+        else:
+            body = al[rng.integers(0, al.size, size=length * count)]
+        if rx == W.cfg3_regex():
+            word = np.frombuffer(W.cfg3_words()[7], np.uint8)
+            for i in rng.choice(count, size=max(1, count // 10), replace=False):
+                o = int(i) * length + int(rng.integers(0, length - word.size))
+                body[o:o + word.size] = word
+        buf = torch.empty(body.size + pad + 16, dtype=torch.uint8, device="cuda")
+        v = buf[pad:pad + body.size]
+        v.copy_(torch.from_numpy(body))
+        res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
+        sfa.match_batch_uniform(v, length, count, res)
+        torch.cuda.synchronize()
+        got = res.cpu().numpy().view(np.uint32).reshape(count, 2)
+        off = np.arange(count + 1, dtype=np.uint64) * length
+        qo, ao = d.run_batch(body, off)
+        assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all(), (length, count, pad)
