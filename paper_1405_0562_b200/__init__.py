@@ -24,7 +24,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsfa.so")
+LIB_PATH = os.environ.get("SFA_LIB") or os.path.join(_HERE, "_lib", "libsfa.so")  # SFA_LIB: A/B builds
 
 SFA_OK, SFA_ERR_SYNTAX, SFA_ERR_UNSUPPORTED, SFA_ERR_CAPACITY, SFA_ERR_INVALID_ARG, SFA_ERR_CUDA, SFA_ERR_OOM = range(7)
 RES_AUTO, RES_SMEM_PRIVATE, RES_SMEM_SHARED, RES_HOT_L2, RES_L2 = range(5)

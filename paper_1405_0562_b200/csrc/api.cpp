@@ -77,6 +77,7 @@ struct sfa_handle {
     uint8_t* drep = nullptr;
     void* dcomp = nullptr;                    // composition table (u8 if nS <= 256, else u16)
     uint32_t* dpairs = nullptr;               // PRIVATE: pair words (device.cuh StepPrivate)
+    uint32_t priv_R = 0;                      // PRIVATE: lane-group copies (0: no PRIVATE layout)
     uint16_t* dTdev = nullptr;                // HOT: window table renumbered by visit frequency
     uint16_t* dperm = nullptr;                // HOT: canonical -> device id
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
@@ -168,6 +169,7 @@ struct sfa_handle {
         t.lo = lo;
         t.W = W;
         t.pairs = dpairs;
+        t.priv_R = priv_R;
         t.Tdev = dTdev;
         t.perm = dperm;
         t.iperm = diperm;
@@ -392,11 +394,28 @@ struct sfa_handle {
             R16[static_cast<size_t>(s) * W + W - 1] = T16[static_cast<size_t>(s) * C + other];
         }
         CU(upload(&dT, T16.data(), T16.size()));
-        if (nS <= 1024) {  // PRIVATE pair words (padded to 16 bytes: bulk-copied)
-            std::vector<uint32_t> pw(static_cast<size_t>(W) * ((nS + 1) / 2));
-            sfa::build_private_pairs(R16.data(), nS, W, pw.data());
-            pw.resize((pw.size() + 3) & ~size_t(3), 0);
-            CU(upload(&dpairs, pw.data(), pw.size()));
+        {  // PRIVATE: R lane-group copies, R the largest of 32, 16, 8 whose table
+           // leaves room for a 3-deep ring of 32-byte stages (else <= 200 KB)
+            const char* re = getenv("SFA_PRIVATE_COPIES");  // diagnostic: cap R
+            const uint32_t Rcap = re ? static_cast<uint32_t>(atoi(re)) : 32u;
+            uint32_t R = 0;
+            for (int pass = 0; pass < 2 && !R; ++pass)
+                for (uint32_t r = 32; r >= 8; r /= 2) {
+                    const uint64_t X = sfa::dfa_X(nS, r);
+                    if (r > Rcap || X > 65535u) continue;
+                    if (X * W <= (pass == 0 ? (112u << 10) : (200u << 10))) {
+                        R = r;
+                        break;
+                    }
+                }
+            if (R) {
+                const uint32_t spl = 64u / R, nl = (nS + spl - 1) / spl;
+                std::vector<uint32_t> pw(static_cast<size_t>(W) * nl * (32u / R));
+                sfa::build_private_pairs(R16.data(), nS, W, R, pw.data());
+                pw.resize((pw.size() + 3) & ~size_t(3), 0);
+                CU(upload(&dpairs, pw.data(), pw.size()));
+                priv_R = R;
+            }
         }
         {  // padded to 16 bytes: the TMA kernel bulk-copies it
             std::vector<uint16_t> padded(R16);

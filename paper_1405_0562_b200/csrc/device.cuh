@@ -169,62 +169,85 @@ __device__ __forceinline__ void copy16(uint4* dst, const uint4* src, size_t n16,
 struct StepPrivate {
     static constexpr bool kFactor = false;
     static constexpr bool kStaged = true;  // TMA kernel: bulk-copy the pair words, expand in smem
-    static __host__ __device__ uint32_t staged_bytes(const DevTables& t) { return ((t.nS + 1) / 2 * t.W * 4 + 15) & ~15u; }
-    static __host__ __device__ const void* staged_src(const DevTables& t) { return t.pairs; }
-    // Lane L's copy lives in bank L.  Cell (s, j) of lane L is the u16 at byte
-    //   j*X + (s>>1)*128 + 4L + 2(s&1)          (X = 128 * ceil(nS/2))
-    // and holds enc(delta_s(s, j), L) = (s'>>1)*128 + 4L + 2(s'&1), the
-    // column-0 offset of the next state in lane L's copy, so the next address
-    // is one IMAD: col*X + state.  Needs X <= 65536 (nS <= 1024).
-    uint32_t X, neg_lo, wmax;
+    // R lane-group copies of the window table (plan.hpp dfa_enc; R = t.priv_R,
+    // 32 = one bank-private copy per lane, 16 when 32 copies do not fit):
+    // cell (s, j) of lane L's copy is the u16 at j*X + dfa_enc(s, L % R, R)
+    // and holds dfa_enc(delta_s(s, j), L % R, R), the column-0 offset of the
+    // next state, so the next address is one IMAD: col*X + state.
+    uint32_t X, neg_lo, wmax, R;
 
-    static __host__ __device__ uint32_t col_bytes(const DevTables& t) { return 128u * ((t.nS + 1) / 2); }
+    static __host__ __device__ uint32_t lines(const DevTables& t) {
+        return t.priv_R ? (t.nS + 64u / t.priv_R - 1) / (64u / t.priv_R) : 0u;
+    }
+    static __host__ __device__ uint32_t col_bytes(const DevTables& t) { return t.priv_R ? dfa_X(t.nS, t.priv_R) : 0u; }
     static __host__ __device__ size_t smem_bytes(const DevTables& t) { return static_cast<size_t>(t.W) * col_bytes(t); }
-    static __host__ __device__ bool supported(const DevTables& t) { return t.nS <= 1024; }
-    static __host__ __device__ __forceinline__ uint32_t enc(uint32_t s, uint32_t L) { return (s >> 1) * 128u + 4u * L + 2u * (s & 1u); }
+    static __host__ __device__ bool supported(const DevTables& t) { return t.priv_R != 0 && t.pairs != nullptr; }
+    static __host__ __device__ uint32_t npairs(const DevTables& t) { return t.priv_R ? t.W * lines(t) * (32u / t.priv_R) : 0u; }
+    static __host__ __device__ uint32_t staged_bytes(const DevTables& t) { return (npairs(t) * 4 + 15) & ~15u; }
+    static __host__ __device__ const void* staged_src(const DevTables& t) { return t.pairs; }
 
-    // The 32 bank-private copies from the lane-independent pair words
-    // t.pairs[j * npairs + p] = (a(s0') | a(s1') << 16), a(s') = (s'>>1)*128 +
-    // 2(s'&1), s0'/s1' = delta_s(2p / 2p+1, column j) (built on the host):
-    // word (j, p, L) at j*X + 128p + 4L = pairs[j*npairs + p] + 4L*0x10001.
-    // One warp per 128-byte line: a broadcast load, an add, a store.
+    // The copies from the lane-independent pair words (built on the host):
+    // pairs[(j * lines + l) * (32/R) + k] = b(s0') | b(s1') << 16 with s0'/s1'
+    // the next states of states l*spl + 2k, +1 in column j and b(x) =
+    // dfa_enc(x, 0, R); word w of line l of column j (copy c = w % R, k = w / R)
+    // = pairs[...] + 4c * 0x10001.  The skew gap after each column is zero.
     // `src_s`: shared-window address of an smem copy of t.pairs (the TMA
-    // kernel stages it), else 0 (read t.pairs from global).  Generic stores
-    // (see k_scan_tma: they keep the smem base foldable into the hot loop).
+    // kernel stages it), else 0 (global).  Generic stores (see k_scan_tma:
+    // they keep the smem base foldable into the hot loop's LDS).
     __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t src_s) {
-        const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5;
-        const uint32_t npairs = (t.nS + 1) / 2, units = npairs * t.W, add = L * 0x40004u;
+        const uint32_t R = t.priv_R, lgR = __ffs(R) - 1, lgk = 5 - lgR, nl = lines(t);
+        const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5, units = t.W * nl, add = (L & (R - 1)) * 0x40004u;
         uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
-        // unit u = j * npairs + p lives at line j*X/128 + p = u (X = 128 * npairs)
+        // Staged pair words: the C++ load (not volatile asm) lets the loads of
+        // several iterations be in flight at once.
+        const uint32_t* sp = src_s ? reinterpret_cast<const uint32_t*>(dsmem + (src_s - smem_u32(dsmem))) : nullptr;
+        // one warp per line unit u = j * nl + l: word L of line l of column j
+        // sits at word 32u + jR + L (X/4 = 32 nl + R); the skew gap is never read
+        if (R == 32) {  // no skew: line unit u is line u
+#pragma unroll 4
+            for (uint32_t u = w; u < units; u += nw) tbl[32 * u + L] = (sp ? sp[u] : __ldg(t.pairs + u)) + add;
+            return;
+        }
+        uint32_t j = w / nl, l = w - j * nl;
+        const uint32_t dj = nw / nl, dl = nw - dj * nl;
 #pragma unroll 4
         for (uint32_t u = w; u < units; u += nw) {
-            const uint32_t a = src_s ? lds_u32(src_s + 4 * u) : __ldg(t.pairs + u);
-            tbl[u * 32 + L] = a + add;
+            const uint32_t pi = (u << lgk) + (L >> lgR);
+            const uint32_t a = sp ? sp[pi] : __ldg(t.pairs + pi);
+            tbl[32 * u + j * R + L] = a + add;
+            j += dj;
+            l += dl;
+            if (l >= nl) {
+                l -= nl;
+                ++j;
+            }
         }
     }
-    // host: the pair words of Trange [nS x W]
-    static __host__ void build_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t* pairs) {
-        const uint32_t npairs = (nS + 1) / 2;
+    // host: the pair words of Trange [nS x W] for R copies
+    static __host__ void build_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t R, uint32_t* pairs) {
+        const uint32_t spl = 64u / R, nl = (nS + spl - 1) / spl, kpl = 32u / R;
         for (uint32_t j = 0; j < W; ++j)
-            for (uint32_t p = 0; p < npairs; ++p) {
-                const uint32_t s0 = Trange[(2 * p) * W + j];
-                const uint32_t s1 = 2 * p + 1 < nS ? Trange[(2 * p + 1) * W + j] : 0u;
-                const uint32_t a0 = enc(s0, 0), a1 = 2 * p + 1 < nS ? enc(s1, 0) : 0u;
-                pairs[j * npairs + p] = a0 | (a1 << 16);
-            }
+            for (uint32_t l = 0; l < nl; ++l)
+                for (uint32_t k = 0; k < kpl; ++k) {
+                    const uint32_t g0 = l * spl + 2 * k, g1 = g0 + 1;
+                    const uint32_t b0 = g0 < nS ? dfa_enc(Trange[g0 * W + j], 0, R) : 0u;
+                    const uint32_t b1 = g1 < nS ? dfa_enc(Trange[g1 * W + j], 0, R) : 0u;
+                    pairs[(j * nl + l) * kpl + k] = b0 | (b1 << 16);
+                }
     }
     __device__ void params(const DevTables& t) {
         X = col_bytes(t);
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
+        R = t.priv_R;
     }
-    __device__ __forceinline__ uint32_t init(uint32_t lane) const { return 4u * lane; }
+    __device__ __forceinline__ uint32_t init(uint32_t lane) const { return dfa_enc(0, lane % R, R); }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
         const uint32_t col = window_col(byte, neg_lo, wmax);
         return ld_tbl_u16(col * X + st);
     }
-    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return ((st >> 7) << 1) | ((st >> 1) & 1u); }
-    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t lane) const { return enc(s, lane); }
+    __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t lane) const { return dfa_dec(st, lane % R, R); }
+    __device__ __forceinline__ uint32_t from_id(uint32_t s, uint32_t lane) const { return dfa_enc(s, lane % R, R); }
 };
 
 

@@ -26,8 +26,8 @@ size_t table_smem_bytes(Res mode, const DevTables& t) {
 // HOT residency: the number of renumbered rows that fit in smem next to what
 // the launch kind needs (kind 0: the TMA scan with K=1, 32-byte stages and a
 // 2-deep ring; 1: k_scan_direct; 2: the batch kernels), capped at nS.
-void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t* pairs) {
-    StepPrivate::build_pairs(Trange, nS, W, pairs);
+void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t R, uint32_t* pairs) {
+    StepPrivate::build_pairs(Trange, nS, W, R, pairs);
 }
 
 uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin) {

@@ -67,8 +67,8 @@ struct TmaConfig {
 };
 
 uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin);
-// Host: the PRIVATE layout's lane-independent pair words (W * ceil(nS/2) u32).
-void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t* pairs);
+// Host: the PRIVATE layout's lane-independent pair words for R copies (StepPrivate::npairs u32).
+void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t R, uint32_t* pairs);
 size_t direct_smem_bytes(Res mode, const DevTables& t);
 size_t table_smem_bytes(Res mode, const DevTables& t);   // SIZE_MAX/2 if the layout cannot hold t
 uint32_t direct_threads_per_cta();

@@ -14,7 +14,8 @@ struct DevTables {
     const uint16_t* T = nullptr;        // nS * C   next SFA id per (state, class)
     const uint8_t* cls = nullptr;       // 256      byte -> class
     const uint16_t* Trange = nullptr;   // nS * W   next SFA id per (state, window column)
-    const uint32_t* pairs = nullptr;    // PRIVATE: W * ceil(nS/2) lane-independent pair words (device.cuh)
+    const uint32_t* pairs = nullptr;    // PRIVATE: lane-independent pair words (device.cuh StepPrivate)
+    uint32_t priv_R = 0;                // PRIVATE: lane-group copies (32 = bank-private), 0 = unavailable
     const uint8_t* maps32 = nullptr;    // nS * 32  f_s(q) for |D| <= 32 (identity-padded)
     const uint16_t* maps16 = nullptr;   // nS * nD  f_s(q) (any |D|; used to apply f_fin to q_in != q0)
     const uint32_t* img0 = nullptr;     // nS       f_s(q0)
@@ -53,9 +54,9 @@ struct DevTables {
 // owns the banks c, c+R, c+2R, ... -- 32/R banks).  Entry (g, column j) of
 // copy c lives at j*X + dfa_enc(g, c, R):
 //   dfa_enc(g, c, R) = (g / spl) * 128 + 4 * (c + R * ((g % spl) / 2)) + 2 * (g & 1),  spl = 64 / R,
-// and X = 128 * ceil(nD / spl) + 4R, so consecutive columns of one state
-// rotate through the copy's banks (lanes of one copy at the same state but on
-// different bytes do not conflict).  R = 32 is a bank-private layout.
+// and X = 128 * ceil(nD / spl) + 4R (R < 32), so consecutive columns of one
+// state rotate through the copy's banks (lanes of one copy at the same state
+// but on different bytes do not conflict).  R = 32 is a bank-private layout.
 __host__ __device__ __forceinline__ uint32_t dfa_enc(uint32_t g, uint32_t c, uint32_t R) {
     const uint32_t spl = 64u / R, k = g % spl;
     return (g / spl) * 128u + 4u * (c + R * (k >> 1)) + 2u * (k & 1u);
@@ -65,7 +66,7 @@ __host__ __device__ __forceinline__ uint32_t dfa_dec(uint32_t e, uint32_t c, uin
     return (e >> 7) * spl + 2u * ((w - c) / R) + ((e >> 1) & 1u);
 }
 __host__ __device__ __forceinline__ uint32_t dfa_X(uint32_t nD, uint32_t R) {
-    return 128u * ((nD + 64u / R - 1) / (64u / R)) + 4u * R;
+    return 128u * ((nD + 64u / R - 1) / (64u / R)) + (R < 32 ? 4u * R : 0u);  // R = 32: one lane per copy, no skew needed
 }
 
 // Residency modes that have a kernel (sfa_residency without AUTO).
