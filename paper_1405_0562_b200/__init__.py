@@ -257,6 +257,7 @@ class SFA:
 
     def __init__(self, regex, alphabet=None, max_sfa: int = 0):
         self.h = sfa_compile(regex, alphabet, max_sfa)
+        self._match_async = lib().sfa_match_async
 
     def close(self):
         if getattr(self, "h", None):
@@ -276,7 +277,14 @@ class SFA:
         return sfa_match(self.h, d_text, None, stream)
 
     def match_async(self, d_text, d_result, stream=None):
-        return sfa_match_async(self.h, d_text, d_result, None, stream)
+        # the hot call of serving loops: plain attribute reads, one C call
+        n = d_text.numel()
+        if n and not (d_text.is_cuda and d_text.dtype.itemsize == 1 and d_text.is_contiguous()):
+            raise ValueError("expected a contiguous uint8 CUDA tensor")
+        rc = self._match_async(self.h, d_text.data_ptr() if n else None, n,
+                               _stream(stream), d_result.data_ptr())
+        if rc:
+            _check(rc)
 
     def match_batch(self, d_texts, d_offsets, count, d_results, stream=None):
         return sfa_match_batch(self.h, d_texts, d_offsets, count, d_results, stream)

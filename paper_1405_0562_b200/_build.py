@@ -47,14 +47,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmds.append(cmd)
         objs.append(obj)
     # one nvcc per translation unit, in parallel (the kernels are split by step policy)
-    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
-        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
-            f.result()
-    tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"])
-    os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
+    try:
+        with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+            for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+                f.result()
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt",
+                               "-lpthread"])
+        os.replace(tmp, LIB)
+    finally:  # an interrupted or failed build leaves no objects behind
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return LIB
 
 

@@ -26,6 +26,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <utility>
 
 #include "device.cuh"
@@ -676,6 +678,23 @@ k_batch_combine(const BatchArgs a) {
 // ------------------------------------------------------------------------------------------
 namespace detail {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was last given on this device (host overhead per launch).
+template <class F>
+cudaError_t ensure_smem(F kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> granted;  // (kernel, device) -> bytes
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = granted.find(key);
+    if (it != granted.end() && it->second >= static_cast<int>(smem)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e == cudaSuccess) granted[key] = static_cast<int>(smem);
+    return e;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while the previous kernel of the stream finishes; it calls pdl_wait()
 // before it touches state the previous kernel may still use.
@@ -719,11 +738,10 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s
     const uint32_t tbytes = static_cast<uint32_t>(table_bytes<Step>(a.t) + a.t.aux_bytes);
     const uint32_t sbytes = cfg.staged ? Step::staged_bytes(a.t) : 0u;
     const size_t smem = tbytes + sbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
     EncodeFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
-    TmaMaps maps;
     cuuint64_t dims[2] = {a.plan.L, a.plan.nchunks};
     cuuint64_t strides[1] = {a.plan.L};
     // Diagnostic only (results are wrong): SFA_DIAG_STRIDE=s overlaps the rows
@@ -739,6 +757,25 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s
     cuuint32_t pbox[2] = {static_cast<cuuint32_t>(kLine), br};
     cuuint32_t estr[2] = {1, 1};
     void* base = const_cast<uint8_t*>(a.text + a.plan.head);
+    // The tensor maps depend only on (base, L, rows, box, promotion, prefetch):
+    // repeated matches of one buffer reuse the last encoding (host overhead).
+    struct Key {
+        void* base;
+        uint64_t L, rows, stride;
+        uint32_t br;
+        int promo, pf;
+        bool operator==(const Key& o) const {
+            return base == o.base && L == o.L && rows == o.rows && stride == o.stride && br == o.br && promo == o.promo &&
+                   pf == o.pf;
+        }
+    };
+    static thread_local Key last_key{nullptr, 0, 0, 0, 0, -1, -9};
+    static thread_local TmaMaps maps;
+    const Key key{base, a.plan.L, a.plan.nchunks, strides[0], br, cfg.promo, cfg.pf_lines};
+    if (key == last_key)
+        return launch_pdl(kern, a.plan.ctas, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring,
+                          cfg.pf_lines);
+    last_key = Key{nullptr, 0, 0, 0, 0, -1, -9};
     const CUtensorMapSwizzle swz = ROWB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                  : ROWB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
     const CUtensorMapL2promotion promo = cfg.promo == 0    ? CU_TENSOR_MAP_L2_PROMOTION_NONE
@@ -748,10 +785,15 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s
     CUresult r = enc(&maps.load, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    r = enc(&maps.pref, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, pbox, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (cfg.pf_lines >= 0) {  // the L2-prefetch map (off by default)
+        r = enc(&maps.pref, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, pbox, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    } else {
+        maps.pref = maps.load;
+    }
+    last_key = key;
     return launch_pdl(kern, a.plan.ctas, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring, cfg.pf_lines);
 }
 
@@ -772,7 +814,7 @@ template <class Step, bool VEC>
 cudaError_t direct_launch(const DirectArgs& a, cudaStream_t stream) {
     auto kern = k_scan_direct<Step, VEC>;
     const size_t smem = kDirectRed + 16 + table_bytes<Step>(a.t) + a.t.aux_bytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
     const uint64_t ctas = (a.npieces + kDirectWarps * 32 - 1) / (kDirectWarps * 32);
     return launch_pdl(kern, static_cast<unsigned>(ctas), kDirectWarps * 32, smem, stream, a);
@@ -783,9 +825,9 @@ cudaError_t batch_launch(const BatchArgs& a, int sm_count, cudaStream_t stream) 
     const size_t smem = table_bytes<Step>(a.t) + a.t.aux_bytes;
     auto scan = k_batch_scan<Step, VEC>;
     auto comb = k_batch_combine<Step, VEC>;
-    cudaError_t e = cudaFuncSetAttribute(scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = ensure_smem(scan, smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(comb, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    e = ensure_smem(comb, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan, kBatchWarps * 32, smem);
