@@ -8,7 +8,8 @@ one text of the workload, through the C-ABI (``sfa_match_async``), with the
 text already resident in HBM.  Default workload: BASELINE.json configs[1]
 (config 2: ``([0-4]{5}[5-9]{5})*`` over a 268,435,450-byte accepted text).
 The text (256 MiB) is larger than the 126 MB L2, so no flush is needed between
-steps.  ``--all`` adds per-config numbers for configs 1, 3, 4 and 5.
+steps.  ``--all`` adds per-config numbers for configs 1, 3, 4 and 5; ``--spec``
+adds the paper's baseline (Alg. 3, speculative DFA) timed on the same texts.
 
 Multi-GPU (torchrun): every rank matches its own copy of the workload (the
 texts are independent problems; no data-path collective), weak scaling;
@@ -222,7 +223,38 @@ def time_batch(torch, P, sfa, dtexts, doff, count, stream, steps, warmup, res):
     return e0.elapsed_time(e1) / steps
 
 
-def extra_config(torch, P, cfg, stream, steps, warmup, peak):
+def time_spec(torch, sfa, dtext, stream, steps, warmup, res):
+    """The paper's baseline, Alg. 3 (speculative DFA, |D| lookups per byte) on the same text."""
+    for _ in range(warmup):
+        sfa.match_speculative(dtext, res, 0, None, stream)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        sfa.match_speculative(dtext, res, 0, None, stream)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def spec_compare(torch, sfa, dtext, nbytes, sfa_ms, stream, warmup, expected):
+    """Alg. 3 beside the SFA on one text: GB/s, lookups per byte, and the SFA's speedup."""
+    res = torch.zeros(2, dtype=torch.int32, device="cuda")
+    nd = sfa.info()["dfa_states"]
+    # ~0.5 s of work at most: the speculative run does |D| lookups per byte
+    steps = max(1, min(50, int(0.5 / max(1e-6, nbytes * nd / 5e12))))
+    ms = time_spec(torch, sfa, dtext, stream, steps, min(warmup, 3), res)
+    got = tuple(int(x) for x in res.cpu().numpy().view(np.uint32))
+    if expected is not None and got != (expected[0], int(expected[1])):
+        raise SystemExit(f"speculative result {got} != {expected}")
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"value": gbs, "unit": UNIT, "ms_per_step": ms, "steps": steps, "lookups_per_byte": nd,
+            "lookups_per_s": gbs * 1e9 * nd, "sfa_speedup": ms / sfa_ms,
+            "kernel": "k_spec_scan (Alg. 3, PAPER.md:293-328: the DFA from every state per chunk)"}
+
+
+def extra_config(torch, P, cfg, stream, steps, warmup, peak, spec=False):
     rx, alpha, text = workload(cfg)
     sfa = P.SFA(rx, alpha)
     if cfg == 5:
@@ -231,7 +263,18 @@ def extra_config(torch, P, cfg, stream, steps, warmup, peak):
         do = torch.from_numpy(off.astype(np.int64)).cuda()
         count = off.size - 1
         res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
-        ms = time_batch(torch, P, sfa, dt, do, count, stream, steps, warmup, res)
+        ms_off = time_batch(torch, P, sfa, dt, do, count, stream, steps, warmup, res)
+        length = int(off[1] - off[0])
+        for _ in range(warmup):
+            sfa.match_batch_uniform(dt, length, count, res, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            sfa.match_batch_uniform(dt, length, count, res, stream)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
         nbytes = texts.size
     else:
         dt = torch.from_numpy(text).cuda()
@@ -240,9 +283,16 @@ def extra_config(torch, P, cfg, stream, steps, warmup, peak):
         nbytes = text.size
     gbs = nbytes / (ms * 1e-3) / 1e9
     info = sfa.info()
-    return {"workload": CONFIG_NAMES[cfg], "value": gbs, "unit": UNIT, "ms_per_step": ms, "bytes": int(nbytes),
-            "roofline_frac": gbs / peak, "residency": P.RES_NAMES.get(info["residency"], "?"),
-            "sfa_states": info["sfa_states"], "dfa_states": info["dfa_states"]}
+    out = {"workload": CONFIG_NAMES[cfg], "value": gbs, "unit": UNIT, "ms_per_step": ms, "bytes": int(nbytes),
+           "roofline_frac": gbs / peak, "residency": P.RES_NAMES.get(info["residency"], "?"),
+           "sfa_states": info["sfa_states"], "dfa_states": info["dfa_states"]}
+    if cfg == 5:
+        out["api"] = "sfa_match_batch_uniform"
+        out["offsets_api_gbs"] = nbytes / (ms_off * 1e-3) / 1e9
+    elif spec:
+        q, acc = sfa.match(dt, stream)
+        out["alg3_speculative"] = spec_compare(torch, sfa, dt, nbytes, ms, stream, warmup, (q, acc))
+    return out
 
 
 def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, peak_kind):
@@ -385,6 +435,8 @@ def main():
     ap.add_argument("--ref-bytes", type=int, default=64 << 20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shard", action="store_true", help="split ONE text over the ranks (strong scaling)")
+    ap.add_argument("--spec", action="store_true",
+                    help="also time the paper's baseline, Alg. 3 (speculative DFA), on each config's text")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -468,7 +520,10 @@ def main():
         for c in (1, 3, 4, 5):
             if c != cfg:
                 steps = 200 if c != 5 else 20
-                extras[f"cfg{c}"] = extra_config(torch, P, c, stream, steps, args.warmup, peak)
+                extras[f"cfg{c}"] = extra_config(torch, P, c, stream, steps, args.warmup, peak, args.spec)
+    spec_line = None
+    if args.spec and rank == 0:
+        spec_line = spec_compare(torch, sfa, dtext, text.size, ms_per_step, stream, args.warmup, expected)
 
     if rank != 0:
         if world > 1:
@@ -505,6 +560,8 @@ def main():
                 "api": "sfa_match_host (pinned host text, 64 MiB slices copied and matched in a pipeline)"},
         "gpu_launches": args.steps,
     }
+    if spec_line:
+        line["alg3_speculative"] = spec_line
     if extras:
         line["per_config"] = extras
     if not args.no_cpu:

@@ -189,6 +189,21 @@ SFA_API int sfa_combine_maps(const sfa_handle* h, const uint32_t* d_maps, size_t
                      sfa_result* d_result);
 
 /*
+ * sfa_match_speculative -- the paper's BASELINE, not the SFA: Alg. 3
+ * (PAPER.md:293-328), the DFA run speculatively from every state.  The text
+ * is cut into `nchunks` chunks by SPEC's rule (0 = as many as fill the GPU;
+ * > n means n one-byte chunks, C6); chunk i yields the mapping
+ * T_i[q] = delta^_d(q, chunk_i) for every DFA state q (|D| dependent lookups
+ * per byte), the T_i are composed in text order and
+ * (q_final = T[q0], [q_final in F_d]) is written to d_result (device).
+ * d_chunk_maps (device, nullable): receives T_i as min(nchunks, max(n, 1)) * |D|
+ * u32, row i = chunk i.  Async, stream-ordered.  n == 0: (0, [eps in L]).
+ * Same result as sfa_match_async for every input (Theorem 2).
+ */
+SFA_API int sfa_match_speculative(const sfa_handle* h, const uint8_t* d_text, size_t n, uint64_t nchunks,
+                          sfa_stream_t stream, uint32_t* d_chunk_maps, sfa_result* d_result);
+
+/*
  * sfa_match_host -- end-to-end call on a HOST buffer (pinned or pageable):
  * the text is copied to the device in slices on `stream` while earlier slices
  * are matched (each slice yields one SFA state; slices compose by Lemma 1,

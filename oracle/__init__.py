@@ -14,6 +14,8 @@ passages it follows) through ctypes:
 * ``.run(text)`` -- Alg. 2 (PAPER.md:259-272): ``(q_final, accept)``.
 * ``brute(regex, alphabet, s)`` -- the regex's meaning evaluated directly on
   the AST (position sets), the independent pin for the automata.
+* ``.run_spec(text, bounds)`` -- Alg. 3, the speculative
+  DFA baseline, per-chunk mappings and the sequential reduction.
 * ``OracleSFA(dfa)`` -- Alg. 4, for SFA-level pins, and
   ``.run_chunked`` -- Alg. 5 with both reductions.
 """
@@ -72,6 +74,8 @@ def lib():
         L.oracle_run.argtypes = [vp, u8p, C.c_uint64, u32p]
         L.oracle_run.restype = C.c_int
         L.oracle_run_batch.argtypes = [vp, u8p, u64p, C.c_uint64, u32p, u8p]
+        L.oracle_run_spec.argtypes = [vp, u8p, u64p, C.c_uint64, u32p, u32p]
+        L.oracle_run_spec.restype = C.c_int
         L.oracle_brute.argtypes = [C.c_char_p, u8p, C.c_int, u8p, C.c_int]
         L.oracle_brute.restype = C.c_int
         L.oracle_brute_all.argtypes = [C.c_char_p, u8p, C.c_int, u8p, C.c_int, C.c_int, u8p]
@@ -148,6 +152,20 @@ class OracleDFA:
         q = C.c_uint32()
         acc = lib().oracle_run(self._h, _ptr(a, C.c_uint8) if a.size else None, a.size, C.byref(q))
         return int(q.value), bool(acc)
+
+    def run_spec(self, text, bounds):
+        """Alg. 3 over chunks [bounds[i], bounds[i+1]):
+        returns (q_final, accept, T) with T[i, q] = delta^(q, chunk i)."""
+        a = _text(text)
+        b = np.ascontiguousarray(bounds, np.uint64)
+        p = b.size - 1
+        maps = np.zeros((max(p, 1), self.n), np.uint32)
+        q = C.c_uint32()
+        acc = lib().oracle_run_spec(self._h, _ptr(a, C.c_uint8) if a.size else None, _ptr(b, C.c_uint64), p,
+                                    _ptr(maps, C.c_uint32), C.byref(q))
+        if acc < 0:
+            raise MemoryError("oracle_run_spec")
+        return int(q.value), bool(acc), maps[:p]
 
     def run_batch(self, texts: np.ndarray, offsets: np.ndarray):
         texts = np.ascontiguousarray(texts, np.uint8)

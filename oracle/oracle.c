@@ -851,6 +851,32 @@ void oracle_run_batch(const oracle_dfa* d, const uint8_t* texts, const uint64_t*
     }
 }
 
+/* Alg. 3, parallel computation of the DFA by speculative
+ * simulation, written out sequentially: chunk i = text[bounds[i], bounds[i+1]);
+ * lines 2-3: T_i[q] <- q for every q; lines 4-6: for every byte sigma_ij and
+ * every q, T_i[q] <- delta(T_i[q], sigma_ij); then the sequential reduction
+ * (right column, lines 9-11; reading C8): q_final <- q0; q_final <- T_i[q_final]
+ * for i = 1..p.  maps (nullable) receives T_i as row i (p * |D| entries). */
+int oracle_run_spec(const oracle_dfa* d, const uint8_t* text, const uint64_t* bounds, uint64_t p,
+                    uint32_t* maps, uint32_t* q_final) {
+    const uint32_t* T = d->table;
+    const uint32_t nd = d->n;
+    uint32_t* Ti = malloc(sizeof(uint32_t) * (nd ? nd : 1));
+    if (!Ti) return -1;
+    uint32_t qf = 0;                                       /* q_final <- q0 */
+    for (uint64_t i = 0; i < p; i++) {
+        for (uint32_t q = 0; q < nd; q++) Ti[q] = q;        /* T_i[q] <- q */
+        for (uint64_t j = bounds[i]; j < bounds[i + 1]; j++)
+            for (uint32_t q = 0; q < nd; q++)
+                Ti[q] = T[(size_t)Ti[q] * 256 + text[j]];   /* T_i[q] <- delta(T_i[q], sigma_ij) */
+        if (maps) memcpy(maps + (size_t)i * nd, Ti, sizeof(uint32_t) * nd);
+        qf = Ti[qf];                                       /* q_final <- T_i[q_final] */
+    }
+    free(Ti);
+    if (q_final) *q_final = qf;
+    return d->finals[qf];
+}
+
 /* ------------------------------------------------------------------------ */
 /* Alg. 4 (D-SFA) and Alg. 5                                                 */
 /* ------------------------------------------------------------------------ */

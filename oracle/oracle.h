@@ -55,6 +55,12 @@ int oracle_run(const oracle_dfa* d, const uint8_t* text, uint64_t n, uint32_t* q
 void oracle_run_batch(const oracle_dfa* d, const uint8_t* texts, const uint64_t* off,
                       uint64_t count, uint32_t* q_final, uint8_t* accept);
 
+/* Alg. 3: speculative DFA per chunk [bounds[i], bounds[i+1]), i < p, with the
+ * sequential reduction.  Returns accept (0/1) or -1 (allocation), writes
+ * q_final and (maps != NULL) T_i[q] = delta^(q, chunk i) as p * |D| entries. */
+int oracle_run_spec(const oracle_dfa* d, const uint8_t* text, const uint64_t* bounds, uint64_t p,
+                    uint32_t* maps, uint32_t* q_final);
+
 /* Brute-force language evaluator on the AST (position-set semantics), for
  * strings of length <= 62.  Returns 1 match, 0 no match, -code on error. */
 int oracle_brute(const char* regex, const uint8_t* sigma, int sigma_len,

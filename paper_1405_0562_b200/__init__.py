@@ -56,7 +56,7 @@ class sfa_info_t(C.Structure):
 
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
-           "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform",
+           "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform", "sfa_match_speculative",
            "sfa_export_dfa", "sfa_export_sfa")
 
 _lib = None
@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
         L.sfa_match_map.argtypes = [vp, vp, C.c_size_t, vp, vp]
         L.sfa_match_batch_uniform.argtypes = [vp, vp, C.c_size_t, C.c_size_t, vp, vp]
         L.sfa_combine_maps.argtypes = [vp, vp, C.c_size_t, vp, vp]
+        L.sfa_match_speculative.argtypes = [vp, vp, C.c_size_t, C.c_uint64, vp, vp, vp]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
         for f in EXPORTS:
@@ -180,6 +181,19 @@ def sfa_match_map(h: int, d_text, d_map, n: int | None = None, stream=None):
 def sfa_combine_maps(h: int, d_maps, count: int, d_result, stream=None):
     """Stream-ordered: d_result (device, 2 x uint32) <- (q, accept) after the shard maps in order."""
     _check(lib().sfa_combine_maps(h, _dptr(d_maps) if count else None, count, _stream(stream), _dptr(d_result)))
+
+
+def sfa_match_speculative(h: int, d_text, d_result, nchunks: int = 0, d_chunk_maps=None, n: int | None = None,
+                          stream=None):
+    """The paper's baseline (Alg. 3): the DFA run speculatively from every state per chunk.
+
+    Stream-ordered: d_result (device, 2 x uint32) <- (q_final, accept); d_chunk_maps (device,
+    chunks x |D| uint32, optional) <- T_i[q] = delta^(q, chunk i).  nchunks = 0: automatic.
+    """
+    n = _nbytes(d_text) if n is None else n
+    _check(lib().sfa_match_speculative(h, _dptr(d_text) if n else None, n, nchunks, _stream(stream),
+                                       _dptr(d_chunk_maps) if d_chunk_maps is not None else None,
+                                       _dptr(d_result)))
 
 
 def sfa_match_batch_uniform(h: int, d_texts, length: int, count: int, d_results, stream=None):
@@ -297,6 +311,9 @@ class SFA:
 
     def combine_maps(self, d_maps, count, d_result, stream=None):
         return sfa_combine_maps(self.h, d_maps, count, d_result, stream)
+
+    def match_speculative(self, d_text, d_result, nchunks=0, d_chunk_maps=None, stream=None):
+        return sfa_match_speculative(self.h, d_text, d_result, nchunks, d_chunk_maps, None, stream)
 
     def match_host(self, h_text, stream=None):
         return sfa_match_host(self.h, h_text, stream)

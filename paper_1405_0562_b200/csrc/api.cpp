@@ -87,6 +87,10 @@ struct sfa_handle {
         const char* e = getenv("SFA_FACTOR");
         return !(e && e[0] == '0');
     }();
+    uint32_t* dspecT = nullptr;               // Alg. 3 baseline: DFA window table (kernels_spec.cu)
+    uint32_t* spec_maps = nullptr;            // Alg. 3: per-CTA maps (spec_cap entries)
+    uint32_t* spec_ticket = nullptr;
+    size_t spec_cap = 0;
     uint4* drep16 = nullptr;                  // rep(s) slots (depth <= 15)
     uint32_t* daux[2] = {nullptr, nullptr};   // aux smem images: [0] comp (TABLE), [1] maps32 (VEC)
     uint32_t aux_bytes[2] = {0, 0};
@@ -115,7 +119,7 @@ struct sfa_handle {
         for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
                         (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
                         (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1],
-                        (void*)dcomp, (void*)dpairs, (void*)dTdev, (void*)dfam, (void*)dfg, (void*)dftab, (void*)ddwin, (void*)dperm, (void*)diperm, (void*)drep16, (void*)daux[0],
+                        (void*)dcomp, (void*)dpairs, (void*)dTdev, (void*)dfam, (void*)dfg, (void*)dftab, (void*)ddwin, (void*)dperm, (void*)diperm, (void*)drep16, (void*)dspecT, (void*)spec_maps, (void*)spec_ticket, (void*)daux[0],
                         (void*)daux[1]})
             if (p) cudaFree(p);
         if (hres) cudaFreeHost(hres);
@@ -661,6 +665,25 @@ struct sfa_handle {
     // stream first waits for everything enqueued on the previous one.
     cudaStream_t last_stream = nullptr;
     bool has_last = false;
+    // Alg. 3 baseline: the DFA window table, u32 cells premultiplied to row
+    // byte offsets (4 W delta_d(q, byte)); column W-1 = every byte outside the
+    // window (one class, so any such byte represents it).
+    int upload_spec() {
+        if (dspecT) return SFA_OK;
+        const uint32_t nD = A.nD;
+        uint32_t ob = 0;
+        while (ob >= lo && ob + 1 < lo + W) ++ob;  // a byte outside [lo, lo + W - 2]
+        std::vector<uint32_t> Td((static_cast<size_t>(nD) * W + 3) & ~size_t(3), 0);
+        for (uint32_t q = 0; q < nD; ++q) {
+            for (uint32_t j = 0; j + 1 < W; ++j) Td[static_cast<size_t>(q) * W + j] = 4 * W * A.dfa[q * 256u + lo + j];
+            Td[static_cast<size_t>(q) * W + W - 1] = 4 * W * A.dfa[q * 256u + ob];
+        }
+        CU(upload(&dspecT, Td.data(), Td.size()));
+        CU(cudaMalloc(&spec_ticket, 16));
+        CU(cudaMemset(spec_ticket, 0, 16));
+        return SFA_OK;
+    }
+
     int begin(cudaStream_t stream) {
         int rc = ensure_uploaded();
         if (rc) return rc;
@@ -1063,6 +1086,57 @@ int sfa_match_batch_uniform(const sfa_handle* hc, const uint8_t* d_texts, size_t
     CU(cudaFreeAsync(d_off, s));
     CU(cudaStreamSynchronize(s));  // `off` is host memory of this frame
     return rc;
+}
+
+int sfa_match_speculative(const sfa_handle* hc, const uint8_t* d_text, size_t n, uint64_t nchunks, sfa_stream_t stream,
+                          uint32_t* d_chunk_maps, sfa_result* d_result) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !d_result) return fail(SFA_ERR_INVALID_ARG, "NULL handle or result");
+    if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    if (n == 0) {  // no chunk: T = identity, q_final = q0
+        if (d_chunk_maps) {
+            std::vector<uint32_t> id(h->A.nD);
+            for (uint32_t q = 0; q < h->A.nD; ++q) id[q] = q;
+            CU(cudaMemcpyAsync(d_chunk_maps, id.data(), id.size() * 4, cudaMemcpyHostToDevice, s));
+        }
+        h->hres[1] = sfa_result{0, h->A.dfa_final[0]};
+        CU(cudaMemcpyAsync(d_result, &h->hres[1], sizeof(sfa_result), cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));  // hres[1] and id are reused / freed
+        return h->end(s);
+    }
+    rc = h->upload_spec();
+    if (rc) return rc;
+    sfa::SpecArgs p, a;
+    p.Td = h->dspecT;
+    p.nD = h->A.nD;
+    p.W = h->W;
+    p.lo = h->lo;
+    p.dfinal = h->dfinal;
+    p.text = d_text;
+    uint32_t threads = 0;
+    size_t smem = 0;
+    cudaError_t e = sfa::spec_plan(p, h->sm_count, h->smem_optin, n, nchunks, &a, &threads, &smem);
+    if (e == cudaErrorInvalidConfiguration) return fail(SFA_ERR_CAPACITY, "DFA too large for the speculative kernel");
+    if (e != cudaSuccess) return cuda_fail(e, "speculative plan");
+    const size_t need = static_cast<size_t>(a.ctas) * h->A.nD;
+    if (h->spec_cap < need) {
+        if (h->spec_maps) CU(cudaFree(h->spec_maps));
+        h->spec_maps = nullptr;
+        h->spec_cap = 0;
+        CU(cudaMalloc(&h->spec_maps, need * 4));
+        h->spec_cap = need;
+    }
+    a.cta_maps = h->spec_maps;
+    a.ticket = h->spec_ticket;
+    a.chunk_maps = d_chunk_maps;
+    a.result = d_result;
+    e = sfa::launch_spec(a, threads, smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "speculative launch");
+    return h->end(s);
 }
 
 int sfa_match_host(const sfa_handle* hc, const uint8_t* h_text, size_t n, sfa_stream_t stream, uint32_t* final_state,

@@ -88,6 +88,30 @@ struct StepLaunch {
 cudaError_t launch_combine_maps(const uint32_t* maps, uint32_t count, uint32_t nD, const uint8_t* dfinal,
                                 sfa_result* result, cudaStream_t stream);
 
+// Alg. 3, speculative DFA simulation (kernels_spec.cu).
+struct SpecArgs {
+    const uint32_t* Td = nullptr;   // nD * W: 4 W delta_d(q, byte of column j), padded to 16 B
+    uint32_t nD = 0, W = 0, lo = 0;
+    const uint8_t* dfinal = nullptr;
+    const uint8_t* text = nullptr;
+    uint64_t n = 0, nchunks = 0;
+    uint64_t cpb = 0;               // chunks per CTA (a multiple of cpc)
+    uint32_t cpc = 0;               // chunks per pass (their |D| chains are the CTA's threads)
+    uint32_t gcap = 0;              // maps the smem group buffer holds
+    uint32_t tbl_smem = 0;          // bytes of the table in smem (0: read through L1/L2)
+    uint32_t ctas = 0;
+    uint32_t* cta_maps = nullptr;   // scratch: ctas * nD
+    uint32_t* ticket = nullptr;     // scratch: last-CTA-done counter (self-resetting, starts 0)
+    uint32_t* chunk_maps = nullptr; // optional: nchunks * nD, T_i[q] (Alg. 3 line 6)
+    uint32_t* map_out = nullptr;    // optional: nD, the text's mapping T
+    sfa_result* result = nullptr;
+};
+// Fills the launch shape (chunks, CTAs, smem) of a speculative run of n bytes
+// in nchunks chunks (0 = auto) into *out from proto's table fields.
+cudaError_t spec_plan(const SpecArgs& proto, int sm_count, size_t smem_optin, uint64_t n, uint64_t nchunks,
+                      SpecArgs* out, uint32_t* threads, size_t* smem);
+cudaError_t launch_spec(const SpecArgs& a, uint32_t threads, size_t smem, cudaStream_t stream);
+
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);
 cudaError_t launch_batch(Res mode, bool vec, const BatchArgs& a, int sm_count, cudaStream_t stream);

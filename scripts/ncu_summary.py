@@ -2,7 +2,7 @@
 into profiles/ncu_summary.json under a config key; bench.py reads the DRAM
 traffic per launch from there (roofline.traffic).
 
-    python scripts/ncu_summary.py <report.ncu-rep> <cfgN> [note]
+    python scripts/ncu_summary.py <report.ncu-rep | raw.csv> <cfgN> [note]
 """
 import csv
 import io
@@ -34,7 +34,11 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1,
 def main():
     rep, key = sys.argv[1], sys.argv[2]
     note = sys.argv[3] if len(sys.argv) > 3 else ""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` output, exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = {"kernel": vals[hdr.index("Kernel Name")], "report": os.path.basename(rep), "note": note}

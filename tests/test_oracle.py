@@ -363,3 +363,69 @@ def test_workload_recipes():
     tb = texts.tobytes()
     hits = [any(w in tb[off[i]:off[i + 1]] for w in words) for i in range(512)]
     assert np.flatnonzero(hits).tolist() == idx.tolist()
+
+
+# --------------------------------------------------------------------------- Alg. 3 (speculative DFA)
+def _bounds(rng, n, p):
+    cuts = np.sort(rng.integers(0, n + 1, size=p - 1))
+    return np.concatenate([[0], cuts, [n]]).astype(np.uint64)
+
+
+@pytest.mark.parametrize("rx,alpha", [CFG1, CFG2, CFG4, ("(ab)*", b"ab")])
+def test_spec_equals_alg2_on_any_chunking(rx, alpha):
+    """Alg. 3's ENSURE: q_final = delta^(q0, w), for any division
+    of w (empty chunks included) -- against Alg. 2 and, on short words, against
+    the brute-force evaluator of the regex."""
+    d = O.OracleDFA(rx, alpha)
+    rng = np.random.default_rng(31)
+    chars = np.frombuffer(alpha + b"x", np.uint8)
+    for n in (0, 1, 2, 9, 40, 333):
+        t = rng.choice(chars, size=n).astype(np.uint8)
+        for p in (1, 2, 5, 17):
+            q, acc, maps = d.run_spec(t, _bounds(rng, n, p))
+            assert (q, acc) == d.run(t)
+            assert maps.shape == (p, d.n)
+        if n <= 9:
+            assert d.run_spec(t, [0, n])[1] == O.brute(rx, alpha, bytes(t))
+
+
+def test_spec_maps_single_bytes_and_empty_chunk():
+    """Lines 2-6 on a one-byte chunk give the DFA column (T_i[q] = delta(q, b),
+    the DFA of Alg. 1 checked by the brute-force pins above); an empty chunk
+    gives the identity (lines 2-3)."""
+    d = O.OracleDFA(*CFG2)
+    t = np.frombuffer(b"07x", np.uint8)
+    _, _, maps = d.run_spec(t, [0, 1, 1, 2, 3])
+    q = np.arange(d.n)
+    assert (maps[0] == d.table.reshape(d.n, 256)[q, ord("0")]).all()
+    assert (maps[1] == q).all()
+    assert (maps[2] == d.table.reshape(d.n, 256)[q, ord("7")]).all()
+    assert (maps[3] == d.dead).all()  # 'x' is outside Sigma: every state to the dead state (C2)
+
+
+def test_spec_maps_compose_homomorphically():
+    """T_{uv} = T_u . T_v with (f . g)(q) = g(f(q)): the chunk
+    map of a concatenation is the composition of the chunk maps, in order."""
+    d = O.OracleDFA(*CFG4)
+    rng = np.random.default_rng(5)
+    t = rng.choice(np.frombuffer(b"ab", np.uint8), size=200).astype(np.uint8)
+    _, _, whole = d.run_spec(t, [0, 200])
+    _, _, parts = d.run_spec(t, [0, 61, 200])
+    assert (whole[0] == parts[1][parts[0]]).all()
+    # closed form: cfg4's DFA remembers the last 9 bytes, so after >= 9 bytes
+    # every live start state lands in the same state; the dead state (reached
+    # only by out-of-Sigma bytes, C2) stays dead
+    live = np.arange(d.n) != d.dead
+    assert (whole[0][live] == whole[0][0]).all() and whole[0][d.dead] == d.dead
+
+
+def test_spec_cfg2_block_closed_form():
+    """Config 2: one accepted 10-byte block sends q0 back to q0 (the language
+    is (block)*) and the dead state to itself; a full accepted text is accepted
+    from q0 on any chunking."""
+    d = O.OracleDFA(*CFG2)
+    blk = W.cfg2_accepted(1)
+    _, _, m = d.run_spec(blk, [0, 10])
+    assert m[0][0] == 0 and m[0][d.dead] == d.dead
+    t = W.cfg2_accepted(1000)
+    assert d.run_spec(t, np.linspace(0, t.size, 8).astype(np.uint64)) [:2] == (0, True)
