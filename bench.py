@@ -9,7 +9,8 @@ text already resident in HBM.  Default workload: BASELINE.json configs[1]
 (config 2: ``([0-4]{5}[5-9]{5})*`` over a 268,435,450-byte accepted text).
 The text (256 MiB) is larger than the 126 MB L2, so no flush is needed between
 steps.  ``--all`` adds per-config numbers for configs 1, 3, 4 and 5; ``--spec``
-adds the paper's baseline (Alg. 3, speculative DFA) timed on the same texts.
+adds the paper's baseline (Alg. 3, speculative DFA) timed on the same texts;
+``--rn`` runs the paper's r_n scalability family (1 GiB accepted texts).
 
 Multi-GPU (torchrun): every rank matches its own copy of the workload (the
 texts are independent problems; no data-path collective), weak scaling;
@@ -254,6 +255,35 @@ def spec_compare(torch, sfa, dtext, nbytes, sfa_ms, stream, warmup, expected):
             "kernel": "k_spec_scan (Alg. 3, PAPER.md:293-328: the DFA from every state per chunk)"}
 
 
+def rn_family(torch, P, stream, warmup, peak, nbytes):
+    """SURVEY 8(f) NEXT-2, the paper's scalability study on the GPU:
+    r_n on an accepted text and r_a on "a"^m, the SFA beside Alg. 3 (speculative DFA)."""
+    import workloads as W
+    out = {}
+    cases = [(f"r{n}", W.rn_regex(n), b"0123456789", lambda n=n: W.rn_accepted(n, nbytes))
+             for n in (5, 10, 20, 50, 100, 127)]
+    cases.append(("ra127", W.ra_regex(127), b"0123456789a", lambda: W.ra_text(nbytes)))
+    for name, rx, alpha, gen in cases:
+        text = gen()
+        sfa = P.SFA(rx, alpha)
+        dt = torch.from_numpy(text).cuda()
+        res = torch.zeros(2, dtype=torch.int32, device="cuda")
+        q, acc = sfa.match(dt, stream)
+        if not acc:
+            raise SystemExit(f"{name}: the accepted text was rejected ({q})")
+        steps = 50
+        ms = time_single(torch, P, sfa, dt, stream, steps, warmup, res)
+        gbs = text.size / (ms * 1e-3) / 1e9
+        info = sfa.info()
+        out[name] = {"regex": rx, "bytes": int(text.size), "dfa_states": info["dfa_states"],
+                     "sfa_states": info["sfa_states"], "residency": P.RES_NAMES.get(info["residency"], "?"),
+                     "value": gbs, "unit": UNIT, "ms_per_step": ms, "roofline_frac": gbs / peak,
+                     "alg3_speculative": spec_compare(torch, sfa, dt, text.size, ms, stream, warmup, (q, acc))}
+        del dt
+        sfa.close()
+    return out
+
+
 def extra_config(torch, P, cfg, stream, steps, warmup, peak, spec=False):
     rx, alpha, text = workload(cfg)
     sfa = P.SFA(rx, alpha)
@@ -435,6 +465,11 @@ def main():
     ap.add_argument("--ref-bytes", type=int, default=64 << 20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shard", action="store_true", help="split ONE text over the ranks (strong scaling)")
+    ap.add_argument("--residency", type=int, default=0,
+                    help="diagnostic: force a residency mode (1 PRIVATE, 2 SHARED, 3 HOT, 4 L2; 0 = auto)")
+    ap.add_argument("--rn", action="store_true",
+                    help="also run the r_n scalability family (r5..r127, r_a) with Alg. 3 beside it")
+    ap.add_argument("--rn-bytes", type=int, default=1 << 30)
     ap.add_argument("--spec", action="store_true",
                     help="also time the paper's baseline, Alg. 3 (speculative DFA), on each config's text")
     args = ap.parse_args()
@@ -456,6 +491,8 @@ def main():
     cfg = args.config
     rx, alpha, text = workload(cfg)
     sfa = P.SFA(rx, alpha)
+    if args.residency:
+        sfa.set_residency(args.residency)
     stream = torch.cuda.Stream()
     if cfg == 5:
         return bench_batch(args, torch, P, sfa, rx, alpha, text, stream, world, rank, local, peak, peak_kind, peaks)
@@ -521,6 +558,7 @@ def main():
             if c != cfg:
                 steps = 200 if c != 5 else 20
                 extras[f"cfg{c}"] = extra_config(torch, P, c, stream, steps, args.warmup, peak, args.spec)
+    rn = rn_family(torch, P, stream, args.warmup, peak, args.rn_bytes) if args.rn and rank == 0 else None
     spec_line = None
     if args.spec and rank == 0:
         spec_line = spec_compare(torch, sfa, dtext, text.size, ms_per_step, stream, args.warmup, expected)
@@ -560,6 +598,8 @@ def main():
                 "api": "sfa_match_host (pinned host text, 64 MiB slices copied and matched in a pipeline)"},
         "gpu_launches": args.steps,
     }
+    if rn:
+        line["rn_family"] = rn
     if spec_line:
         line["alg3_speculative"] = spec_line
     if extras:

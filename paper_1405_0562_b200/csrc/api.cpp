@@ -525,6 +525,13 @@ struct sfa_handle {
             *out = m;
             return SFA_OK;
         }
+        // TMA scan: a factorable automaton whose DFA window gets more lane copies
+        // than the PRIVATE SFA table (fewer bank conflicts per lookup) runs
+        // HOT + FACTORED (cfg4: R = 32 DFA copies against R = 16 SFA copies).
+        if (kind == 0 && dfam && factor_on && dwin_R > priv_R && fits(sfa::Res::Hot, kind)) {
+            *out = sfa::Res::Hot;
+            return SFA_OK;
+        }
         for (sfa::Res m : {sfa::Res::Private, sfa::Res::Shared, sfa::Res::Hot, sfa::Res::Global})
             if (fits(m, kind)) {
                 *out = m;

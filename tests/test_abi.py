@@ -218,3 +218,18 @@ def test_set_compose_capacity():
         P.sfa_set_compose(h, m)
     assert P.sfa_info(h)["compose_mode"] == P.COMPOSE_TABLE
     P.sfa_free(h)
+
+
+def test_rn_family_through_product():
+    """r_n: |S| = |D|^2 + |D| - 1 (live) up to the largest n
+    whose D-SFA fits u16 ids (n = 127: 64,770 states); r_500's D-SFA
+    (1,000,999 states) is refused with CAPACITY (reading C16)."""
+    for n in (10, 100, 127):
+        h = P.sfa_compile("([0-4]{%d}[5-9]{%d})*" % (n, n), b"0123456789")
+        info = P.sfa_info(h)
+        P.sfa_free(h)
+        live = info["dfa_states"] - 1
+        assert live == 2 * n and info["sfa_states"] - 1 == live * live + live - 1
+    with pytest.raises(P.SFAError) as e:
+        P.sfa_compile("([0-4]{500}[5-9]{500})*", b"0123456789")
+    assert e.value.code == 3

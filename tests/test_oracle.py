@@ -429,3 +429,11 @@ def test_spec_cfg2_block_closed_form():
     assert m[0][0] == 0 and m[0][d.dead] == d.dead
     t = W.cfg2_accepted(1000)
     assert d.run_spec(t, np.linspace(0, t.size, 8).astype(np.uint64)) [:2] == (0, True)
+
+
+def test_rn_dfa_sizes_printed_for_r500_and_ra():
+    """The r_500 and r_a captions (|D| = 1000 and 1002, no dead state, C4)."""
+    for line in golden_lines("rn_dfa_sizes.txt"):
+        name, regex, alpha, nd, _cite = line.split("\t")
+        d = O.OracleDFA(regex, alpha)
+        assert d.dead >= 0 and d.live == int(nd), name

@@ -233,3 +233,33 @@ def ragged_batch(seed: int, count: int, max_len: int, alphabet: bytes) -> tuple:
     off = np.zeros(count + 1, np.uint64)
     off[1:] = np.cumsum(lens)
     return t, off
+
+
+# --------------------------------------------------------------------------- r_n family
+# r_n = ([0-4]{n}[5-9]{n})*, "1GB string accepted
+# by those automata"; r_a = r_n|a* on a repetition of "a".
+# Streams: SeedSequence(1000 + n), so every n has its own text.
+RN_BYTES = 1 << 30
+
+
+def rn_regex(n: int) -> str:
+    return f"([0-4]{{{n}}}[5-9]{{{n}}})*"
+
+
+def rn_accepted(n: int, nbytes: int = RN_BYTES) -> np.ndarray:
+    """Back-to-back blocks of n digits U('0'..'4') then n digits U('5'..'9'),
+    as many whole blocks as fit in nbytes (so the text is accepted)."""
+    blocks = max(1, nbytes // (2 * n))
+    rng = np.random.default_rng(np.random.SeedSequence(1000 + n))
+    t = np.empty((blocks, 2 * n), np.uint8)
+    t[:, :n] = rng.integers(48, 53, size=(blocks, n), dtype=np.uint8)
+    t[:, n:] = rng.integers(53, 58, size=(blocks, n), dtype=np.uint8)
+    return t.reshape(-1)
+
+
+def ra_regex(n: int) -> str:
+    return f"{rn_regex(n)}|a*"
+
+
+def ra_text(nbytes: int = RN_BYTES) -> np.ndarray:
+    return np.full(nbytes, 97, np.uint8)
