@@ -598,8 +598,14 @@ struct sfa_handle {
             const uint64_t body = n - head;
             // rows of L bytes (a multiple of 256), at most G*R of them, spread
             // evenly over G CTAs in multiples of NB (TMA box count x alignment)
-            uint64_t L = 256 * ((body + 256 * G * R - 1) / (256 * G * R));
-            if (L == 0) L = 256;
+            static const uint64_t align = [] {  // diagnostic: SFA_ROW_ALIGN (16..256, power of 2)
+                const char* e = getenv("SFA_ROW_ALIGN");
+                const uint64_t v = e ? static_cast<uint64_t>(atoi(e)) : 256u;
+                return (v >= 16 && v <= 256 && !(v & (v - 1))) ? v : 256u;
+            }();
+            const uint64_t al = std::max<uint64_t>(align, static_cast<uint64_t>(cfg.rowb));  // whole stages per row
+            uint64_t L = al * ((body + al * G * R - 1) / (al * G * R));
+            if (L < 256) L = 256;
             const uint64_t rows = body / L;
             const uint64_t rc = NB * ((rows + G * NB - 1) / (G * NB));
             a.plan.head = head;

@@ -91,6 +91,17 @@ struct Comp<Step, false> {
             const uint32_t i = a * t.nS + b;
             return t.comp_u8 ? static_cast<const uint8_t*>(t.comp)[i] : static_cast<const uint16_t*>(t.comp)[i];
         }
+        if (t.fact_fam && t.maps16) {
+            // a factorable: f_a = (family F, g) sends its unmarked q to g and the
+            // marked ones to absorbing states, which f_b fixes; so f_a . f_b =
+            // (F, f_b(g)) -- one mapping lookup instead of a replay of rep(b).
+            const uint32_t fa = __ldg(t.fact_fam + a);
+            if (fa != 0xffffu) {
+                const uint32_t gb = __ldg(t.maps16 + static_cast<uint64_t>(b) * t.nD + __ldg(t.fact_g + a));
+                const uint32_t r = __ldg(t.fact_tab + fa * t.nD + gb);
+                if (r != 0xffffu) return r;
+            }
+        }
         return replay(S, t, a, b, lane_id());
     }
     // the 32 lanes' ids, in lane order, folded by a shuffle tree; result in every lane
