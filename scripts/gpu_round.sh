@@ -11,6 +11,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; echo "bench rc=$?"
 timeout 900 python bench.py --all --spec --steps 300 --no-cpu > gpurun_out/bench_all_$tag.json 2> gpurun_out/bench_all_$tag.err; echo "bench-all rc=$?"
 timeout 900 python bench.py --config 5 --steps 20 --no-cpu > gpurun_out/bench_c5_$tag.json 2> gpurun_out/bench_c5_$tag.err; echo "bench-c5 rc=$?"
+timeout 900 python bench.py --rn --steps 100 --no-cpu --e2e-steps 1 > gpurun_out/bench_rn_$tag.json 2> gpurun_out/bench_rn_$tag.err; echo "bench-rn rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err; echo "bench-ref rc=$?"
 CMD="python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu"
 $CMD > gpurun_out/plain_launch_$tag.log 2>&1 && \
