@@ -632,7 +632,7 @@ k_batch_scan(const BatchArgs a) {
         const uint32_t ntasks = a.task_off[i + 1] - a.task_off[i];
         const uint64_t t0 = a.off[i], t1 = max(t0, a.off[i + 1]);
         const uint64_t s0 = min(t1, t0 + j * a.seg), s1 = min(t1, s0 + a.seg);
-        const uint64_t per = (((s1 - s0) + 31) / 32 + 15) & ~uint64_t(15);
+        const uint64_t per = (((s1 - s0) + 31) / 32 + 31) & ~uint64_t(31);  // whole 32-B sectors per lane
         const uint64_t p0 = min(s1, s0 + lane * per), p1 = min(s1, p0 + per);
         uint32_t s;
         if constexpr (Step::kFactor) {  // 32 bytes through the SFA table, then the factored step if all lanes allow
@@ -643,12 +643,12 @@ k_batch_scan(const BatchArgs a) {
             if (__all_sync(kFull, ok)) {
                 StepDfa D;
                 D.params(t);
-                s = fact_to_id(t, fam, run_range(D, g, a.texts, pm, p1));
+                s = fact_to_id(t, fam, run_range32(D, g, a.texts, pm, p1));
             } else {
-                s = S.id(run_range(S, s0, a.texts, pm, p1), lane);
+                s = S.id(run_range32(S, s0, a.texts, pm, p1), lane);
             }
         } else {
-            s = S.id(run_range(S, S.init(lane), a.texts, p0, p1), lane);
+            s = S.id(run_range32(S, S.init(lane), a.texts, p0, p1), lane);
         }
         const uint32_t val = CP::fold_states(S, t, s);
         if (ntasks == 1) {
