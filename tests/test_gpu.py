@@ -470,3 +470,21 @@ def test_batch_uniform(torch_cuda, rx, alpha, compose):
         off = np.arange(count + 1, dtype=np.uint64) * length
         qo, ao = d.run_batch(body, off)
         assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all(), (length, count, pad)
+
+
+def test_row_alignment_choices(torch_cuda):
+    """Text sizes for which the TMA plan picks 256-, 128- and 64-byte row
+    lengths (rows used vs DRAM cost, api.cpp), with ragged heads and tails,
+    for the PRIVATE (cfg2) and HOT + FACTORED (cfg4) scans."""
+    torch = torch_cuda
+    rng = np.random.default_rng(21)
+    for (rx, alpha), gen in ((CFG2, lambda n: W.cfg2_accepted(n // 10 + 1)), (CFG4, W.cfg4_text)):
+        sfa = P.SFA(rx, alpha)
+        d = oracle_pair(rx, alpha)
+        big = gen(300 << 20)
+        for n in (40_000_003, 97_000_000, 150 << 20, 268_435_450, 299_999_999):
+            t = big[:n]
+            if rng.random() < 0.5:
+                t = t.copy()
+                t[rng.integers(0, n)] ^= np.uint8(1)
+            check_text(torch, sfa, d, t, int(rng.integers(0, 16)))
