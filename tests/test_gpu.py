@@ -205,6 +205,14 @@ def test_cfg5_full_size_batch(torch_cuda):
     qo, acco = d.run_batch(texts, off)
     assert (q == qo).all() and (acc == acco).all()
     assert np.flatnonzero(acc).tolist() == idx.tolist()        # exactly the planted texts
+    # the launch configuration bench.py times: equal texts through sfa_match_batch_uniform
+    count, length = off.size - 1, int(off[1] - off[0])
+    dt = torch.from_numpy(texts).cuda()
+    res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
+    sfa.match_batch_uniform(dt, length, count, res)
+    torch.cuda.synchronize()
+    r = res.cpu().numpy().view(np.uint32).reshape(count, 2)
+    assert (r[:, 0] == qo).all() and (r[:, 1] == acco).all()
 
 
 @pytest.mark.parametrize("rx,alpha", [CFG1, CFG2, CFG4, (W.cfg3_regex(), None)])
