@@ -36,7 +36,8 @@ int cuda_fail(cudaError_t e, const char* where) {
     } while (0)
 
 constexpr uint64_t kTmaMin = 4ull << 20;       // below: k_scan_direct
-constexpr uint64_t kDirectPiece = 64;          // bytes per thread in k_scan_direct
+constexpr uint64_t kDirectPiece = 64;          // bytes per thread in k_scan_direct (at least)
+constexpr uint64_t kDirectPieceMax = 512;      // ... and at most (texts < kTmaMin)
 constexpr uint32_t kMaxSlots = (1u << 16) + 2; // partial slots (CTAs + tail)
 constexpr uint64_t kSlice = 64ull << 20;       // sfa_match_host slice
 constexpr uint64_t kBatchSeg = 64ull << 10;    // bytes per batch task
@@ -565,7 +566,18 @@ struct sfa_handle {
             a.t = tables(mode, 1);
             a.text = d_text;
             a.n = n;
-            a.npieces = force_pieces ? force_pieces : std::max<uint64_t>(1, (n + kDirectPiece - 1) / kDirectPiece);
+            // Bytes per thread: about 8192 threads (32 CTAs) until pieces reach
+            // 512 B.  Every CTA builds its own smem table, so more, shorter pieces
+            // cost more than their shorter chains save (3 MiB, cfg2: 12.3 us at
+            // 64-B pieces, 6.5 us at 384-512).  SFA_DIRECT_PIECE (diagnostic) forces one.
+            static const uint64_t forced_piece = [] {
+                const char* e = getenv("SFA_DIRECT_PIECE");
+                const long v = e ? atol(e) : 0;
+                return v >= 16 && v <= 4096 ? static_cast<uint64_t>(v) : 0u;
+            }();
+            const uint64_t piece =
+                forced_piece ? forced_piece : std::min<uint64_t>(kDirectPieceMax, std::max<uint64_t>(kDirectPiece, n / 8192));
+            a.npieces = force_pieces ? force_pieces : std::max<uint64_t>(1, (n + piece - 1) / piece);
             a.sc = scratch();
             a.q_in = q_in;
             a.result = d_result;
