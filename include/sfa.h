@@ -144,26 +144,36 @@ SFA_API int sfa_match(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_
 
 /* Same work as sfa_match, stream-ordered and non-blocking: the result is
  * written to device memory d_result (8 bytes, caller-owned) when the stream
- * reaches it.  Suitable for CUDA-event timing and graph capture. */
+ * reaches it (n == 0 included: a one-thread kernel writes it).  No host
+ * synchronisation, no host<->device copy: suitable for CUDA-event timing and
+ * graph capture. */
 SFA_API int sfa_match_async(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_stream_t stream,
                     sfa_result* d_result);
 
 /*
- * sfa_match_batch -- count independent texts, text i = d_texts[d_offsets[i] :
- * d_offsets[i+1]).  d_offsets (count+1 uint64, device) must be non-decreasing
- * (not checked on the host: it is device memory; a decreasing pair yields an
- * empty text).  Writes d_results[i] (device, count entries).  Async,
- * stream-ordered.  count == 0 is a no-op; an empty text gives (0, [eps in L]).
+ * sfa_match_batch -- count independent texts (A5, the "naive" parallelism over
+ * data of PAPER.md:67-70), text i = d_texts[d_offsets[i] : d_offsets[i+1]).
+ *   d_texts    device pointer the offsets index (any alignment), caller-owned.
+ *   d_offsets  count+1 uint64, device, caller-owned; must be non-decreasing.
+ *   d_results  count sfa_result, device, caller-owned.
+ * Async and stream-ordered: the call only enqueues work (no host read of the
+ * offsets, no synchronisation).  The texts, back to back, are scanned as one
+ * range by the TMA pipeline with every text boundary honoured in place; a
+ * device-side plan kernel validates the offsets.  If any pair decreases (or
+ * d_offsets[count] < d_offsets[0]) EVERY result is written as
+ * {SFA_INVALID_STATE, 0}.  count == 0 is a no-op; an empty text gives
+ * (0, [eps in L]).  Scratch is per handle (matches on one handle serialise).
+ * Errors (returned): INVALID_ARG (NULL pointers, count > 2^31), CAPACITY, CUDA.
  */
+#define SFA_INVALID_STATE 0xffffffffu
 SFA_API int sfa_match_batch(const sfa_handle* h, const uint8_t* d_texts, const uint64_t* d_offsets,
                     size_t count, sfa_stream_t stream, sfa_result* d_results);
 
 /*
  * sfa_match_batch_uniform -- `count` texts of `len` bytes each, back to back
- * at d_texts (device; text i = d_texts[i*len : (i+1)*len)).  Same results as
- * sfa_match_batch with offsets i*len; async, stream-ordered.  When d_texts is
- * 16-byte aligned and len a multiple of 256, the texts go through the TMA
- * scan as a [rows x len/m] tensor (m rows per text) with a per-text fold.
+ * at d_texts (device, any alignment; text i = d_texts[i*len : (i+1)*len)).
+ * Same results as sfa_match_batch with offsets i*len and the same kernel; the
+ * plan is made on the host (no offsets array).  Async, stream-ordered.
  */
 SFA_API int sfa_match_batch_uniform(const sfa_handle* h, const uint8_t* d_texts, size_t len, size_t count,
                             sfa_stream_t stream, sfa_result* d_results);
@@ -197,7 +207,9 @@ SFA_API int sfa_combine_maps(const sfa_handle* h, const uint32_t* d_maps, size_t
  * per byte), the T_i are composed in text order and
  * (q_final = T[q0], [q_final in F_d]) is written to d_result (device).
  * d_chunk_maps (device, nullable): receives T_i as min(nchunks, max(n, 1)) * |D|
- * u32, row i = chunk i.  Async, stream-ordered.  n == 0: (0, [eps in L]).
+ * u32, row i = chunk i; it needs nchunks > 0 (INVALID_ARG otherwise: the
+ * automatic count is not reported).  Async, stream-ordered.  n == 0:
+ * (0, [eps in L]) and, with d_chunk_maps, the identity in row 0.
  * Same result as sfa_match_async for every input (Theorem 2).
  */
 SFA_API int sfa_match_speculative(const sfa_handle* h, const uint8_t* d_text, size_t n, uint64_t nchunks,
@@ -224,6 +236,23 @@ SFA_API int sfa_match_host(const sfa_handle* h, const uint8_t* h_text, size_t n,
 SFA_API int sfa_match_chunked(const sfa_handle* h, const uint8_t* d_text, size_t n, uint32_t nchunks,
                       sfa_stream_t stream, uint32_t* final_state, int* accept, uint32_t* h_chunk_states);
 
+/*
+ * sfa_match_rows -- diagnostic view of the TMA scan (the kernel sfa_match
+ * times for texts >= 4 MiB), forced for any n >= 64 KiB: writes the canonical
+ * SFA id of every row (chunk) to d_row_ids (device, row_cap u32, caller-owned;
+ * CAPACITY if the plan has more rows), the result to d_result (device) and the
+ * row geometry to *plan (host): head piece [0, head), rows [head + r*row_len,
+ * head + (r+1)*row_len) for r < rows, tail [tail_start, n).  The ids are
+ * Alg. 5 lines 1-5 per chunk (Lemma 1 / Thm. 3,
+ * PAPER.md:434-479).  Async, stream-ordered.
+ */
+typedef struct {
+    uint64_t head, row_len, rows, tail_start;
+    uint32_t ctas, rows_hi, rows_lo, ctas_hi;  /* the first ctas_hi CTAs scan rows_hi rows, the rest rows_lo */
+} sfa_rows_plan;
+SFA_API int sfa_match_rows(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_stream_t stream,
+                           uint32_t* d_row_ids, size_t row_cap, sfa_rows_plan* plan, sfa_result* d_result);
+
 /* Forces a residency mode (SFA_RES_*); CAPACITY if it does not fit. */
 SFA_API int sfa_set_residency(sfa_handle* h, int mode);
 
@@ -231,15 +260,36 @@ SFA_API int sfa_set_residency(sfa_handle* h, int mode);
  * sample of text (the first min(n, 8 MiB) bytes of d_sample, device memory,
  * caller-owned; copied to the host on `stream`), so the most visited rows sit
  * in shared memory.  Blocking: waits for earlier work of the handle, then
- * rewrites the HOT tables.  n == 0 restores the static ranking.  Without a
- * call, the first HOT match of the handle tunes on its own text (environment
- * SFA_HOT_AUTOTUNE=0 disables that).  Results never depend on the ranking. */
+ * rewrites the HOT tables.  n == 0 restores the static ranking (the default:
+ * no match call ever tunes on its own).  Results never depend on the ranking. */
 SFA_API int sfa_tune_residency(sfa_handle* h, const uint8_t* d_sample, size_t n, sfa_stream_t stream);
 
 /* Forces a composition mode (SFA_COMPOSE_*); CAPACITY if the handle cannot
  * use it (VEC needs |D| <= 32, TABLE |S| <= 4096).  Results do not depend on
  * it (composition is exact); only the epilogue cost does. */
 SFA_API int sfa_set_compose(sfa_handle* h, int mode);
+
+/*
+ * sfa_set_tuning -- launch-shape knobs for measurements and tests (NULL or a
+ * zeroed struct = automatic).  None of them can change a result: every shape
+ * computes the same exact Alg. 5.  Blocking: waits for the handle's device
+ * work and drops its device tables (rebuilt by the next device call).
+ * INVALID_ARG for a value out of range.  The library reads no environment
+ * variable.
+ */
+typedef struct {
+    int32_t tma_k;            /* chunks per compute thread of the TMA scan: 0 auto, 1 or 2     */
+    int32_t tma_rowb;         /* bytes per row per pipeline stage: 0 auto, 16/32/64 (needs tma_k) */
+    int32_t tma_ring;         /* cap on the stage-ring depth: 0 = as deep as fits, 2..8        */
+    int32_t tma_promo;        /* L2 promotion of the TMA loads: 0 none (auto), 64, 128, 256    */
+    uint32_t hot_rows;        /* HOT residency: cap on the rows kept in smem (0 = all that fit) */
+    uint32_t no_factor;       /* 1: never use the FACTORED step                                */
+    uint32_t dfa_copies;      /* FACTORED: cap on lane-group copies of the DFA window (0 = 32)  */
+    uint32_t private_copies;  /* PRIVATE: cap on lane-group copies of the SFA table (0 = 32)    */
+    uint32_t row_align;       /* TMA row length alignment: 0 auto, 64, 128 or 256              */
+    uint32_t direct_piece;    /* bytes per thread of the short-text kernel: 0 auto, 16..4096   */
+} sfa_tuning_t;
+SFA_API int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* t);
 
 /* Minimal DFA over all 256 bytes: table |D|*256 canonical ids, finals |D| (0/1). */
 SFA_API int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals);

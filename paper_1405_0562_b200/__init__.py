@@ -13,8 +13,9 @@ for device memory and streams.
 
 Functions keep the C names: ``sfa_compile``, ``sfa_match``,
 ``sfa_match_async``, ``sfa_match_batch``, ``sfa_match_host``,
-``sfa_match_chunked``, ``sfa_set_residency``, ``sfa_set_compose``, ``sfa_info``,
-``sfa_export_dfa``, ``sfa_export_sfa``, ``sfa_free``; ``SFA`` wraps a handle.
+``sfa_match_chunked``, ``sfa_match_rows``, ``sfa_set_residency``, ``sfa_set_compose``,
+``sfa_set_tuning``, ``sfa_info``, ``sfa_export_dfa``, ``sfa_export_sfa``, ``sfa_free``;
+``SFA`` wraps a handle.
 """
 from __future__ import annotations
 
@@ -54,10 +55,23 @@ class sfa_info_t(C.Structure):
     ]
 
 
+class sfa_tuning_t(C.Structure):
+    _fields_ = [("tma_k", C.c_int32), ("tma_rowb", C.c_int32), ("tma_ring", C.c_int32), ("tma_promo", C.c_int32),
+                ("hot_rows", C.c_uint32), ("no_factor", C.c_uint32), ("dfa_copies", C.c_uint32),
+                ("private_copies", C.c_uint32), ("row_align", C.c_uint32), ("direct_piece", C.c_uint32)]
+
+
+class sfa_rows_plan(C.Structure):
+    _fields_ = [("head", C.c_uint64), ("row_len", C.c_uint64), ("rows", C.c_uint64), ("tail_start", C.c_uint64),
+                ("ctas", C.c_uint32), ("rows_hi", C.c_uint32), ("rows_lo", C.c_uint32), ("ctas_hi", C.c_uint32)]
+
+
+INVALID_STATE = 0xFFFFFFFF
+
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
            "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform", "sfa_match_speculative",
-           "sfa_export_dfa", "sfa_export_sfa")
+           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows")
 
 _lib = None
 
@@ -87,6 +101,8 @@ def lib() -> C.CDLL:
         L.sfa_match_batch_uniform.argtypes = [vp, vp, C.c_size_t, C.c_size_t, vp, vp]
         L.sfa_combine_maps.argtypes = [vp, vp, C.c_size_t, vp, vp]
         L.sfa_match_speculative.argtypes = [vp, vp, C.c_size_t, C.c_uint64, vp, vp, vp]
+        L.sfa_set_tuning.argtypes = [vp, C.POINTER(sfa_tuning_t)]
+        L.sfa_match_rows.argtypes = [vp, vp, C.c_size_t, vp, vp, C.c_size_t, C.POINTER(sfa_rows_plan), vp]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
         for f in EXPORTS:
@@ -239,6 +255,32 @@ def sfa_tune_residency(h: int, d_sample=None, n: int | None = None, stream=None)
     _check(lib().sfa_tune_residency(h, _dptr(d_sample), n, _stream(stream)))
 
 
+def sfa_set_tuning(h: int, **knobs):
+    """Launch-shape knobs (sfa_tuning_t field names; none changes a result).  No
+    arguments: back to automatic.  Blocking; the device tables are rebuilt lazily."""
+    if not knobs:
+        _check(lib().sfa_set_tuning(h, None))
+        return
+    t = sfa_tuning_t()
+    t.tma_promo = -1
+    for k, v in knobs.items():
+        if k not in dict(sfa_tuning_t._fields_):
+            raise ValueError(f"unknown tuning knob {k}")
+        setattr(t, k, int(v))
+    _check(lib().sfa_set_tuning(h, C.byref(t)))
+
+
+def sfa_match_rows(h: int, d_text, d_row_ids, d_result, n: int | None = None, stream=None) -> dict:
+    """TMA scan with its per-row SFA ids (diagnostic; n >= 64 KiB): stream-ordered writes of
+    d_row_ids (device u32) and d_result; returns the row geometry."""
+    n = _nbytes(d_text) if n is None else n
+    p = sfa_rows_plan()
+    cap = d_row_ids.numel() if not isinstance(d_row_ids, int) else 1 << 40
+    _check(lib().sfa_match_rows(h, _dptr(d_text), n, _stream(stream), _dptr(d_row_ids), cap, C.byref(p),
+                                _dptr(d_result)))
+    return {k: getattr(p, k) for k, _ in sfa_rows_plan._fields_}
+
+
 def sfa_set_compose(h: int, mode: int):
     _check(lib().sfa_set_compose(h, mode))
 
@@ -326,6 +368,12 @@ class SFA:
 
     def set_compose(self, mode: int):
         sfa_set_compose(self.h, mode)
+
+    def set_tuning(self, **knobs):
+        sfa_set_tuning(self.h, **knobs)
+
+    def match_rows(self, d_text, d_row_ids, d_result, stream=None):
+        return sfa_match_rows(self.h, d_text, d_row_ids, d_result, None, stream)
 
     def tune_residency(self, d_sample=None, stream=None):
         sfa_tune_residency(self.h, d_sample, None, stream)

@@ -40,7 +40,6 @@ constexpr uint64_t kDirectPiece = 64;          // bytes per thread in k_scan_dir
 constexpr uint64_t kDirectPieceMax = 512;      // ... and at most (texts < kTmaMin)
 constexpr uint32_t kMaxSlots = (1u << 16) + 2; // partial slots (CTAs + tail)
 constexpr uint64_t kSlice = 64ull << 20;       // sfa_match_host slice
-constexpr uint64_t kBatchSeg = 64ull << 10;    // bytes per batch task
 constexpr uint32_t kCompMaxStates = 4096;      // composition table up to |S|^2 = 16M entries
 constexpr size_t kAuxMax = 16u << 10;          // comp / maps32 copied into smem up to this size
 constexpr uint64_t kDfaMax = 132u << 10;       // FACTORED: the DFA table copies take at most this much smem
@@ -84,10 +83,19 @@ struct sfa_handle {
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
     uint16_t *dfam = nullptr, *dfg = nullptr, *dftab = nullptr, *ddwin = nullptr;  // FACTORED step tables
     uint32_t dwin_bytes = 0, nfam = 0, dwin_R = 0, dwin_X = 0;
-    bool factor_on = [] {  // SFA_FACTOR=0 disables the factored step (A/B measurements, tests)
-        const char* e = getenv("SFA_FACTOR");
-        return !(e && e[0] == '0');
-    }();
+    sfa_tuning_t tuning{};                    // shape knobs (sfa_set_tuning); zero = automatic
+    bool factor_on() const { return tuning.no_factor == 0; }
+    sfa::Tuning ktune() const {
+        sfa::Tuning k;
+        k.tma_k = tuning.tma_k;
+        k.tma_rowb = tuning.tma_rowb;
+        k.tma_ring = tuning.tma_ring;
+        k.tma_promo = tuning.tma_promo;
+        k.hot_rows = tuning.hot_rows;
+        k.row_align = tuning.row_align;
+        k.direct_piece = tuning.direct_piece;
+        return k;
+    }
     uint32_t* dspecT = nullptr;               // Alg. 3 baseline: DFA window table (kernels_spec.cu)
     uint32_t* spec_maps = nullptr;            // Alg. 3: per-CTA maps (spec_cap entries)
     uint32_t* spec_ticket = nullptr;
@@ -102,34 +110,51 @@ struct sfa_handle {
     uint32_t* ticket = nullptr;
     sfa_result* dres = nullptr;       // 2 results (single-text matches and the slice ring)
     sfa_result* hres = nullptr;       // pinned
-    uint32_t* task_off = nullptr;     // batch plan
-    uint32_t* work = nullptr;
-    uint8_t* seg_parts = nullptr;
-    size_t task_cap = 0, seg_cap = 0;
+    sfa::TmaPlan* dplan = nullptr;    // batch: the plan k_batch_plan writes
+    void* gmaps = nullptr;            // batch: 3 tensor maps rewritten on the device
+    uint32_t* berr = nullptr;         // batch: error word (== epoch: bad offsets)
+    uint32_t epoch = 0;
     uint8_t* stage[2] = {nullptr, nullptr};   // sfa_match_host staging
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     cudaEvent_t ev_done = nullptr;    // orders uses of the shared scratch across streams
 
-    ~sfa_handle() {
+    ~sfa_handle() { release_device(); }
+
+    // Frees every device table and scratch buffer (after the device work that
+    // used them); the next device call uploads again.
+    void release_device() {
         if (!uploaded) return;
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         cudaDeviceSynchronize();
-        for (void* p : {(void*)dT, (void*)dcls, (void*)dTrange, (void*)dmaps32, (void*)dmaps16, (void*)dimg0,
-                        (void*)dfinal, (void*)drep_off, (void*)drep, (void*)partials, (void*)ticket, (void*)dres,
-                        (void*)task_off, (void*)work, (void*)seg_parts, (void*)stage[0], (void*)stage[1],
-                        (void*)dcomp, (void*)dpairs, (void*)dTdev, (void*)dfam, (void*)dfg, (void*)dftab, (void*)ddwin, (void*)dperm, (void*)diperm, (void*)drep16, (void*)dspecT, (void*)spec_maps, (void*)spec_ticket, (void*)daux[0],
-                        (void*)daux[1]})
-            if (p) cudaFree(p);
+        for (void** pp : {(void**)&dT, (void**)&dcls, (void**)&dTrange, (void**)&dmaps32, (void**)&dmaps16, (void**)&dimg0,
+                          (void**)&dfinal, (void**)&drep_off, (void**)&drep, (void**)&partials, (void**)&ticket, (void**)&dres,
+                          (void**)&dplan, (void**)&gmaps, (void**)&berr, (void**)&stage[0], (void**)&stage[1],
+                          (void**)&dcomp, (void**)&dpairs, (void**)&dTdev, (void**)&dfam, (void**)&dfg, (void**)&dftab,
+                          (void**)&ddwin, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
+                          (void**)&spec_maps, (void**)&spec_ticket, (void**)&daux[0], (void**)&daux[1]}) {
+            if (*pp) cudaFree(*pp);
+            *pp = nullptr;
+        }
         if (hres) cudaFreeHost(hres);
+        hres = nullptr;
         for (int i = 0; i < 2; ++i) {
             if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
             if (ev_used[i]) cudaEventDestroy(ev_used[i]);
+            ev_copied[i] = ev_used[i] = nullptr;
         }
         if (ev_done) cudaEventDestroy(ev_done);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        ev_done = nullptr;
+        copy_stream = nullptr;
+        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = 0;
+        aux_bytes[0] = aux_bytes[1] = 0;
+        spec_cap = 0;
+        dev_bytes = 0;
+        has_last = false;
+        uploaded = false;
         cudaSetDevice(prev);
     }
 
@@ -143,9 +168,11 @@ struct sfa_handle {
     bool vec() const { return compose_mode() == SFA_COMPOSE_VEC; }
 
     // device tables as seen by a kernel (aux = the composition mode's smem image)
-    sfa::DevTables tables(sfa::Res mode = sfa::Res::Global, int kind = 0) const {
+    // id_only: the batch (SEG) kernels compose SFA ids (TABLE or REPLAY), never vectors
+    sfa::DevTables tables(sfa::Res mode = sfa::Res::Global, int kind = 0, bool id_only = false) const {
         sfa::DevTables t;
-        const int cm = compose_mode();
+        int cm = compose_mode();
+        if (id_only && cm == SFA_COMPOSE_VEC) cm = has_comp() ? SFA_COMPOSE_TABLE : SFA_COMPOSE_REPLAY;
         t.comp = cm == SFA_COMPOSE_TABLE ? dcomp : nullptr;
         t.comp_u8 = A.nS <= 256 ? 1u : 0u;
         t.rep16 = drep16;
@@ -178,7 +205,7 @@ struct sfa_handle {
         t.Tdev = dTdev;
         t.perm = dperm;
         t.iperm = diperm;
-        if (mode == sfa::Res::Hot && dfam && factor_on) {
+        if (mode == sfa::Res::Hot && dfam && factor_on()) {
             t.fact_fam = dfam;
             t.fact_g = dfg;
             t.fact_tab = dftab;
@@ -187,7 +214,7 @@ struct sfa_handle {
             t.dwin_R = dwin_R;
             t.dwin_X = dwin_X;
         }
-        t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin) : 0;
+        t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin, tuning.hot_rows) : 0;
         return t;
     }
 
@@ -331,8 +358,7 @@ struct sfa_handle {
                 dw[static_cast<size_t>(q) * W + j] = static_cast<uint16_t>(A.dfa[static_cast<size_t>(q) * 256 + b]);
             }
         uint32_t R = 32, X = 0;
-        const char* re = getenv("SFA_DFA_COPIES");  // diagnostic: force R
-        const uint32_t Rmax = re ? static_cast<uint32_t>(atoi(re)) : 32u;
+        const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R
         for (; R >= 1; R /= 2) {
             X = sfa::dfa_X(nD, R);
             if (R <= Rmax && static_cast<uint64_t>(X) * W <= (kDfaMax) && X <= 65535u) break;
@@ -356,27 +382,17 @@ struct sfa_handle {
         return SFA_OK;
     }
 
-    // Profile-guided HOT ranking from (a prefix of) a device text, once per
-    // handle unless forced.  Waits for all earlier work of the handle (the
-    // tables are rewritten in place).  Results never depend on the ranking.
-    bool hot_tuned = false;
-    static bool auto_tune() {
-        static const bool on = [] {
-            const char* e = getenv("SFA_HOT_AUTOTUNE");
-            return !(e && e[0] == '0');
-        }();
-        return on;
-    }
+    // Profile-guided HOT ranking from (a prefix of) a device text
+    // (sfa_tune_residency only: a match never blocks on it).  Waits for all
+    // earlier work of the handle (the tables are rewritten in place).  Results
+    // never depend on the ranking.
     int tune_hot(const uint8_t* d_text, size_t n, cudaStream_t stream) {
         const size_t ns = std::min<size_t>(n, 8u << 20);
         std::vector<uint8_t> sample(ns);
         if (has_last) CU(cudaStreamSynchronize(last_stream));
         CU(cudaMemcpyAsync(sample.data(), d_text, ns, cudaMemcpyDeviceToHost, stream));
         CU(cudaStreamSynchronize(stream));
-        int rc = upload_hot(sample.data(), ns);
-        if (rc) return rc;
-        hot_tuned = true;
-        return SFA_OK;
+        return upload_hot(sample.data(), ns);
     }
 
     // Lazy upload: sfa_compile works without a GPU (host tests); the first
@@ -401,8 +417,7 @@ struct sfa_handle {
         CU(upload(&dT, T16.data(), T16.size()));
         {  // PRIVATE: R lane-group copies, R the largest of 32, 16, 8 whose table
            // leaves room for a 3-deep ring of 32-byte stages (else <= 200 KB)
-            const char* re = getenv("SFA_PRIVATE_COPIES");  // diagnostic: cap R
-            const uint32_t Rcap = re ? static_cast<uint32_t>(atoi(re)) : 32u;
+            const uint32_t Rcap = tuning.private_copies ? tuning.private_copies : 32u;  // tuning: cap R
             uint32_t R = 0;
             for (int pass = 0; pass < 2 && !R; ++pass)
                 for (uint32_t r = 32; r >= 8; r /= 2) {
@@ -502,22 +517,24 @@ struct sfa_handle {
         CU(cudaMalloc(&ticket, sizeof(uint32_t)));
         CU(cudaMemset(ticket, 0, sizeof(uint32_t)));
         CU(cudaMalloc(&dres, 2 * sizeof(sfa_result)));
-        CU(cudaMalloc(&work, sizeof(uint32_t)));
+        CU(cudaMalloc(&dplan, sizeof(sfa::TmaPlan)));
+        CU(cudaMalloc(&gmaps, 512));
+        CU(cudaMalloc(&berr, 16));
+        CU(cudaMemset(berr, 0, 16));
         CU(cudaMallocHost(&hres, 2 * sizeof(sfa_result)));
         CU(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
         return SFA_OK;
     }
 
     // does `mode` fit for this launch kind?
-    bool fits(sfa::Res mode, int kind /*0 tma, 1 direct, 2 batch*/) const {
+    bool fits(sfa::Res mode, int kind /*0 tma, 1 direct*/) const {
         const sfa::DevTables t = tables(mode, kind);
         if (mode == sfa::Res::Hot && t.hotH == 0) return false;
         if (kind == 0) {
             sfa::TmaConfig c;
-            return sfa::tma_choose(mode, t, smem_optin, &c);
+            return sfa::tma_choose(mode, t, smem_optin, ktune(), &c);
         }
-        const size_t need = kind == 1 ? sfa::direct_smem_bytes(mode, t) : sfa::table_smem_bytes(mode, t);
-        return need <= smem_optin;
+        return sfa::direct_smem_bytes(mode, t) <= smem_optin;
     }
     int resolve(int kind, sfa::Res* out) const {
         if (forced != SFA_RES_AUTO) {
@@ -529,7 +546,7 @@ struct sfa_handle {
         // TMA scan: a factorable automaton whose DFA window gets more lane copies
         // than the PRIVATE SFA table (fewer bank conflicts per lookup) runs
         // HOT + FACTORED (cfg4: R = 32 DFA copies against R = 16 SFA copies).
-        if (kind == 0 && dfam && factor_on && dwin_R > priv_R && fits(sfa::Res::Hot, kind)) {
+        if (kind == 0 && dfam && factor_on() && dwin_R > priv_R && fits(sfa::Res::Hot, kind)) {
             *out = sfa::Res::Hot;
             return SFA_OK;
         }
@@ -549,17 +566,28 @@ struct sfa_handle {
         return s;
     }
 
-    // One text on the device -> result (device), stream-ordered.
+    // The TMA scan's launch shape and plan for n bytes at d_text.
+    int tma_plan(sfa::Res mode, const sfa::DevTables& t, const uint8_t* d_text, uint64_t n, sfa::TmaConfig* cfg,
+                 sfa::TmaPlan* plan) const {
+        if (!sfa::tma_choose(mode, t, smem_optin, ktune(), cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
+        sfa::make_plan(reinterpret_cast<uintptr_t>(d_text), n, static_cast<uint32_t>(sm_count), cfg->rows_per_cta,
+                       cfg->nb, static_cast<uint32_t>(cfg->rowb), tuning.row_align, plan);
+        if (plan->nchunks == 0 || plan->ctas == 0 || plan->ctas > kMaxSlots - 2)
+            return fail(SFA_ERR_INVALID_ARG, "text too short for the TMA scan");
+        return SFA_OK;
+    }
+
+    // One text on the device -> result (device), stream-ordered.  force_tma:
+    // the TMA scan even below kTmaMin (sfa_match_rows); row_ids / plan_out:
+    // its per-row SFA ids and geometry.
     int launch_one(const uint8_t* d_text, uint64_t n, cudaStream_t stream, const uint32_t* q_in, sfa_result* d_result,
-                   uint64_t force_pieces = 0, uint32_t* piece_ids = nullptr, uint32_t* map_out = nullptr) {
-        const bool direct = force_pieces > 0 || n < kTmaMin;
+                   uint64_t force_pieces = 0, uint32_t* piece_ids = nullptr, uint32_t* map_out = nullptr,
+                   bool force_tma = false, uint32_t* row_ids = nullptr, size_t row_cap = 0,
+                   sfa::TmaPlan* plan_out = nullptr) {
+        const bool direct = !force_tma && (force_pieces > 0 || n < kTmaMin);
         sfa::Res mode;
         int rc = resolve(direct ? 1 : 0, &mode);
         if (rc) return rc;
-        if (mode == sfa::Res::Hot && !hot_tuned && auto_tune()) {
-            rc = tune_hot(d_text, n, stream);
-            if (rc) return rc;
-        }
         cudaError_t e;
         if (direct) {
             sfa::DirectArgs a;
@@ -569,12 +597,9 @@ struct sfa_handle {
             // Bytes per thread: about 8192 threads (32 CTAs) until pieces reach
             // 512 B.  Every CTA builds its own smem table, so more, shorter pieces
             // cost more than their shorter chains save (3 MiB, cfg2: 12.3 us at
-            // 64-B pieces, 6.5 us at 384-512).  SFA_DIRECT_PIECE (diagnostic) forces one.
-            static const uint64_t forced_piece = [] {
-                const char* e = getenv("SFA_DIRECT_PIECE");
-                const long v = e ? atol(e) : 0;
-                return v >= 16 && v <= 4096 ? static_cast<uint64_t>(v) : 0u;
-            }();
+            // 64-B pieces, 6.5 us at 384-512).  Tuning direct_piece forces one.
+            const uint64_t forced_piece =
+                tuning.direct_piece >= 16 && tuning.direct_piece <= 4096 ? tuning.direct_piece : 0u;
             const uint64_t piece =
                 forced_piece ? forced_piece : std::min<uint64_t>(kDirectPieceMax, std::max<uint64_t>(kDirectPiece, n / 8192));
             a.npieces = force_pieces ? force_pieces : std::max<uint64_t>(1, (n + piece - 1) / piece);
@@ -587,116 +612,80 @@ struct sfa_handle {
             if (ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "too many chunks");
             e = sfa::launch_scan_direct(mode, vec(), a, stream);
         } else {
-            sfa::ScanArgs a;
+            sfa::ScanArgs a{};
             a.t = tables(mode, 0);
             a.text = d_text;
             a.n = n;
             a.sc = scratch();
             a.q_in = q_in;
             a.result = d_result;
-            a.stamps = nullptr;
             a.map_out = map_out;
-            a.seg_m = 0;
-            a.results = nullptr;
-            static const uint32_t diag = getenv("SFA_DIAG_FLAGS") ? static_cast<uint32_t>(atoi(getenv("SFA_DIAG_FLAGS"))) : 0u;
-            a.diag = diag;
+            a.row_ids = row_ids;
             sfa::TmaConfig cfg;
-            if (!sfa::tma_choose(mode, a.t, smem_optin, &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
-            // box heights (rows_per_cta / nb) are multiples of 8 rows, so every TMA
-            // destination is aligned to its swizzle atom (8 rows x ROWB bytes)
-            const uint64_t R = cfg.rows_per_cta, NB = cfg.nb * 8, G = static_cast<uint64_t>(sm_count);
-            uint64_t head = (256 - (reinterpret_cast<uintptr_t>(d_text) & 255)) & 255;
-            head = std::min<uint64_t>(head, n);
-            const uint64_t body = n - head;
-            // rows of L bytes (a multiple of 256), at most G*R of them, spread
-            // evenly over G CTAs in multiples of NB (TMA box count x alignment)
-            // Row alignment: the rows fill at most G*R chunks; a coarser L leaves
-            // compute rows idle (256 MiB at 256-B rows uses 89% of them), a finer
-            // one costs DRAM efficiency (64-B rows: -2.3% measured at 1 GiB; 128
-            // costs nothing measurable).  Take the best rows used x alignment cost.
-            // SFA_ROW_ALIGN (diagnostic) forces one.
-            static const uint64_t forced_align = [] {
-                const char* e = getenv("SFA_ROW_ALIGN");
-                const uint64_t v = e ? static_cast<uint64_t>(atoi(e)) : 0u;
-                return (v >= 16 && v <= 256 && !(v & (v - 1))) ? v : 0u;
-            }();
-            uint64_t L = 0;
-            double best = -1;
-            for (uint64_t a0 : {256u, 128u, 64u}) {
-                if (forced_align && a0 != 256u) break;
-                const uint64_t al = std::max<uint64_t>(forced_align ? forced_align : a0, static_cast<uint64_t>(cfg.rowb));
-                uint64_t Lc = al * ((body + al * G * R - 1) / (al * G * R));
-                if (Lc < 256) Lc = 256;
-                const double used = static_cast<double>(body / Lc) / static_cast<double>(G * R);
-                const double score = used * (al >= 128 ? 1.0 : 0.977);
-                if (score > best + 1e-9) {
-                    best = score;
-                    L = Lc;
-                }
-            }
-            const uint64_t rows = body / L;
-            const uint64_t rc = NB * ((rows + G * NB - 1) / (G * NB));
-            a.plan.head = head;
-            a.plan.L = L;
-            a.plan.nchunks = static_cast<uint32_t>(rows);
-            a.plan.rows_per_cta = static_cast<uint32_t>(rc);
-            a.plan.ctas = rc ? static_cast<uint32_t>((rows + rc - 1) / rc) : 0;
-            a.plan.tail_start = head + rows * L;
-            if (rows == 0 || a.plan.ctas > a.sc.max_ctas) return fail(SFA_ERR_INVALID_ARG, "bad scan plan");
-            static const bool dbg = getenv("SFA_DEBUG_STAMPS") != nullptr;
-            if (dbg) CU(cudaMallocAsync(&a.stamps, 8 * sizeof(uint64_t) * a.plan.ctas, stream));
+            rc = tma_plan(mode, a.t, d_text, n, &cfg, &a.plan);
+            if (rc) return rc;
+            if (row_ids && a.plan.nchunks > row_cap) return fail(SFA_ERR_CAPACITY, "row_cap is smaller than the row count");
+            if (plan_out) *plan_out = a.plan;
             e = sfa::launch_scan_tma(mode, vec(), a, cfg, stream);
-            if (dbg && e == cudaSuccess) {  // diagnostic: per-CTA phase times (ns) to stderr
-                std::vector<uint64_t> st(8ull * a.plan.ctas);
-                CU(cudaMemcpyAsync(st.data(), a.stamps, st.size() * 8, cudaMemcpyDeviceToHost, stream));
-                CU(cudaStreamSynchronize(stream));
-                CU(cudaFree(a.stamps));
-                uint64_t t0 = UINT64_MAX, tend = 0;
-                double ph[4] = {0, 0, 0, 0};
-                for (uint32_t b = 0; b < a.plan.ctas; ++b) t0 = std::min(t0, st[8 * b]);
-                for (uint32_t b = 0; b < a.plan.ctas; ++b) {
-                    for (int k = 0; k < 4; ++k) ph[k] += double(st[8 * b + k + 1] - st[8 * b + k]) / a.plan.ctas;
-                    tend = std::max(tend, st[8 * b + 4]);
-                }
-                double f5 = 0, f6 = 0;
-                for (uint32_t b = 0; b < a.plan.ctas; ++b) {
-                    f5 += double(st[8 * b + 5]) / a.plan.ctas;
-                    f6 += double(st[8 * b + 6]) / a.plan.ctas;
-                }
-                fprintf(stderr, "stamps: fill(thread0)=%.0f cyc of which staging wait=%.0f cyc\n", f5, f6);
-                if (a.diag & 2) {
-                    double cold = 0, warm = 0;
-                    for (uint32_t b = 0; b < a.plan.ctas; ++b) {
-                        cold += double(st[8 * b + 5] >> 32) / a.plan.ctas;
-                        warm += double(st[8 * b + 5] & 0xffffffffull) / a.plan.ctas;
-                    }
-                    fprintf(stderr, "stamps: first build %.0f cyc, second (warm) build %.0f cyc\n", cold, warm);
-                }
-                {
-                    uint64_t e0 = UINT64_MAX, e1 = 0, m0 = UINT64_MAX, m1 = 0;
-                    for (uint32_t b = 0; b < a.plan.ctas; ++b) {
-                        e0 = std::min(e0, st[8 * b + 2]);
-                        e1 = std::max(e1, st[8 * b + 2]);
-                        m0 = std::min(m0, st[8 * b + 1]);
-                        m1 = std::max(m1, st[8 * b + 1]);
-                    }
-                    fprintf(stderr, "stamps: scan-start spread %.2fus, scan-end spread %.2fus\n", (m1 - m0) / 1e3,
-                            (e1 - e0) / 1e3);
-                    std::vector<std::pair<double, uint32_t>> dur;
-                    for (uint32_t b = 0; b < a.plan.ctas; ++b) dur.push_back({(st[8 * b + 2] - st[8 * b + 1]) / 1e3, b});
-                    std::sort(dur.begin(), dur.end());
-                    fprintf(stderr, "stamps: scan us min %.1f (cta %u) median %.1f max %.1f (cta %u) 2nd %.1f (cta %u)\n",
-                            dur.front().first, dur.front().second, dur[dur.size() / 2].first, dur.back().first,
-                            dur.back().second, dur[dur.size() - 2].first, dur[dur.size() - 2].second);
-                }
-                uint64_t smax = 0;
-                for (uint32_t b = 0; b < a.plan.ctas; ++b) smax = std::max(smax, st[8 * b] - t0);
-                fprintf(stderr, "stamps: ctas=%u start-spread=%.2fus tables=%.2fus scan=%.2fus blockfold=%.2fus epi=%.2fus total=%.2fus L=%llu rc=%u\n",
-                        a.plan.ctas, smax / 1e3, ph[0] / 1e3, ph[1] / 1e3, ph[2] / 1e3, ph[3] / 1e3, (tend - t0) / 1e3,
-                        (unsigned long long)a.plan.L, a.plan.rows_per_cta);
-            }
         }
         if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+        return SFA_OK;
+    }
+
+    int launch_seg_empty(sfa_result* d_results, uint64_t count, cudaStream_t stream) {
+        cudaError_t e = sfa::launch_fill_results(d_results, count, 0, A.dfa_final[0], stream);
+        return e == cudaSuccess ? SFA_OK : cuda_fail(e, "fill launch");
+    }
+
+    // A batch through the SEG scan: texts back to back at `base`; host plan
+    // for equal texts of `len` bytes (off == nullptr), else the device plan.
+    int launch_seg(const uint8_t* base, const uint64_t* d_off, uint64_t len, uint64_t count, sfa_result* d_results,
+                   cudaStream_t stream) {
+        sfa::Res mode;
+        int rc = resolve(0, &mode);
+        if (rc) return rc;
+        sfa::ScanArgs a{};
+        a.t = tables(mode, 0, true);
+        a.text = base;
+        a.sc = scratch();
+        a.off = d_off;
+        a.count = count;
+        a.results = d_results;
+        sfa::TmaConfig cfg;
+        if (!sfa::tma_choose(mode, a.t, smem_optin, ktune(), &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
+        const uint32_t G = static_cast<uint32_t>(sm_count);
+        cudaError_t e;
+        if (d_off) {
+            sfa::BatchPlanArgs p;
+            p.texts = base;
+            p.off = d_off;
+            p.count = count;
+            p.G = G;
+            p.R = cfg.rows_per_cta;
+            p.NB = cfg.nb;
+            p.rowb = static_cast<uint32_t>(cfg.rowb);
+            p.row_align = tuning.row_align;
+            p.dplan = dplan;
+            p.gmaps = gmaps;
+            p.err = berr;
+            p.epoch = ++epoch ? epoch : ++epoch;  // never 0 (the error word starts at 0)
+            p.results = d_results;
+            p.eps_accept = A.dfa_final[0];
+            e = sfa::launch_batch_plan(p, cfg, sm_count, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "batch plan launch");
+            a.dplan = dplan;
+            a.gmaps = gmaps;
+            a.err = berr;
+            a.epoch = p.epoch;
+            e = sfa::launch_scan_seg(mode, a, cfg, G, stream);
+        } else {
+            a.n = len * count;
+            sfa::make_plan(reinterpret_cast<uintptr_t>(base), a.n, G, cfg.rows_per_cta, cfg.nb,
+                           static_cast<uint32_t>(cfg.rowb), tuning.row_align, &a.plan);
+            a.plan.len = len;
+            e = sfa::launch_scan_seg(mode, a, cfg, G, stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "batch scan launch");
         return SFA_OK;
     }
 
@@ -840,9 +829,7 @@ int sfa_tune_residency(sfa_handle* h, const uint8_t* d_sample, size_t n, sfa_str
     if (rc) return rc;
     if (n == 0) {  // back to the static ranking
         if (h->has_last) CU(cudaStreamSynchronize(h->last_stream));
-        rc = h->upload_hot(nullptr, 0);
-        if (!rc) h->hot_tuned = true;
-        return rc;
+        return h->upload_hot(nullptr, 0);
     }
     return h->tune_hot(d_sample, n, reinterpret_cast<cudaStream_t>(stream));
 }
@@ -854,6 +841,26 @@ int sfa_set_compose(sfa_handle* h, int mode) {
     if (mode == SFA_COMPOSE_TABLE && !h->has_comp()) return fail(SFA_ERR_CAPACITY, "composition table needs |S| <= 4096");
     std::lock_guard<std::mutex> lk(h->mu);
     h->compose = mode;
+    return SFA_OK;
+}
+
+int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* tu) {
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    sfa_tuning_t t{};
+    if (tu) t = *tu;
+    if (t.tma_k < 0 || t.tma_k > 2 || (t.tma_rowb && t.tma_rowb != 16 && t.tma_rowb != 32 && t.tma_rowb != 64) ||
+        (t.tma_rowb && !t.tma_k) || t.tma_ring < 0 || t.tma_ring > 8 ||
+        (t.tma_promo != -1 && t.tma_promo != 0 && t.tma_promo != 64 && t.tma_promo != 128 && t.tma_promo != 256) ||
+        (t.row_align && t.row_align != 64 && t.row_align != 128 && t.row_align != 256) ||
+        (t.dfa_copies & (t.dfa_copies - 1)) || t.dfa_copies > 32 ||
+        (t.private_copies & (t.private_copies - 1)) || t.private_copies > 32 ||
+        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)))
+        return fail(SFA_ERR_INVALID_ARG, "bad tuning value");
+    if (!tu) t.tma_promo = -1;
+    std::lock_guard<std::mutex> lk(h->mu);
+    // the table layouts depend on the copy caps and the factoring switch: rebuild lazily
+    h->release_device();
+    h->tuning = t;
     return SFA_OK;
 }
 
@@ -883,11 +890,9 @@ int sfa_match_async(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_s
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int rc = h->begin(s);
     if (rc) return rc;
-    if (n == 0) {
-        sfa_result r{0, h->A.dfa_final[0]};
-        h->hres[1] = r;
-        CU(cudaMemcpyAsync(d_result, &h->hres[1], sizeof(r), cudaMemcpyHostToDevice, s));
-        CU(cudaStreamSynchronize(s));  // hres[1] is reused
+    if (n == 0) {  // (q0, [eps in L]) written by a one-thread kernel: no host round trip
+        cudaError_t e = sfa::launch_fill_result(d_result, 0, h->A.dfa_final[0], nullptr, 0, s);
+        if (e != cudaSuccess) return cuda_fail(e, "fill launch");
         return h->end(s);
     }
     rc = h->launch_one(d_text, n, s, nullptr, d_result);
@@ -956,6 +961,29 @@ int sfa_match_chunked(const sfa_handle* hc, const uint8_t* d_text, size_t n, uin
     return SFA_OK;
 }
 
+int sfa_match_rows(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_stream_t stream, uint32_t* d_row_ids,
+                   size_t row_cap, sfa_rows_plan* plan, sfa_result* d_result) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !d_text || !d_row_ids || !plan || !d_result) return fail(SFA_ERR_INVALID_ARG, "NULL argument");
+    if (n < (64u << 10)) return fail(SFA_ERR_INVALID_ARG, "sfa_match_rows needs n >= 64 KiB");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    sfa::TmaPlan p;
+    rc = h->launch_one(d_text, n, s, nullptr, d_result, 0, nullptr, nullptr, true, d_row_ids, row_cap, &p);
+    if (rc) return rc;
+    plan->head = p.head;
+    plan->row_len = p.L;
+    plan->rows = p.nchunks;
+    plan->tail_start = p.tail_start;
+    plan->ctas = p.ctas;
+    plan->rows_hi = p.rc_hi;
+    plan->rows_lo = p.rc_lo;
+    plan->ctas_hi = p.m;
+    return h->end(s);
+}
+
 int sfa_match_map(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_stream_t stream, uint32_t* d_map) {
     sfa_handle* h = const_cast<sfa_handle*>(hc);
     if (!h || !d_map) return fail(SFA_ERR_INVALID_ARG, "NULL handle or map");
@@ -966,10 +994,8 @@ int sfa_match_map(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_str
     if (rc) return rc;
     if (!h->vec() && !h->dmaps16) return fail(SFA_ERR_CAPACITY, "mapping table too large for sfa_match_map");
     if (n == 0) {  // f_eps = identity
-        std::vector<uint32_t> id(h->A.nD);
-        for (uint32_t q = 0; q < h->A.nD; ++q) id[q] = q;
-        CU(cudaMemcpyAsync(d_map, id.data(), id.size() * 4, cudaMemcpyHostToDevice, s));
-        CU(cudaStreamSynchronize(s));
+        cudaError_t e = sfa::launch_fill_result(nullptr, 0, 0, d_map, h->A.nD, s);
+        if (e != cudaSuccess) return cuda_fail(e, "fill launch");
         return h->end(s);
     }
     rc = h->launch_one(d_text, n, s, nullptr, nullptr, 0, nullptr, d_map);
@@ -996,137 +1022,38 @@ int sfa_match_batch(const sfa_handle* hc, const uint8_t* d_texts, const uint64_t
     sfa_handle* h = const_cast<sfa_handle*>(hc);
     if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
     if (count == 0) return SFA_OK;
-    if (!d_offsets || !d_results) return fail(SFA_ERR_INVALID_ARG, "NULL offsets or results");
-    if (count > (1ull << 30)) return fail(SFA_ERR_INVALID_ARG, "count too large");
+    if (!d_offsets || !d_results || !d_texts) return fail(SFA_ERR_INVALID_ARG, "NULL texts, offsets or results");
+    if (count > (1ull << 31)) return fail(SFA_ERR_INVALID_ARG, "count too large");
     std::lock_guard<std::mutex> lk(h->mu);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int rc = h->begin(s);
     if (rc) return rc;
-    sfa::Res mode;
-    rc = h->resolve(2, &mode);
+    rc = h->launch_seg(d_texts, d_offsets, 0, count, d_results, s);
     if (rc) return rc;
-    if (h->task_cap < count + 1) {
-        if (h->task_off) CU(cudaFree(h->task_off));
-        h->task_off = nullptr;
-        h->task_cap = 0;
-        CU(cudaMalloc(&h->task_off, (count + 1) * sizeof(uint32_t)));
-        h->task_cap = count + 1;
-    }
-    // segments: at most (total bytes / seg) + count tasks; size the parts buffer
-    // lazily for the worst case of this count with one task per text plus the
-    // multi-segment texts (bounded by 2^32 tasks).
-    uint64_t total_bytes = 0;
-    {
-        uint64_t ends[2] = {0, 0};
-        CU(cudaMemcpyAsync(&ends[0], d_offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(&ends[1], d_offsets + count, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        total_bytes = ends[1] > ends[0] ? ends[1] - ends[0] : 0;
-        if (!d_texts && total_bytes > 0) return fail(SFA_ERR_INVALID_ARG, "d_texts is NULL");
-    }
-    const uint64_t max_tasks = count + total_bytes / kBatchSeg + 1;
-    if (max_tasks > 0xffffffffull) return fail(SFA_ERR_INVALID_ARG, "batch too large");
-    const size_t need = max_tasks * (h->vec() ? 32 : 4);
-    if (h->seg_cap < need) {
-        if (h->seg_parts) CU(cudaFree(h->seg_parts));
-        h->seg_parts = nullptr;
-        h->seg_cap = 0;
-        CU(cudaMalloc(&h->seg_parts, need));
-        h->seg_cap = need;
-    }
-    if (mode == sfa::Res::Hot && !h->hot_tuned && h->auto_tune() && total_bytes > 0) {
-        uint64_t first = 0;
-        CU(cudaMemcpy(&first, d_offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost));
-        rc = h->tune_hot(d_texts + first, total_bytes, s);
-        if (rc) return rc;
-    }
-    sfa::BatchArgs a;
-    a.t = h->tables(mode, 2);
-    a.texts = d_texts;
-    a.off = d_offsets;
-    a.count = count;
-    a.seg = kBatchSeg;
-    a.task_off = h->task_off;
-    a.work = h->work;
-    a.seg_parts = h->seg_parts;
-    a.results = d_results;
-    cudaError_t e = sfa::launch_batch(mode, h->vec(), a, h->sm_count, s);
-    if (e != cudaSuccess) return cuda_fail(e, "batch launch");
     return h->end(s);
 }
 
-// A batch of `count` back-to-back texts of `len` bytes each through the TMA scan:
-// the texts are a 2-D tensor [count * m rows x len/m bytes], m rows per text
-// (m | 32, so one text's rows are consecutive lanes of one warp) and the
-// kernel folds each text's m row states with a segmented shuffle tree.
+// `count` back-to-back texts of `len` bytes: the same SEG scan with the
+// boundaries at multiples of len and the plan made on the host.
 int sfa_match_batch_uniform(const sfa_handle* hc, const uint8_t* d_texts, size_t len, size_t count, sfa_stream_t stream,
                             sfa_result* d_results) {
     sfa_handle* h = const_cast<sfa_handle*>(hc);
     if (!h || (count && !d_results)) return fail(SFA_ERR_INVALID_ARG, "NULL handle or results");
     if (count == 0) return SFA_OK;
     if (!d_texts && len > 0) return fail(SFA_ERR_INVALID_ARG, "d_texts is NULL");
+    if (count > (1ull << 31) || (len && count > UINT64_MAX / len)) return fail(SFA_ERR_INVALID_ARG, "count too large");
+    std::lock_guard<std::mutex> lk(h->mu);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    {
-        std::lock_guard<std::mutex> lk(h->mu);
-        int rc = h->begin(s);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    if (len == 0) {  // every text empty: (q0, [eps in L]) each
+        rc = h->launch_seg_empty(d_results, count, s);
         if (rc) return rc;
-        sfa::Res mode;
-        rc = h->resolve(0, &mode);
-        if (rc) return rc;
-        sfa::TmaConfig cfg;
-        const sfa::DevTables t0 = h->tables(mode, 0);
-        const bool aligned = (reinterpret_cast<uintptr_t>(d_texts) & 15) == 0;
-        if (!h->vec() && aligned && len >= 512 && sfa::tma_choose(mode, t0, h->smem_optin, &cfg)) {
-            if (mode == sfa::Res::Hot && !h->hot_tuned && h->auto_tune()) {
-                rc = h->tune_hot(d_texts, len * count, s);
-                if (rc) return rc;
-            }
-            const uint64_t G = static_cast<uint64_t>(h->sm_count), R = cfg.rows_per_cta;
-            // largest m <= 32 (power of 2) with len/m a multiple of the stage width and of 256
-            uint32_t m = 32;
-            while (m > 1 && (len % (static_cast<uint64_t>(m) * 256) != 0 || count * m > G * R)) m /= 2;
-            const uint64_t L = len / m;
-            if (len % 256 == 0 && L % static_cast<uint64_t>(cfg.rowb) == 0) {
-                const uint64_t per_launch = std::max<uint64_t>(1, (G * R) / m);  // texts per launch
-                for (uint64_t c0 = 0; c0 < count; c0 += per_launch) {
-                    const uint64_t cnt = std::min<uint64_t>(per_launch, count - c0);
-                    sfa::ScanArgs a{};
-                    a.t = h->tables(mode, 0);
-                    a.text = d_texts + c0 * len;
-                    a.n = cnt * len;
-                    a.sc = h->scratch();
-                    a.q_in = nullptr;
-                    a.result = nullptr;
-                    a.stamps = nullptr;
-                    a.map_out = nullptr;
-                    a.diag = 0;
-                    a.seg_m = m;
-                    a.results = d_results + c0;
-                    const uint64_t rows = cnt * m, NB = cfg.nb * 8;
-                    const uint64_t rc_ = NB * ((rows + G * NB - 1) / (G * NB));
-                    a.plan.head = 0;
-                    a.plan.L = L;
-                    a.plan.nchunks = static_cast<uint32_t>(rows);
-                    a.plan.rows_per_cta = static_cast<uint32_t>(rc_);
-                    a.plan.ctas = static_cast<uint32_t>((rows + rc_ - 1) / rc_);
-                    a.plan.tail_start = a.n;
-                    cudaError_t e = sfa::launch_scan_tma(mode, false, a, cfg, s);
-                    if (e != cudaSuccess) return cuda_fail(e, "uniform batch launch");
-                }
-                return h->end(s);
-            }
-        }
+        return h->end(s);
     }
-    // general path: explicit offsets
-    std::vector<uint64_t> off(count + 1);
-    for (size_t i = 0; i <= count; ++i) off[i] = i * len;
-    uint64_t* d_off = nullptr;
-    CU(cudaMallocAsync(&d_off, off.size() * 8, s));
-    CU(cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s));
-    int rc = sfa_match_batch(hc, d_texts, d_off, count, stream, d_results);
-    CU(cudaFreeAsync(d_off, s));
-    CU(cudaStreamSynchronize(s));  // `off` is host memory of this frame
-    return rc;
+    rc = h->launch_seg(d_texts, nullptr, len, count, d_results, s);
+    if (rc) return rc;
+    return h->end(s);
 }
 
 int sfa_match_speculative(const sfa_handle* hc, const uint8_t* d_text, size_t n, uint64_t nchunks, sfa_stream_t stream,
@@ -1134,19 +1061,15 @@ int sfa_match_speculative(const sfa_handle* hc, const uint8_t* d_text, size_t n,
     sfa_handle* h = const_cast<sfa_handle*>(hc);
     if (!h || !d_result) return fail(SFA_ERR_INVALID_ARG, "NULL handle or result");
     if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    if (d_chunk_maps && nchunks == 0)  // the caller must know how many rows it receives
+        return fail(SFA_ERR_INVALID_ARG, "d_chunk_maps needs an explicit nchunks");
     std::lock_guard<std::mutex> lk(h->mu);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int rc = h->begin(s);
     if (rc) return rc;
     if (n == 0) {  // no chunk: T = identity, q_final = q0
-        if (d_chunk_maps) {
-            std::vector<uint32_t> id(h->A.nD);
-            for (uint32_t q = 0; q < h->A.nD; ++q) id[q] = q;
-            CU(cudaMemcpyAsync(d_chunk_maps, id.data(), id.size() * 4, cudaMemcpyHostToDevice, s));
-        }
-        h->hres[1] = sfa_result{0, h->A.dfa_final[0]};
-        CU(cudaMemcpyAsync(d_result, &h->hres[1], sizeof(sfa_result), cudaMemcpyHostToDevice, s));
-        CU(cudaStreamSynchronize(s));  // hres[1] and id are reused / freed
+        cudaError_t e = sfa::launch_fill_result(d_result, 0, h->A.dfa_final[0], d_chunk_maps, h->A.nD, s);
+        if (e != cudaSuccess) return cuda_fail(e, "fill launch");
         return h->end(s);
     }
     rc = h->upload_spec();

@@ -48,6 +48,11 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -135,6 +140,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int x, int y) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tmap), "r"(x), "r"(y) : "memory");
+}
+// A tensor map another kernel rewrote in global memory (tensormap.replace):
+// order the generic-proxy writes before this kernel's TMA uses of it.
+__device__ __forceinline__ void tmap_acquire(const void* tmap) {
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmap) : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
@@ -363,11 +373,13 @@ struct StepHot {
     // branch, no reconvergence; only the lanes whose state is cold touch L2.
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
         const uint32_t idx = st * W + window_col(byte, neg_lo, wmax);
-        uint32_t r;
+        // "+r" from st: ptxas cannot tell that the two predicated loads cover
+        // every case, so an output-only register would stay live (and spill)
+        uint32_t r = st;
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t"
-            "@p ld.shared.u16 %0, [%3];\n\t@!p ld.global.nc.u16 %0, [%4];\n\t}"
-            : "=r"(r) : "r"(st), "r"(H), "r"(sbase + 2 * idx), "l"(Tdev + idx) : "memory");
+            "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %0, %1;\n\t"
+            "@p ld.shared.u16 %0, [%2];\n\t@!p ld.global.nc.u16 %0, [%3];\n\t}"
+            : "+r"(r) : "r"(H), "r"(sbase + 2 * idx), "l"(Tdev + idx) : "memory");
         return r;
     }
     __device__ __forceinline__ uint32_t id(uint32_t st, uint32_t) const { return __ldg(iperm + st); }

@@ -17,17 +17,23 @@ namespace sfa {
 
 struct ScanArgs {
     DevTables t;
-    const uint8_t* text;  // base of the text (device)
+    const uint8_t* text;  // base of the scanned range (device): one text, or a batch's texts back to back
     uint64_t n;
-    TmaPlan plan;
+    TmaPlan plan;         // the host's plan (dplan == nullptr)
+    const TmaPlan* dplan; // batch: the plan k_batch_plan wrote (read after griddepcontrol.wait)
+    const void* gmaps;    // batch: its three tensor maps in global memory (load, last_hi, last_lo), else nullptr
     Scratch sc;
     const uint32_t* q_in;
     sfa_result* result;
-    uint64_t* stamps;     // diagnostic (SFA_DEBUG_STAMPS): 8 %globaltimer stamps per CTA, else NULL
-    uint32_t diag;        // diagnostic (SFA_DIAG_FLAGS, results invalid): 1 = skip the table build
     uint32_t* map_out;    // optional: f_fin(q) for every DFA state q (nD u32, device)
-    uint32_t seg_m;       // 0: one text.  > 0: a batch of equal texts, each seg_m consecutive rows
-    sfa_result* results;  // seg_m > 0: per-text results
+    uint32_t* row_ids;    // optional: canonical SFA id of every row (plan.nchunks u32, device)
+    // batch (SEG kernels): text i = [off[i] - off[0], off[i+1] - off[0]) of the range, or
+    // [i * plan.len, (i+1) * plan.len) when off == nullptr
+    const uint64_t* off;
+    uint64_t count;
+    sfa_result* results;
+    const uint32_t* err;  // batch error word: == epoch when k_batch_plan found bad offsets
+    uint32_t epoch;
 };
 
 struct DirectArgs {
@@ -42,45 +48,55 @@ struct DirectArgs {
     uint32_t* map_out;    // optional: f_fin(q) for every DFA state q (nD u32, device)
 };
 
-struct BatchArgs {
-    DevTables t;
+// k_batch_plan: validates the offsets, answers the empty texts and plans the
+// batch's TMA scan on the device (no host round trip).
+struct BatchPlanArgs {
     const uint8_t* texts;
-    const uint64_t* off;   // count + 1
+    const uint64_t* off;
     uint64_t count;
-    uint64_t seg;          // max bytes per task
-    uint32_t* task_off;    // count + 1 (scratch)
-    uint32_t* work;        // work-stealing counter (scratch)
-    uint8_t* seg_parts;    // per task: 32 B (vector) or 4 B (id)
-    sfa_result* results;   // count
+    uint32_t G, R, NB, rowb, row_align;
+    TmaPlan* dplan;
+    void* gmaps;           // 3 x 128-B tensor maps, rewritten from the template (tensormap.replace)
+    uint32_t* err;
+    uint32_t epoch;
+    sfa_result* results;
+    uint32_t eps_accept;   // [eps in L]: the result of an empty text is (q0 = 0, eps_accept)
 };
 
 // Shape of a k_scan_tma launch: K chunks per compute thread, ROWB bytes of
-// every row per pipeline stage, nring stages in the smem ring, L2 prefetch
-// distance in 256-byte lines.
+// every row per pipeline stage, nring stages in the smem ring.
 struct TmaConfig {
     int K = 1, rowb = 16;
     uint32_t nring = 2, rows_per_cta = 0;
-    int pf_lines = 1;     // L2 prefetch distance in 256-B lines (-1: no prefetch)
-    int promo = 256;      // L2 promotion of the TMA loads (bytes; 0 = none)
+    int promo = 0;        // L2 promotion of the TMA loads (bytes; 0 = none)
     bool staged = false;  // bulk-copy the step's compact table into smem before building it
-    uint32_t nb = 4;   // TMA boxes per stage: rows_per_cta of a launch must be a multiple
+    uint32_t nb = 4;      // TMA boxes per stage
 };
 
-uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin);
+// Shape knobs (sfa_set_tuning); 0 = automatic.  None of them changes a result.
+struct Tuning {
+    int tma_k = 0, tma_rowb = 0, tma_ring = 0, tma_promo = -1;
+    uint32_t hot_rows = 0;
+    uint32_t row_align = 0;
+    uint32_t direct_piece = 0;
+};
+
+uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin, uint32_t cap);
 // Host: the PRIVATE layout's lane-independent pair words for R copies (StepPrivate::npairs u32).
 void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t R, uint32_t* pairs);
 size_t direct_smem_bytes(Res mode, const DevTables& t);
 size_t table_smem_bytes(Res mode, const DevTables& t);   // SIZE_MAX/2 if the layout cannot hold t
 uint32_t direct_threads_per_cta();
 // false if `mode` cannot run the TMA scan within smem_optin bytes
-bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, TmaConfig* out);
+bool tma_choose(Res mode, const DevTables& t, size_t smem_optin, const Tuning& tu, TmaConfig* out);
 
 // Per-step-policy launchers, specialised in kernels_<step>.cu.
 template <class Step>
 struct StepLaunch {
     static cudaError_t scan_tma(bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s);
     static cudaError_t scan_direct(bool vec, const DirectArgs& a, cudaStream_t s);
-    static cudaError_t batch(bool vec, const BatchArgs& a, int sm_count, cudaStream_t s);
+    // batch (SEG) scan: host plan (a.dplan == nullptr, maps encoded here) or device plan
+    static cudaError_t scan_seg(const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t s);
 };
 
 // Sequential reduction over shard mappings (Alg. 5, right column):
@@ -114,6 +130,11 @@ cudaError_t launch_spec(const SpecArgs& a, uint32_t threads, size_t smem, cudaSt
 
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);
-cudaError_t launch_batch(Res mode, bool vec, const BatchArgs& a, int sm_count, cudaStream_t stream);
+cudaError_t launch_scan_seg(Res mode, const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t stream);
+// k_batch_plan (plain launch: it waits for all earlier work of the stream, e.g. the kernel that wrote the offsets)
+cudaError_t launch_batch_plan(const BatchPlanArgs& a, const TmaConfig& cfg, int sm_count, cudaStream_t stream);
+// n == 0 answers and the identity mapping without a host round trip
+cudaError_t launch_fill_result(sfa_result* r, uint32_t q, uint32_t acc, uint32_t* map, uint32_t nD, cudaStream_t stream);
+cudaError_t launch_fill_results(sfa_result* r, uint64_t count, uint32_t q, uint32_t acc, cudaStream_t stream);
 
 }  // namespace sfa

@@ -2,21 +2,29 @@
 // and their host launch templates.  Included by one kernels_<step>.cu per step
 // policy (parallel build); kernels.cu holds the host-side planning/dispatch.
 //
-//   k_scan_tma     one long text.  One CTA per SM: kNW compute warps + 1 TMA
-//                  producer warp.  The 16-aligned body of the text is viewed as
-//                  a 2-D tensor [nchunks rows x L bytes]; every stage the
-//                  producer loads a 16-byte column slice of all of the CTA's
-//                  rows (TMA 2-D boxes, mbarrier ring), each compute thread owns
-//                  K rows (= K chunks of Alg. 5 lines 1-5, interleaved for ILP),
-//                  so every byte of HBM is read once and the smem reads of the
-//                  staged text are conflict-free.  Chunk states are composed
-//                  warp -> block -> grid (line 6); the last CTA to finish folds
-//                  the per-CTA partials (plus the head piece) and finalises
-//                  (line 7).  The last CTA also runs the ragged tail.
-//   k_scan_direct  small texts and the forced-chunking test knob: one piece
+//   k_scan_tma     a long byte range.  One CTA per SM: kNW compute warps + 1
+//                  TMA producer warp.  The 256-aligned body of the range is
+//                  viewed as a 2-D tensor [nchunks rows x L bytes]; every stage
+//                  the producer loads a ROWB-byte column slice of all of the
+//                  CTA's rows (TMA 2-D boxes, mbarrier ring), each compute
+//                  thread owns K rows (= K chunks of Alg. 5 lines 1-5,
+//                  interleaved for ILP), so every byte of HBM is read once and
+//                  the smem reads of the staged text are conflict-free.
+//                  Two modes:
+//                    one text (SEG = false): chunk states are composed warp ->
+//                      block -> grid (line 6); the last CTA to finish folds the
+//                      per-CTA partials (plus the head piece and the ragged
+//                      tail) and finalises (line 7).
+//                    a batch (SEG = true, A5): the texts lie back to back in
+//                      the range; a row may hold several text boundaries.  A
+//                      chunk's value is then a segmented element (the piece
+//                      before its first boundary, the piece after its last),
+//                      texts that start and end inside a row are finished in
+//                      place, and the same warp -> block -> grid tree composes
+//                      the elements with a segmented operator that finishes a
+//                      text where its first and last pieces meet.
+//   k_scan_direct  short texts and the forced-chunking test knob: one piece
 //                  per thread (SPEC's chunk rule), same composition tree.
-//   k_batch_*      many texts (A5): a device-side plan, a work-stealing scan
-//                  over (text, segment) tasks and a per-text combine.
 #pragma once
 
 #include <cuda.h>
@@ -26,6 +34,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -64,7 +73,11 @@ template <class Step>
 struct Comp<Step, true> {
     static constexpr int kSlot = 32;  // bytes per stored value
     __device__ static uint32_t identity() { return lane_id(); }
-    __device__ static uint32_t fold_states(const Step&, const DevTables& t, uint32_t s) { return vec_fold_ids(t.maps32, s); }
+    // maps32: its smem copy when the aux image holds it
+    __device__ static const uint8_t* maps(const DevTables& t) {
+        return t.aux_maps ? dsmem + table_bytes<Step>(t) + t.aux_maps_off : t.maps32;
+    }
+    __device__ static uint32_t fold_states(const Step&, const DevTables& t, uint32_t s) { return vec_fold_ids(maps(t), s); }
     __device__ static uint32_t combine(const Step&, const DevTables&, uint32_t a, uint32_t b) { return vec_compose(a, b); }
     __device__ static void store(uint8_t* slot, uint32_t v) { slot[lane_id()] = static_cast<uint8_t>(v); }
     __device__ static uint32_t load(const uint8_t* slot) { return slot[lane_id()]; }
@@ -86,11 +99,18 @@ template <class Step>
 struct Comp<Step, false> {
     static constexpr int kSlot = 4;
     __device__ static uint32_t identity() { return 0; }  // f_I has id 0 (C3)
-    __device__ static uint32_t combine(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
-        if (t.comp) {
+    __device__ __forceinline__ static uint32_t combine(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
+        if (a == 0) return b;  // f_I . f = f
+        if (b == 0) return a;
+        if (t.comp) {  // its smem copy when the aux image holds it
+            const void* c = t.aux_comp ? static_cast<const void*>(dsmem + table_bytes<Step>(t)) : t.comp;
             const uint32_t i = a * t.nS + b;
-            return t.comp_u8 ? static_cast<const uint8_t*>(t.comp)[i] : static_cast<const uint16_t*>(t.comp)[i];
+            return t.comp_u8 ? static_cast<const uint8_t*>(c)[i] : static_cast<const uint16_t*>(c)[i];
         }
+        return combine_slow(S, t, a, b);
+    }
+    // no composition table (|S| > 4096): a call, so the folds stay small
+    __device__ __noinline__ static uint32_t combine_slow(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
         if (t.fact_fam && t.maps16) {
             // a factorable: f_a = (family F, g) sends its unmarked q to g and the
             // marked ones to absorbing states, which f_b fixes; so f_a . f_b =
@@ -139,20 +159,16 @@ struct Comp<Step, false> {
 // Kernel prologue: the step table -> dsmem[0, tbl) (expanded from the compact
 // window table), the aux image (composition table and/or maps32,
 // DevTables::aux) -> dsmem[tbl, tbl + aux) unless `aux_async` (the caller
-// bulk-copies it), cooperatively by `nthreads` threads; `t` is rebound to the
-// smem copies.
+// bulk-copies it), cooperatively by `nthreads` threads.  `t` stays the
+// kernel parameter (no local copy): Comp finds the smem copies by offset.
 template <class Step>
-__device__ __forceinline__ void load_tables(DevTables& t, int tid, int nthreads, bool aux_async = false,
+__device__ __forceinline__ void load_tables(const DevTables& t, int tid, int nthreads, bool aux_async = false,
                                             uint32_t compact_s = 0) {
     Step::fill(t, tid, nthreads, compact_s);
     const uint32_t tb = static_cast<uint32_t>((Step::smem_bytes(t) + 15) & ~size_t(15));
-    if (t.aux_bytes) {
-        if (!aux_async)
-            copy16(reinterpret_cast<uint4*>(dsmem + tb), reinterpret_cast<const uint4*>(t.aux), t.aux_bytes / 16, tid,
-                   nthreads);
-        if (t.aux_comp) t.comp = dsmem + tb;
-        if (t.aux_maps) t.maps32 = dsmem + tb + t.aux_maps_off;
-    }
+    if (t.aux_bytes && !aux_async)
+        copy16(reinterpret_cast<uint4*>(dsmem + tb), reinterpret_cast<const uint4*>(t.aux), t.aux_bytes / 16, tid,
+               nthreads);
 }
 
 template <class Step, bool VEC>
@@ -225,30 +241,200 @@ __device__ __forceinline__ void store_partial(uint8_t* partials, uint32_t slot, 
 }
 
 // ------------------------------------------------------------------------------------------
+// Batches (A5, SEG kernels): the texts back to back form one range; text
+// boundaries may fall anywhere in a chunk.
+//
+// A chunk (row, head/tail piece, warp, CTA, ...) folds to a segmented element
+//   (h, b, tl, t):  b = the chunk contains a text boundary (its start counts);
+//                   h = the SFA state of the piece before the first boundary
+//                       (the whole chunk if !b; f_I if the chunk starts a text);
+//                   tl, t = the text of the piece after the last boundary and
+//                       that piece's value.
+// Elements compose in text order by
+//   (h1,0)      . (h2,0)      = (h1.h2, 0)
+//   (h1,0)      . (h2,1,l2,t2)= (h1.h2, 1, l2, t2)
+//   (h1,1,l1,t1). (h2,0)      = (h1, 1, l1, t1.h2)
+//   (h1,1,l1,t1). (h2,1,l2,t2)= (h1, 1, l2, t2)   and text l1 = t1.h2 is complete
+// (associative: it is the composition of Alg. 5 line 6 restricted to each
+// text).  A complete text's result is written where its two ends meet, so
+// every text is finished exactly once; the range's last text when the whole
+// range is folded.
+//
+// A value is an SFA id, or, for the piece that starts a text, possibly a DFA
+// state tagged with kTag: a text always starts in q0, so its first piece only
+// needs f(q0) -- which the FACTORED step (a warp running the DFA on each
+// chunk's surviving image) computes directly.  (kTag | q) . s = kTag | f_s(q).
+// ------------------------------------------------------------------------------------------
+constexpr uint32_t kTag = 0x80000000u;
+constexpr uint32_t kTagFam = 0xfffeu;  // FACTORED step: the lane runs the DFA from q0 (a text's first piece)
+
+struct SegEl {
+    uint32_t h, t, tl, b;
+};
+
+__device__ __forceinline__ SegEl seg_identity() { return SegEl{0u, 0u, 0u, 0u}; }
+
+__device__ __forceinline__ SegEl shfl_down_el(const SegEl& e, int d) {
+    return SegEl{__shfl_down_sync(kFull, e.h, d), __shfl_down_sync(kFull, e.t, d), __shfl_down_sync(kFull, e.tl, d),
+                 __shfl_down_sync(kFull, e.b, d)};
+}
+
+// The boundaries of a batch range: text i = [start(i), start(i+1)).
+struct Bounds {
+    const uint64_t* off;  // count + 1 absolute offsets; nullptr: equal texts of `len` bytes
+    uint64_t off0, count, len;
+    __device__ __forceinline__ uint64_t start(uint64_t i) const {
+        return off ? __ldg(off + i) - off0 : i * len;
+    }
+    // the nonempty text that holds byte x (x < range length): the last i with start(i) <= x
+    __device__ uint32_t text_at(uint64_t x) const {
+        if (!off) return static_cast<uint32_t>(x / len);
+        uint64_t lo = 0, hi = count;  // start(lo) <= x < start(hi)
+        const uint64_t ax = x + off0;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (__ldg(off + mid) <= ax) lo = mid;
+            else hi = mid;
+        }
+        return static_cast<uint32_t>(lo);
+    }
+    // the nonempty text that starts where text i ends (empty texts skipped)
+    __device__ __noinline__ uint32_t next(uint32_t i) const {
+        if (!off) return i + 1;
+        const uint64_t e = __ldg(off + i + 1);
+        ++i;
+        while (__ldg(off + i + 1) == e) ++i;
+        return i;
+    }
+};
+
+template <class Step>
+struct Seg {
+    // f_s(q): the mapping table, else Lemma-1 replay of rep(s) through the DFA
+    // window table (smem; kTag values only come from FACTORED warps, which have it)
+    __device__ __noinline__ static uint32_t apply(const DevTables& t, uint32_t s, uint32_t q) {
+        if (t.maps16) return __ldg(t.maps16 + static_cast<uint64_t>(s) * t.nD + q);
+        const uint32_t R = t.dwin_R, c = lane_id() % R, neg_lo = 0u - t.lo, wmax = t.W - 1;
+        uint32_t st = dfa_enc(q, c, R);
+        const uint32_t e = __ldg(t.rep_off + s + 1);
+        for (uint32_t k = __ldg(t.rep_off + s); k < e; ++k)
+            st = ld_tbl_u16(window_col(__ldg(t.rep + k), neg_lo, wmax) * t.dwin_X + st);
+        return dfa_dec(st, c, R);
+    }
+    // a . b for two values of one text in order (b is never tagged)
+    __device__ static uint32_t cval(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
+        if (a & kTag) return b == 0 ? a : (kTag | apply(t, b, a & ~kTag));
+        return Comp<Step, false>::combine(S, t, a, b);
+    }
+    __device__ __noinline__ static void emit(const DevTables& t, sfa_result* res, uint32_t ti, uint32_t v) {
+        const uint32_t q = (v & kTag) ? (v & ~kTag) : t.img0[v];
+        res[ti] = sfa_result{q, t.dfinal[q]};
+    }
+    __device__ __noinline__ static SegEl comb(const Step& S, const DevTables& t, sfa_result* res, const SegEl x,
+                                              const SegEl y) {
+        SegEl r;
+        if (!x.b) {
+            r.h = cval(S, t, x.h, y.h);
+            r.b = y.b;
+            r.tl = y.tl;
+            r.t = y.t;
+        } else {
+            const uint32_t m = cval(S, t, x.t, y.h);
+            r.h = x.h;
+            r.b = 1;
+            if (y.b) {
+                emit(t, res, x.tl, m);
+                r.tl = y.tl;
+                r.t = y.t;
+            } else {
+                r.tl = x.tl;
+                r.t = m;
+            }
+        }
+        return r;
+    }
+    // the 32 lanes' elements in lane order; result in lane 0
+    __device__ static SegEl fold_warp(const Step& S, const DevTables& t, sfa_result* res, SegEl e) {
+        const uint32_t lane = lane_id();
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const SegEl o = shfl_down_el(e, d);
+            if ((lane & (2 * d - 1)) == 0) e = comb(S, t, res, e, o);
+        }
+        return e;
+    }
+    // fold `count` stored elements (smem or global) in order into acc (valid in lane 0)
+    __device__ static SegEl fold_slots(const Step& S, const DevTables& t, sfa_result* res, const uint4* base,
+                                       uint32_t count, SegEl acc, bool global) {
+        for (uint32_t c0 = 0; c0 < count; c0 += 32) {
+            const uint32_t u = c0 + lane_id();
+            SegEl x = seg_identity();
+            if (u < count) {
+                const uint4 v = global ? __ldcg(base + u) : base[u];
+                x = SegEl{v.x, v.y, v.z, v.w};
+            }
+            x = fold_warp(S, t, res, x);
+            if (lane_id() == 0) acc = comb(S, t, res, acc, x);
+        }
+        return acc;
+    }
+    // a piece [x0, x1) of the range run byte by byte by one thread (head and tail pieces)
+    __device__ __noinline__ static SegEl run_piece(const Step& S, const DevTables& t, sfa_result* res, const Bounds B,
+                                      const uint8_t* text, uint64_t x0, uint64_t x1) {
+        SegEl e = seg_identity();
+        if (x0 >= x1) return e;
+        const uint32_t lane = lane_id();
+        uint32_t ti = B.text_at(x0);
+        e.b = B.start(ti) == x0;
+        uint64_t nb = B.start(static_cast<uint64_t>(ti) + 1);
+        uint32_t st = S.init(lane);
+        uint64_t p = x0;
+        for (;;) {
+            const uint64_t q = nb < x1 ? nb : x1;
+            st = run_range(S, st, text, p, q);
+            p = q;
+            if (p == x1) break;
+            const uint32_t v = S.id(st, lane);  // a boundary inside the piece
+            if (!e.b) {
+                e.h = v;
+                e.b = 1;
+            } else {
+                emit(t, res, ti, v);
+            }
+            ti = B.next(ti);
+            nb = B.start(static_cast<uint64_t>(ti) + 1);
+            st = S.init(lane);
+        }
+        if (e.b) {  // the running piece is the last one
+            e.tl = ti;
+            e.t = S.id(st, lane);
+        } else {    // no boundary: the whole piece is h
+            e.h = S.id(st, lane);
+        }
+        return e;
+    }
+};
+
+// ------------------------------------------------------------------------------------------
 // k_scan_tma
 //
-// Shared memory (dynamic):  [table | red slots | flag | mbarriers | stage ring]
+// Shared memory (dynamic):  [table | staging | red slots | flag | mbarriers | stage ring]
 // The table is first so its base is an immediate of every LDS.  A stage holds
-// ROWB bytes of each of the CTA's R rows (row-major, ROWB per row), loaded by
-// NB 2-D TMA boxes of [ROWB x BR]; the ring depth is chosen at launch from the
-// shared memory left after the table.  The producer also prefetches each
-// row's next 256-byte line into L2 once (a second tensor map with 256-B boxes)
-// so the TMA loads hit L2.
+// ROWB bytes of each of the CTA's rows (row-major, ROWB per row), loaded by
+// NB 2-D TMA boxes; the ring depth is chosen at launch from the shared memory
+// left after the table.
 // ------------------------------------------------------------------------------------------
 constexpr int kNW = 31;        // compute warps
 constexpr int kMaxRing = 8;    // max smem ring depth
-constexpr int kLine = 256;     // L2 prefetch granularity (bytes of a row)
 
 template <int K>
 __host__ __device__ constexpr int Sh_NB() { return (K * kNW * 32 + 255) / 256; }
 
 template <int K, int ROWB>
 struct TmaShape {
-    static constexpr int R = K * kNW * 32;            // rows (chunks) per CTA
+    static constexpr int R = K * kNW * 32;            // rows (chunks) per CTA at most
     static constexpr int NB = (R + 255) / 256;        // TMA boxes per stage (box dim <= 256)
-    static constexpr int BR = R / NB;                 // rows per box
-    static_assert(R % NB == 0, "rows must split evenly into boxes");
-    static_assert(ROWB % 16 == 0 && kLine % ROWB == 0, "row slice must be 16-B granular");
+    static_assert(ROWB % 16 == 0 && 256 % ROWB == 0, "row slice must be 16-B granular");
     // TMA swizzle matched to the row slice (16 B: none, 32 B: SWIZZLE_32B,
     // 64 B: SWIZZLE_64B): 16-byte chunk bits [4, 4+log2(ROWB/16)) of a smem
     // address are XORed with bits [7, ...).  With it, the 8 lanes of one LDS.128
@@ -264,14 +450,37 @@ struct TmaShape {
 };
 
 struct TmaMaps {
-    CUtensorMap load;      // box [ROWB x BR]
-    CUtensorMap pref;      // box [256 x BR], L2 prefetch only
+    CUtensorMap load;      // box [ROWB x bh]: the first NB - 1 boxes of a stage
+    CUtensorMap last_hi;   // box [ROWB x bl_hi]: the last box of CTAs with rc_hi rows
+    CUtensorMap last_lo;   // box [ROWB x bl_lo]: ... with rc_lo rows
 };
 
 // The consumer side of the stage ring: full/empty mbarriers, slot, phase.
 struct Ring {
     uint32_t full0, empty0, base, n, slot, phase;
+    __device__ __forceinline__ uint32_t src(uint32_t stage_bytes) const { return base + slot * stage_bytes; }
+    // Release the slot only after every lane has consumed its loaded bytes,
+    // so no LDS of this stage can still be in flight when the producer's next
+    // TMA write lands (an arrive right after issuing the LDS raced).
+    __device__ __forceinline__ void release(uint32_t lane) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+        if (++slot == n) {
+            slot = 0;
+            phase ^= 1;
+        }
+    }
 };
+
+template <int K, int ROWB, class Sh>
+__device__ __forceinline__ void load_stage(uint4 (&v)[K][ROWB / 16], const uint32_t (&rsrc)[K][ROWB / 16], Ring& ring) {
+    mbar_wait(ring.full0 + 8 * ring.slot, ring.phase);
+    const uint32_t src = ring.base + ring.slot * Sh::kStageBytes;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int c = 0; c < ROWB / 16; ++c) v[k][c] = lds_v4(src + rsrc[k][c]);
+}
 
 // Stages [i0, i1) of the K rows of this thread through `S` (Alg. 5 lines 3-5):
 // wait for the stage, read each row's ROWB bytes (swizzled LDS.128), step the
@@ -280,13 +489,8 @@ template <int K, int ROWB, class Sh, class StepT>
 __device__ __forceinline__ void scan_stages(const StepT& S, uint32_t (&st)[K], const uint32_t (&rsrc)[K][ROWB / 16],
                                             Ring& ring, uint32_t i0, uint32_t i1, uint32_t lane) {
     for (uint32_t i = i0; i < i1; ++i) {
-        mbar_wait(ring.full0 + 8 * ring.slot, ring.phase);
-        const uint32_t src = ring.base + ring.slot * Sh::kStageBytes;
         uint4 v[K][ROWB / 16];
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-            for (int c = 0; c < ROWB / 16; ++c) v[k][c] = lds_v4(src + rsrc[k][c]);
+        load_stage<K, ROWB, Sh>(v, rsrc, ring);
 #pragma unroll
         for (int c = 0; c < ROWB / 16; ++c) {
             const uint32_t* w[K];
@@ -304,26 +508,76 @@ __device__ __forceinline__ void scan_stages(const StepT& S, uint32_t (&st)[K], c
                 for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
             }
         }
-        // Release the slot only now: every lane has consumed its loaded bytes,
-        // so no LDS of this stage can still be in flight when the producer's
-        // next TMA write lands (an arrive right after issuing the LDS raced).
-        __syncwarp();
-        if (lane == 0) mbar_arrive(ring.empty0 + 8 * ring.slot);
-        if (++ring.slot == ring.n) {
-            ring.slot = 0;
-            ring.phase ^= 1;
-        }
+        ring.release(lane);
     }
 }
 
-template <class Step, int K, int ROWB, bool VEC>
+// Per-row segment state of a SEG scan (row-relative positions).
+template <int K>
+struct RowSegs {
+    uint64_t x0[K];   // row start in the range
+    uint32_t nb[K];   // next boundary (row-relative); >= L: none inside the row
+    uint32_t h[K], tl[K];
+    uint32_t b[K], ts[K];  // ts: the running piece starts a text
+};
+
+// The same for a batch: a stage in which some row of the warp meets a text
+// boundary runs byte by byte (LDS.U8 from the stage) and `close(k)` ends row
+// k's running piece after the byte that reaches its boundary nb[k].
+template <int K, int ROWB, class Sh, class StepT, class Close>
+__device__ __forceinline__ void scan_stages_seg(const StepT& S, uint32_t (&st)[K], const uint32_t (&rsrc)[K][ROWB / 16],
+                                                const uint32_t (&rrow)[K], Ring& ring, uint32_t i0, uint32_t i1,
+                                                uint32_t lane, const uint32_t (&nb)[K], Close&& close) {
+    for (uint32_t i = i0; i < i1; ++i) {
+        const uint32_t pend = (i + 1) * ROWB;
+        bool need = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) need |= nb[k] <= pend;
+        if (!__any_sync(kFull, need)) {
+            uint4 v[K][ROWB / 16];
+            load_stage<K, ROWB, Sh>(v, rsrc, ring);
+#pragma unroll
+            for (int c = 0; c < ROWB / 16; ++c) {
+                const uint32_t* w[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) w[k] = reinterpret_cast<const uint32_t*>(&v[k][c]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<0>(w[k][q]));
+#pragma unroll
+                    for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<1>(w[k][q]));
+#pragma unroll
+                    for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<2>(w[k][q]));
+#pragma unroll
+                    for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
+                }
+            }
+        } else {
+            mbar_wait(ring.full0 + 8 * ring.slot, ring.phase);
+            const uint32_t src = ring.src(Sh::kStageBytes);
+#pragma unroll 1
+            for (uint32_t j = 0; j < ROWB; ++j) {
+                const uint32_t pos = i * ROWB + j + 1;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    st[k] = S.step(st[k], lds_u8(src + Sh::swz(rrow[k] * ROWB + j)));
+                    if (pos == nb[k]) close(k);
+                }
+            }
+        }
+        ring.release(lane);
+    }
+}
+
+template <class Step, int K, int ROWB, bool VEC, bool SEG>
 __global__ void __launch_bounds__((kNW + 1) * 32, 1)
-k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_t tbl_bytes, const uint32_t stage_bytes,
-           const uint32_t nring, const int pf_lines) {
-    // rows of this CTA: [blockIdx.x * rc, +rc), loaded as NB boxes of br rows
-    const uint32_t rc = a.plan.rows_per_cta, br = rc / Sh_NB<K>();
+k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArgs a, const uint32_t tbl_bytes,
+           const uint32_t stage_bytes,
+           const uint32_t nring) {
     using Sh = TmaShape<K, ROWB>;
     using CP = Comp<Step, VEC>;
+    using SG = Seg<Step>;
     // [step table + aux (tbl_bytes) | compact table staging (stage_bytes) | red | flag | bars | ring]
     uint8_t* const staging = dsmem + ((tbl_bytes + 15) & ~15u);
     uint8_t* red = staging + stage_bytes;
@@ -335,7 +589,6 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     const uint32_t ring0 = (smem_u32(bars + 2 * kMaxRing + 3) + 1023) & ~1023u;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nstages = static_cast<uint32_t>(a.plan.L / ROWB);
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + kMaxRing * 8;
     pdl_launch_dependents();
     if (threadIdx.x == 0) {
@@ -352,10 +605,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
 
     if (warp == kNW) {  // ---- TMA producer ----
         if (lane == 0) {
-            prefetch_tmap(&maps.load);
-            prefetch_tmap(&maps.pref);
-            const uint64_t policy = policy_evict_first();
-            if (stage_bytes) {  // the compact table, expanded in smem by the compute warps
+            if (stage_bytes) {  // the compact table (the handle's), expanded in smem by the compute warps
                 mbar_expect_tx(cbar, stage_bytes);
                 bulk_g2s(smem_u32(staging), Step::staged_src(a.t), stage_bytes, cbar);
             }
@@ -364,11 +614,25 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
                 mbar_expect_tx(abar, a.t.aux_bytes);
                 bulk_g2s(smem_u32(dsmem + tb), a.t.aux, a.t.aux_bytes, abar);
             }
-            const int y0 = blockIdx.x * rc;
-            const uint32_t nlines = static_cast<uint32_t>((a.plan.L + kLine - 1) / kLine);
-            for (int l = 0; l <= pf_lines && l < static_cast<int>(nlines); ++l)
-                for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&maps.pref, l * kLine, y0 + j * br);
-            constexpr uint32_t kStagesPerLine = kLine / ROWB;
+            // The text (and a batch's plan) may come from the previous kernel of
+            // the stream: nothing of it is read before that kernel completed.
+            pdl_wait();
+            if (SEG && a.err && *a.err == a.epoch) return;  // bad offsets: the compute warps report
+            const TmaPlan P = a.dplan ? *a.dplan : a.plan;
+            const uint32_t rc = P.cta_rows(blockIdx.x);
+            if (rc == 0) return;
+            const CUtensorMap* gm = static_cast<const CUtensorMap*>(a.gmaps);
+            const CUtensorMap* mload = gm ? gm : &maps.load;
+            const CUtensorMap* mlast = gm ? gm + (rc == P.rc_hi ? 1 : 2) : (rc == P.rc_hi ? &maps.last_hi : &maps.last_lo);
+            if (gm) {
+                tmap_acquire(mload);
+                tmap_acquire(mlast);
+            }
+            prefetch_tmap(mload);
+            prefetch_tmap(mlast);
+            const uint64_t policy = policy_evict_first();
+            const int y0 = static_cast<int>(P.cta_row0(blockIdx.x));
+            const uint32_t nstages = static_cast<uint32_t>(P.L / ROWB);
             uint32_t slot = 0, phase = 0;
             for (uint32_t i = 0; i < nstages; ++i) {
                 // Only the first stage is requested before the compute warps
@@ -378,13 +642,11 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
                 if (i >= nring) mbar_wait(empty0 + 8 * slot, phase ^ 1);
                 mbar_expect_tx(full0 + 8 * slot, rc * ROWB);
                 const uint32_t dst = ring0 + slot * Sh::kStageBytes;
-                for (int j = 0; j < Sh::NB; ++j)
-                    tma_load_2d(dst + j * br * ROWB, &maps.load, full0 + 8 * slot, i * ROWB, y0 + j * br, policy);
-                if (pf_lines >= 0 && i % kStagesPerLine == 0) {  // entering line l: prefetch line l + pf_lines + 1
-                    const uint32_t l = i / kStagesPerLine + pf_lines + 1;
-                    if (l < nlines)
-                        for (int j = 0; j < Sh::NB; ++j) tma_prefetch_2d(&maps.pref, l * kLine, y0 + j * br);
-                }
+#pragma unroll
+                for (int j = 0; j < Sh::NB - 1; ++j)
+                    tma_load_2d(dst + j * P.bh * ROWB, mload, full0 + 8 * slot, i * ROWB, y0 + j * P.bh, policy);
+                tma_load_2d(dst + (Sh::NB - 1) * P.bh * ROWB, mlast, full0 + 8 * slot, i * ROWB,
+                            y0 + (Sh::NB - 1) * P.bh, policy);
                 if (++slot == nring) {
                     slot = 0;
                     phase ^= 1;
@@ -395,46 +657,57 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     }
 
     // ---- compute warps ----
-    uint64_t* const stamp = (a.stamps && threadIdx.x == 0) ? a.stamps + 8 * blockIdx.x : nullptr;
-    if (stamp) stamp[0] = globaltimer();
     Step S;
-    DevTables t = a.t;
+    const DevTables& t = a.t;
     S.params(t);
     // The table images (built on the host at upload) -> smem.  A cooperative
     // copy through generic stores (not a bulk copy): with it ptxas keeps the
     // smem base in a uniform register and folds it into every LDS.U16 of the
     // hot loop ([R+UR]), one IADD per byte less.
-    const long long c0 = clock64();
     if (stage_bytes) mbar_wait(cbar, 0);
-    const long long cw = clock64();
-    if (!(a.diag & 1))
-        load_tables<Step>(t, threadIdx.x, kNW * 32, true, stage_bytes ? smem_u32(staging) : 0u);
-    long long c1 = clock64();
-    if (a.diag & 2) {  // diagnostic: time a second, warm build
-        const long long c2 = clock64();
-        load_tables<Step>(t, threadIdx.x, kNW * 32, true, stage_bytes ? smem_u32(staging) : 0u);
-        c1 = c0 + (clock64() - c2) + ((c2 - c0) << 32);  // stamp[5]: cold cycles << 32 | warm cycles
-    }
+    load_tables<Step>(t, threadIdx.x, kNW * 32, true, stage_bytes ? smem_u32(staging) : 0u);
     __syncwarp();
     if (lane == 0) mbar_arrive(rbar);
     bar_compute(kNW * 32);
-    if (stamp) {
-        stamp[1] = globaltimer();
-        stamp[5] = static_cast<uint64_t>(c1 - c0);           // thread 0's own fill, SM cycles
-        stamp[6] = static_cast<uint64_t>(cw - c0);           // wait for the staged compact table
+    // Everything below reads the text, the plan or the scratch shared with
+    // the previous launch of the stream: wait for it (the prologue above
+    // overlapped its tail).
+    pdl_wait();
+    if (SEG && a.err && *a.err == a.epoch) {  // k_batch_plan found decreasing offsets: every result is invalid
+        if (t.aux_bytes) mbar_wait(abar, 0);  // no bulk copy may land after the CTA exits
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kNW * 32 + threadIdx.x; i < a.count;
+             i += static_cast<uint64_t>(gridDim.x) * kNW * 32)
+            a.results[i] = sfa_result{0xffffffffu, 0u};
+        return;
     }
+    const TmaPlan P = a.dplan ? *a.dplan : a.plan;
+    const uint32_t rc = P.cta_rows(blockIdx.x);
+    const uint64_t crow0 = P.cta_row0(blockIdx.x);
+    const uint32_t nstages = rc ? static_cast<uint32_t>(P.L / ROWB) : 0u;
+    const Bounds B{a.off, a.off ? __ldg(a.off) : 0ull, a.count, P.len};
+    const uint8_t* const text = a.text + B.off0;  // the range: one text, or the batch's texts back to back
+    if (t.aux_bytes) mbar_wait(abar, 0);
 
-    // The last CTA also runs the ragged tail [tail_start, n) (< L + 16 bytes),
-    // split over its compute threads; its value goes to slot gridDim.x (stored
-    // after pdl_wait below, with the CTA's own partial).
+    // The last CTA also runs the ragged tail [tail_start, n) (< (1 + 8 NB) L
+    // bytes), split over its compute threads; its value goes to slot
+    // gridDim.x of the partials.
     uint32_t tail_acc = 0;
+    SegEl tail_el = seg_identity();
     if (blockIdx.x == gridDim.x - 1) {
-        if (t.aux_bytes) mbar_wait(abar, 0);
-        const uint64_t len = a.n - a.plan.tail_start;
+        const uint64_t len = P.n - P.tail_start;
         const uint64_t per = (len + kNW * 32 - 1) / (kNW * 32);
-        const uint64_t p0 = min(a.n, a.plan.tail_start + threadIdx.x * per), p1 = min(a.n, p0 + per);
-        const uint32_t s = S.id(run_range(S, S.init(lane), a.text, p0, p1), lane);
-        tail_acc = block_fold<Step, VEC>(S, t, s, kNW, red);
+        const uint64_t p0 = min(P.n, P.tail_start + threadIdx.x * per), p1 = min(P.n, p0 + per);
+        if constexpr (SEG) {
+            SegEl e = SG::fold_warp(S, t, a.results, SG::run_piece(S, t, a.results, B, text, p0, p1));
+            if (lane == 0) *reinterpret_cast<uint4*>(red + warp * 16) = make_uint4(e.h, e.t, e.tl, e.b);
+            bar_compute(kNW * 32);
+            if (warp == 0)
+                tail_el = SG::fold_slots(S, t, a.results, reinterpret_cast<const uint4*>(red), kNW, seg_identity(), false);
+            bar_compute(kNW * 32);
+        } else {
+            const uint32_t s = S.id(run_range(S, S.init(lane), text, p0, p1), lane);
+            tail_acc = block_fold<Step, VEC>(S, t, s, kNW, red);
+        }
     }
 
     uint32_t st[K];
@@ -442,90 +715,181 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const ScanArgs a, const uint32_
     for (int k = 0; k < K; ++k) st[k] = S.init(lane);
     const uint32_t row0 = warp * 32 + lane;
     uint32_t rsrc[K][ROWB / 16];  // swizzled stage offset of each 16-B piece of this thread's rows
+    uint32_t rrow[K];             // the rows in the stage (0 for rows past the CTA's)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const uint32_t r = k * kNW * 32 + row0;
+        rrow[k] = r < rc ? r : 0u;
 #pragma unroll
-        for (int c = 0; c < ROWB / 16; ++c) rsrc[k][c] = Sh::swz((r < rc ? r : 0u) * ROWB + c * 16);
+        for (int c = 0; c < ROWB / 16; ++c) rsrc[k][c] = Sh::swz(rrow[k] * ROWB + c * 16);
     }
+    bool valid[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t r = k * kNW * 32 + row0;
+        valid[k] = r < rc && crow0 + r < P.nchunks;
+    }
+    RowSegs<K> rs{};
+    if constexpr (SEG) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            rs.x0[k] = P.head + (crow0 + k * kNW * 32 + row0) * P.L;
+            rs.h[k] = 0;
+            rs.b[k] = rs.ts[k] = 0;
+            rs.tl[k] = 0;
+            rs.nb[k] = 0xffffffffu;
+            if (valid[k]) {
+                const uint32_t ti = B.text_at(rs.x0[k]);
+                rs.tl[k] = ti;
+                rs.b[k] = rs.ts[k] = B.start(ti) == rs.x0[k];
+                const uint64_t e = B.start(static_cast<uint64_t>(ti) + 1) - rs.x0[k];
+                rs.nb[k] = e < P.L ? static_cast<uint32_t>(e) : 0xffffffffu;  // a boundary at the row end is the next row's
+            }
+        }
+    }
+    // row k's running piece ends at its boundary nb[k] (v = its value): the
+    // first boundary of the row closes h; later ones finish a whole text
+    auto seg_close = [&](int k, uint32_t v) {
+        if (!rs.b[k]) {
+            rs.h[k] = v;
+            rs.b[k] = 1;
+        } else {
+            SG::emit(t, a.results, rs.tl[k], v);
+        }
+        const uint32_t ti = B.next(rs.tl[k]);
+        rs.tl[k] = ti;
+        const uint64_t e = B.start(static_cast<uint64_t>(ti) + 1) - rs.x0[k];
+        rs.nb[k] = e < P.L ? static_cast<uint32_t>(e) : 0xffffffffu;
+        rs.ts[k] = 1;
+    };
+
     Ring ring{full0, empty0, ring0, nring, 0, 0};
-    uint32_t fact_ids[K];  // canonical ids of factored chunks (valid when `factored`)
+    uint32_t fam[K], g[K];  // FACTORED: (family, DFA state) of each row
     bool factored = false;
+    auto close_sfa = [&](int k) {
+        seg_close(k, S.id(st[k], lane));
+        st[k] = S.init(lane);
+    };
     if constexpr (Step::kFactor) {
         // Stages through the SFA table until every lane's state is factorable
         // (<= 1 non-absorbing image; the image count never grows along a
         // walk), checked after stages 1, 2, 4, 8, ...; the rest with the
-        // factored DFA step.
+        // factored DFA step.  A batch row's piece that starts a text needs
+        // only f(q0): it continues as the DFA run from q0 (kTagFam).
         uint32_t i = 0, next_check = 1;
         while (i < nstages) {
-            scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, i, i + 1, lane);
+            if constexpr (SEG) scan_stages_seg<K, ROWB, Sh>(S, st, rsrc, rrow, ring, i, i + 1, lane, rs.nb, close_sfa);
+            else scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, i, i + 1, lane);
             ++i;
             if (!t.fact_fam || i != next_check || i == nstages) continue;
             next_check *= 2;
-            uint32_t fam[K], g[K];
             bool ok = true;
 #pragma unroll
-            for (int k = 0; k < K; ++k) ok &= fact_from_id(t, S.id(st[k], lane), fam[k], g[k]);
+            for (int k = 0; k < K; ++k) {
+                const uint32_t sid = S.id(st[k], lane);
+                if (SEG && rs.ts[k]) {
+                    fam[k] = kTagFam;
+                    g[k] = dfa_enc(t.img0[sid], lane % t.dwin_R, t.dwin_R);
+                } else {
+                    ok &= fact_from_id(t, sid, fam[k], g[k]);
+                }
+            }
             if (__all_sync(kFull, ok)) {
                 StepDfa D;
                 D.params(t);
-                scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i, nstages, lane);
-#pragma unroll
-                for (int k = 0; k < K; ++k) fact_ids[k] = fact_to_id(t, fam[k], g[k]);
+                if constexpr (SEG) {
+                    const uint32_t g0 = dfa_enc(0u, lane % t.dwin_R, t.dwin_R);
+                    auto close_fact = [&](int k) {
+                        const uint32_t v = fam[k] == kTagFam ? (kTag | dfa_dec(g[k], lane % t.dwin_R, t.dwin_R))
+                                                             : fact_to_id(t, fam[k], g[k]);
+                        seg_close(k, v);
+                        fam[k] = kTagFam;
+                        g[k] = g0;
+                    };
+                    scan_stages_seg<K, ROWB, Sh>(D, g, rsrc, rrow, ring, i, nstages, lane, rs.nb, close_fact);
+                } else {
+                    scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i, nstages, lane);
+                }
                 factored = true;
                 break;
             }
         }
     } else {
-        scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages, lane);
+        if constexpr (SEG) scan_stages_seg<K, ROWB, Sh>(S, st, rsrc, rrow, ring, 0, nstages, lane, rs.nb, close_sfa);
+        else scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages, lane);
     }
-
-    if (stamp) stamp[2] = globaltimer();
-    if (t.aux_bytes) mbar_wait(abar, 0);
-    if constexpr (!VEC) {
-        if (a.seg_m) {  // batch of equal texts: text = seg_m consecutive rows (lanes); per-text fold, no grid fold
-            const uint32_t m = a.seg_m;
-            pdl_wait();   // results may be reused by the previous launch on the stream
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const uint32_t r = k * kNW * 32 + row0;
-                const uint32_t row = blockIdx.x * rc + r;
-                uint32_t sv = factored ? fact_ids[k] : S.id(st[k], lane);
-                for (uint32_t d = 1; d < m; d <<= 1) {  // segmented shuffle tree (m | 32, texts never straddle warps)
-                    const uint32_t o = __shfl_down_sync(kFull, sv, d);
-                    if ((lane & (2 * d - 1)) == 0) sv = Comp<Step, false>::combine(S, t, sv, o);
-                }
-                if (lane % m == 0 && r < rc && row < a.plan.nchunks) {
-                    const uint32_t q = t.img0[sv];
-                    a.results[row / m] = sfa_result{q, t.dfinal[q]};
-                }
-            }
-            return;
-        }
-    }
-    // ---- composition: warp -> block (rows are ordered k-major, then warp, then lane) ----
+    // canonical value of each row's running piece
+    uint32_t val[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const uint32_t r = k * kNW * 32 + row0;
-        const uint32_t row = blockIdx.x * rc + r;
-        const uint32_t sid = factored ? fact_ids[k] : S.id(st[k], lane);
-        const uint32_t s = (r < rc && row < a.plan.nchunks) ? sid : 0u;  // rows past the text: f_I
-        CP::store(red + (k * kNW + warp) * CP::kSlot, CP::fold_states(S, t, s));
+        if (factored) {
+            val[k] = (SEG && fam[k] == kTagFam) ? (kTag | dfa_dec(g[k], lane % t.dwin_R, t.dwin_R))
+                                                : fact_to_id(t, fam[k], g[k]);
+        } else {
+            val[k] = S.id(st[k], lane);
+        }
     }
-    bar_compute(kNW * 32);
-    // Scratch (partials, ticket, result) is shared with the previous launch on
-    // the stream: everything above overlapped its tail (PDL), this waits for it.
-    pdl_wait();
-    if (warp == 0) {
-        uint32_t acc = CP::fold_slots(S, t, red, K * kNW, CP::identity(), false);
-        store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
-        if (blockIdx.x == gridDim.x - 1) store_partial<VEC>(a.sc.partials, gridDim.x, tail_acc);
+
+    if constexpr (SEG) {
+        // ---- segmented composition: warp -> block -> grid ----
+        uint4* slots = reinterpret_cast<uint4*>(red);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            SegEl e = seg_identity();  // rows past the range: f_I
+            if (valid[k]) e = rs.b[k] ? SegEl{rs.h[k], val[k], rs.tl[k], 1u} : SegEl{val[k], 0u, 0u, 0u};
+            e = SG::fold_warp(S, t, a.results, e);
+            if (lane == 0) slots[k * kNW + warp] = make_uint4(e.h, e.t, e.tl, e.b);
+        }
+        bar_compute(kNW * 32);
+        uint4* parts = reinterpret_cast<uint4*>(a.sc.partials);
+        if (warp == 0) {
+            const SegEl e = SG::fold_slots(S, t, a.results, slots, K * kNW, seg_identity(), false);
+            if (lane == 0) {
+                parts[blockIdx.x] = make_uint4(e.h, e.t, e.tl, e.b);
+                if (blockIdx.x == gridDim.x - 1) parts[gridDim.x] = make_uint4(tail_el.h, tail_el.t, tail_el.tl, tail_el.b);
+            }
+        }
+        // last CTA to finish: head piece . CTA 0 . ... . CTA G-1 . tail
+        if (warp == 0) {
+            __threadfence();
+            if (lane == 0) *flag = (atomicAdd(a.sc.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+        }
+        bar_compute(kNW * 32);
+        if (*flag == 0) return;
+        __threadfence();
+        if (warp == 0) {
+            const uint64_t hp = (P.head + 31) / 32;
+            const uint64_t h0 = min(P.head, lane * hp), h1 = min(P.head, h0 + hp);
+            SegEl acc = SG::fold_warp(S, t, a.results, SG::run_piece(S, t, a.results, B, text, h0, h1));
+            acc = SG::fold_slots(S, t, a.results, parts, gridDim.x + 1, acc, true);
+            if (lane == 0) {
+                if (acc.b) SG::emit(t, a.results, acc.tl, acc.t);  // the range's last text
+                *a.sc.ticket = 0;
+            }
+        }
+        return;
+    } else {
+        if (a.row_ids) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (valid[k]) a.row_ids[crow0 + k * kNW * 32 + row0] = val[k];
+        }
+        // ---- composition: warp -> block (rows are ordered k-major, then warp, then lane) ----
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t s = valid[k] ? val[k] : 0u;  // rows past the text: f_I
+            CP::store(red + (k * kNW + warp) * CP::kSlot, CP::fold_states(S, t, s));
+        }
+        bar_compute(kNW * 32);
+        if (warp == 0) {
+            uint32_t acc = CP::fold_slots(S, t, red, K * kNW, CP::identity(), false);
+            store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
+            if (blockIdx.x == gridDim.x - 1) store_partial<VEC>(a.sc.partials, gridDim.x, tail_acc);
+        }
+        bar_compute(kNW * 32);
+        grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, P.head, gridDim.x + 1, a.q_in, kNW, red, flag,
+                                 a.map_out);
     }
-    bar_compute(kNW * 32);
-    if (stamp) stamp[3] = globaltimer();
-    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, a.plan.head, gridDim.x + 1, a.q_in, kNW, red, flag,
-                             a.map_out);
-    if (stamp) stamp[4] = globaltimer();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -541,147 +905,28 @@ __device__ __forceinline__ uint64_t piece_start(uint64_t g, uint64_t n, uint64_t
 
 template <class Step, bool VEC>
 __global__ void __launch_bounds__(kDirectWarps * 32)
-k_scan_direct(const DirectArgs a) {
+k_scan_direct(const __grid_constant__ DirectArgs a) {
     uint8_t* red = dsmem + table_bytes<Step>(a.t) + a.t.aux_bytes;
     uint32_t* flag = reinterpret_cast<uint32_t*>(red + kDirectRed);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_launch_dependents();
     Step S;
-    DevTables t = a.t;
+    const DevTables& t = a.t;
     S.params(t);
     load_tables<Step>(t, threadIdx.x, blockDim.x);
     __syncthreads();
+    pdl_wait();  // the text and the scratch may belong to the previous kernel of the stream
     const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     uint32_t s = 0;
     if (g < a.npieces) {
         uint64_t b0 = piece_start(g, a.n, a.npieces), b1 = piece_start(g + 1, a.n, a.npieces);
         s = S.id(run_range(S, S.init(lane), a.text, b0, b1), lane);
     }
-    pdl_wait();  // scratch is shared with the previous launch on the stream
     if (g < a.npieces && a.piece_ids) a.piece_ids[g] = s;
     const uint32_t acc = block_fold<Step, VEC>(S, t, s, kDirectWarps, red);
-    if (warp == 0) store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
+    if ((threadIdx.x >> 5) == 0) store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
     bar_compute(kDirectWarps * 32);
     grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, 0, gridDim.x, a.q_in, kDirectWarps, red, flag, a.map_out);
-}
-
-// ------------------------------------------------------------------------------------------
-// Batch (A5).  Text i = texts[off[i], off[i+1]) is cut into segments of at most
-// seg bytes; a task is one segment, run by one warp (32 lane pieces).
-// ------------------------------------------------------------------------------------------
-constexpr int kBatchWarps = 16;
-
-// task_off[i] = number of tasks of texts < i (exclusive prefix), task_off[count] = total.
-static __global__ void __launch_bounds__(1024) k_batch_plan(const uint64_t* __restrict__ off, uint64_t count,
-                                                      uint64_t seg, uint32_t* __restrict__ task_off,
-                                                      uint32_t* __restrict__ work) {
-    __shared__ uint32_t part[1024];
-    const uint32_t tid = threadIdx.x;
-    const uint64_t per = (count + 1023) / 1024;
-    const uint64_t i0 = min(count, tid * per), i1 = min(count, i0 + per);
-    uint32_t sum = 0;
-    for (uint64_t i = i0; i < i1; ++i) {
-        uint64_t a = off[i], b = off[i + 1];
-        uint64_t len = b > a ? b - a : 0;
-        sum += len == 0 ? 1u : static_cast<uint32_t>((len + seg - 1) / seg);
-    }
-    part[tid] = sum;
-    __syncthreads();
-    for (int d = 1; d < 1024; d <<= 1) {  // inclusive Hillis-Steele scan
-        uint32_t x = tid >= static_cast<uint32_t>(d) ? part[tid - d] : 0;
-        __syncthreads();
-        part[tid] += x;
-        __syncthreads();
-    }
-    uint32_t run = tid ? part[tid - 1] : 0;
-    for (uint64_t i = i0; i < i1; ++i) {
-        task_off[i] = run;
-        uint64_t a = off[i], b = off[i + 1];
-        uint64_t len = b > a ? b - a : 0;
-        run += len == 0 ? 1u : static_cast<uint32_t>((len + seg - 1) / seg);
-    }
-    if (tid == 1023) task_off[count] = part[1023];
-    if (tid == 0) *work = 0;
-}
-
-template <class Step, bool VEC>
-__global__ void __launch_bounds__(kBatchWarps * 32)
-k_batch_scan(const BatchArgs a) {
-    using CP = Comp<Step, VEC>;
-    const int lane = threadIdx.x & 31;
-    Step S;
-    DevTables t = a.t;
-    S.params(t);
-    load_tables<Step>(t, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const uint32_t total = a.task_off[a.count];
-    for (;;) {
-        uint32_t task = 0;
-        if (lane == 0) task = atomicAdd(a.work, 1u);
-        task = __shfl_sync(kFull, task, 0);
-        if (task >= total) break;
-        // text of this task: last i with task_off[i] <= task
-        uint64_t lo = 0, hi = a.count;  // invariant: task_off[lo] <= task < task_off[hi]
-        while (hi - lo > 1) {
-            uint64_t mid = (lo + hi) / 2;
-            if (a.task_off[mid] <= task) lo = mid;
-            else hi = mid;
-        }
-        const uint64_t i = lo;
-        const uint32_t j = task - a.task_off[i];
-        const uint32_t ntasks = a.task_off[i + 1] - a.task_off[i];
-        const uint64_t t0 = a.off[i], t1 = max(t0, a.off[i + 1]);
-        const uint64_t s0 = min(t1, t0 + j * a.seg), s1 = min(t1, s0 + a.seg);
-        const uint64_t per = (((s1 - s0) + 31) / 32 + 31) & ~uint64_t(31);  // whole 32-B sectors per lane
-        const uint64_t p0 = min(s1, s0 + lane * per), p1 = min(s1, p0 + per);
-        uint32_t s;
-        if constexpr (Step::kFactor) {  // 32 bytes through the SFA table, then the factored step if all lanes allow
-            const uint64_t pm = min(p1, p0 + 32);
-            const uint32_t s0 = run_range(S, S.init(lane), a.texts, p0, pm);
-            uint32_t fam = 0, g = 0;
-            const bool ok = t.fact_fam && fact_from_id(t, S.id(s0, lane), fam, g);
-            if (__all_sync(kFull, ok)) {
-                StepDfa D;
-                D.params(t);
-                s = fact_to_id(t, fam, run_range32(D, g, a.texts, pm, p1));
-            } else {
-                s = S.id(run_range32(S, s0, a.texts, pm, p1), lane);
-            }
-        } else {
-            s = S.id(run_range32(S, S.init(lane), a.texts, p0, p1), lane);
-        }
-        const uint32_t val = CP::fold_states(S, t, s);
-        if (ntasks == 1) {
-            const uint32_t q = CP::q_final(t, val, 0);
-            if (lane == 0) a.results[i] = sfa_result{q, t.dfinal[q]};
-        } else if (VEC) {
-            a.seg_parts[static_cast<uint64_t>(task) * CP::kSlot + lane] = static_cast<uint8_t>(val);
-        } else if (lane == 0) {
-            reinterpret_cast<uint32_t*>(a.seg_parts)[task] = val;
-        }
-    }
-}
-
-template <class Step, bool VEC>
-__global__ void __launch_bounds__(kBatchWarps * 32)
-k_batch_combine(const BatchArgs a) {
-    using CP = Comp<Step, VEC>;
-    Step S;
-    DevTables t = a.t;
-    S.params(t);
-    load_tables<Step>(t, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t i = wid; i < a.count; i += nw) {
-        const uint32_t k0 = a.task_off[i], k1 = a.task_off[i + 1];
-        if (k1 - k0 <= 1) continue;
-        uint32_t acc = CP::fold_slots(S, t, a.seg_parts + static_cast<uint64_t>(k0) * CP::kSlot, k1 - k0,
-                                      CP::identity(), true);
-        const uint32_t q = CP::q_final(t, acc, 0);
-        if (lane == 0) a.results[i] = sfa_result{q, t.dfinal[q]};
-    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -708,7 +953,7 @@ cudaError_t ensure_smem(F kern, size_t smem) {
 
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while the previous kernel of the stream finishes; it calls pdl_wait()
-// before it touches state the previous kernel may still use.
+// before it touches the text or state the previous kernel may still use.
 template <class... KArgs, class... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
                        Args&&... args) {
@@ -741,82 +986,87 @@ inline EncodeFn encode_fn() {
     return fn;
 }
 
+// One 2-D u8 tensor map [rows x L] at `base` with a [rowb x bh] box, swizzle matched to rowb.
+inline cudaError_t encode_map(CUtensorMap* m, void* base, uint64_t L, uint64_t rows, uint32_t rowb, uint32_t bh, int promo) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {L, rows ? rows : 1};
+    cuuint64_t strides[1] = {L};
+    cuuint32_t box[2] = {rowb, bh ? bh : 8};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle swz = rowb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : rowb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    const CUtensorMapL2promotion pr = promo == 64    ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                    : promo == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     swz, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
-template <class Step, int K, int ROWB, bool VEC>
-cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
+// The host's maps for a host plan: the last encoding is reused when the
+// geometry repeats (repeated matches of one buffer: host overhead).
+inline cudaError_t host_maps(const ScanArgs& a, const TmaConfig& cfg, TmaMaps* out) {
+    struct Key {
+        const void* base;
+        uint64_t L, rows;
+        uint32_t bh, bl_hi, bl_lo, rowb;
+        int promo;
+        bool operator==(const Key& o) const {
+            return base == o.base && L == o.L && rows == o.rows && bh == o.bh && bl_hi == o.bl_hi && bl_lo == o.bl_lo &&
+                   rowb == o.rowb && promo == o.promo;
+        }
+    };
+    static thread_local Key last{nullptr, 0, 0, 0, 0, 0, 0, -9};
+    static thread_local TmaMaps maps;
+    const TmaPlan& P = a.plan;
+    void* base = const_cast<uint8_t*>(a.text + P.head);
+    if (P.nchunks == 0) base = reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(base) & ~uintptr_t(255));
+    const Key key{base, P.L, P.nchunks, P.bh, P.bl_hi, P.bl_lo, static_cast<uint32_t>(cfg.rowb), cfg.promo};
+    if (!(key == last)) {
+        last = Key{nullptr, 0, 0, 0, 0, 0, 0, -9};
+        cudaError_t e = encode_map(&maps.load, base, P.L, P.nchunks, cfg.rowb, P.bh, cfg.promo);
+        if (e == cudaSuccess) e = encode_map(&maps.last_hi, base, P.L, P.nchunks, cfg.rowb, P.bl_hi, cfg.promo);
+        if (e == cudaSuccess) e = encode_map(&maps.last_lo, base, P.L, P.nchunks, cfg.rowb, P.bl_lo, cfg.promo);
+        if (e != cudaSuccess) return e;
+        last = key;
+    }
+    *out = maps;
+    return cudaSuccess;
+}
+
+template <class Step, int K, int ROWB, bool VEC, bool SEG>
+cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t stream) {
     using Sh = TmaShape<K, ROWB>;
-    auto kern = k_scan_tma<Step, K, ROWB, VEC>;
+    auto kern = k_scan_tma<Step, K, ROWB, VEC, SEG>;
     const uint32_t tbytes = static_cast<uint32_t>(table_bytes<Step>(a.t) + a.t.aux_bytes);
     const uint32_t sbytes = cfg.staged ? Step::staged_bytes(a.t) : 0u;
     const size_t smem = tbytes + sbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
     cudaError_t e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    EncodeFn enc = encode_fn();
-    if (!enc) return cudaErrorNotSupported;
-    cuuint64_t dims[2] = {a.plan.L, a.plan.nchunks};
-    cuuint64_t strides[1] = {a.plan.L};
-    // Diagnostic only (results are wrong): SFA_DIAG_STRIDE=s overlaps the rows
-    // at stride s so the whole text the kernel reads is L2-resident, which
-    // times the compute side of the scan without HBM.
-    if (const char* ds = getenv("SFA_DIAG_STRIDE")) {
-        const long v = atol(ds);
-        if (v >= 16 && v % 16 == 0 && static_cast<uint64_t>(v) <= a.plan.L) strides[0] = static_cast<cuuint64_t>(v);
-    }
-    const cuuint32_t br = a.plan.rows_per_cta / Sh::NB;
-    if (br == 0 || br > 256 || br * Sh::NB != a.plan.rows_per_cta || br % 8) return cudaErrorInvalidValue;
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(ROWB), br};
-    cuuint32_t pbox[2] = {static_cast<cuuint32_t>(kLine), br};
-    cuuint32_t estr[2] = {1, 1};
-    void* base = const_cast<uint8_t*>(a.text + a.plan.head);
-    // The tensor maps depend only on (base, L, rows, box, promotion, prefetch):
-    // repeated matches of one buffer reuse the last encoding (host overhead).
-    struct Key {
-        void* base;
-        uint64_t L, rows, stride;
-        uint32_t br;
-        int promo, pf;
-        bool operator==(const Key& o) const {
-            return base == o.base && L == o.L && rows == o.rows && stride == o.stride && br == o.br && promo == o.promo &&
-                   pf == o.pf;
-        }
-    };
-    static thread_local Key last_key{nullptr, 0, 0, 0, 0, -1, -9};
-    static thread_local TmaMaps maps;
-    const Key key{base, a.plan.L, a.plan.nchunks, strides[0], br, cfg.promo, cfg.pf_lines};
-    if (key == last_key)
-        return launch_pdl(kern, a.plan.ctas, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring,
-                          cfg.pf_lines);
-    last_key = Key{nullptr, 0, 0, 0, 0, -1, -9};
-    const CUtensorMapSwizzle swz = ROWB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                 : ROWB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
-    const CUtensorMapL2promotion promo = cfg.promo == 0    ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                                       : cfg.promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                       : cfg.promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    CUresult r = enc(&maps.load, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    if (cfg.pf_lines >= 0) {  // the L2-prefetch map (off by default)
-        r = enc(&maps.pref, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, pbox, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    TmaMaps maps;
+    if (a.dplan) {
+        std::memset(&maps, 0, sizeof(maps));  // unused: the kernel reads a.gmaps
     } else {
-        maps.pref = maps.load;
+        const TmaPlan& P = a.plan;
+        for (uint32_t h : {P.bh, P.bl_hi, P.bl_lo})
+            if (P.nchunks && (h == 0 || h > 256 || h % 8)) return cudaErrorInvalidValue;
+        e = host_maps(a, cfg, &maps);
+        if (e != cudaSuccess) return e;
     }
-    last_key = key;
-    return launch_pdl(kern, a.plan.ctas, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring, cfg.pf_lines);
+    return launch_pdl(kern, grid, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring);
 }
 
-template <class Step, bool VEC>
-cudaError_t tma_launch(const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream) {
+template <class Step, bool VEC, bool SEG>
+cudaError_t tma_launch(const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t stream) {
     switch (cfg.K * 1000 + cfg.rowb) {
-        case 1016: return tma_launch_t<Step, 1, 16, VEC>(a, cfg, stream);
-        case 1032: return tma_launch_t<Step, 1, 32, VEC>(a, cfg, stream);
-        case 2016: return tma_launch_t<Step, 2, 16, VEC>(a, cfg, stream);
-        case 2032: return tma_launch_t<Step, 2, 32, VEC>(a, cfg, stream);
-        case 1064: return tma_launch_t<Step, 1, 64, VEC>(a, cfg, stream);
-        case 2064: return tma_launch_t<Step, 2, 64, VEC>(a, cfg, stream);
+        case 1016: return tma_launch_t<Step, 1, 16, VEC, SEG>(a, cfg, grid, stream);
+        case 1032: return tma_launch_t<Step, 1, 32, VEC, SEG>(a, cfg, grid, stream);
+        case 2016: return tma_launch_t<Step, 2, 16, VEC, SEG>(a, cfg, grid, stream);
+        case 2032: return tma_launch_t<Step, 2, 32, VEC, SEG>(a, cfg, grid, stream);
+        case 1064: return tma_launch_t<Step, 1, 64, VEC, SEG>(a, cfg, grid, stream);
+        case 2064: return tma_launch_t<Step, 2, 64, VEC, SEG>(a, cfg, grid, stream);
     }
     return cudaErrorInvalidValue;
 }
@@ -831,39 +1081,24 @@ cudaError_t direct_launch(const DirectArgs& a, cudaStream_t stream) {
     return launch_pdl(kern, static_cast<unsigned>(ctas), kDirectWarps * 32, smem, stream, a);
 }
 
-template <class Step, bool VEC>
-cudaError_t batch_launch(const BatchArgs& a, int sm_count, cudaStream_t stream) {
-    const size_t smem = table_bytes<Step>(a.t) + a.t.aux_bytes;
-    auto scan = k_batch_scan<Step, VEC>;
-    auto comb = k_batch_combine<Step, VEC>;
-    cudaError_t e = ensure_smem(scan, smem);
-    if (e != cudaSuccess) return e;
-    e = ensure_smem(comb, smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan, kBatchWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    k_batch_plan<<<1, 1024, 0, stream>>>(a.off, a.count, a.seg, a.task_off, a.work);
-    scan<<<sm_count * per_sm, kBatchWarps * 32, smem, stream>>>(a);
-    comb<<<sm_count, kBatchWarps * 32, smem, stream>>>(a);
-    return cudaGetLastError();
-}
-
 }  // namespace detail
 
-// One step policy's launchers (defined in kernels_<step>.cu).
+// One step policy's launchers: single-text kernels in kernels_<step>.cu, the
+// batch (SEG) kernels in kernels_<step>_seg.cu.
 #define SFA_DEFINE_STEP_LAUNCHERS(STEP)                                                                      \
     template <>                                                                                              \
     cudaError_t StepLaunch<STEP>::scan_tma(bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t s) { \
-        return vec ? detail::tma_launch<STEP, true>(a, cfg, s) : detail::tma_launch<STEP, false>(a, cfg, s); \
+        return vec ? detail::tma_launch<STEP, true, false>(a, cfg, a.plan.ctas, s)                          \
+                   : detail::tma_launch<STEP, false, false>(a, cfg, a.plan.ctas, s);                        \
     }                                                                                                        \
     template <>                                                                                              \
     cudaError_t StepLaunch<STEP>::scan_direct(bool vec, const DirectArgs& a, cudaStream_t s) {               \
         return vec ? detail::direct_launch<STEP, true>(a, s) : detail::direct_launch<STEP, false>(a, s);     \
-    }                                                                                                        \
+    }
+#define SFA_DEFINE_STEP_SEG_LAUNCHER(STEP)                                                                   \
     template <>                                                                                              \
-    cudaError_t StepLaunch<STEP>::batch(bool vec, const BatchArgs& a, int sm, cudaStream_t s) {              \
-        return vec ? detail::batch_launch<STEP, true>(a, sm, s) : detail::batch_launch<STEP, false>(a, sm, s); \
+    cudaError_t StepLaunch<STEP>::scan_seg(const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t s) { \
+        return detail::tma_launch<STEP, false, true>(a, cfg, grid, s);                                       \
     }
 
 }  // namespace sfa

@@ -1,0 +1,7 @@
+// kernels_shared_seg.cu -- instantiates the batch (SEG) scan kernels for StepShared
+// (one translation unit per step policy and mode so the library builds in parallel).
+#include "kernels_impl.cuh"
+
+namespace sfa {
+SFA_DEFINE_STEP_SEG_LAUNCHER(StepShared)
+}  // namespace sfa

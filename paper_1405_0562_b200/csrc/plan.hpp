@@ -79,20 +79,96 @@ struct Scratch {
     uint32_t max_ctas = 0;         // slots available in partials (excluding the tail slot)
 };
 
-// Single-text scan through the TMA pipeline.  The text [0, n) is cut into
+// The TMA scan's cut of a byte range [0, n) (one text, or a batch's texts
+// back to back):
 //   head  [0, head)                           < 256 bytes, up to 256-B alignment
 //   rows  [head + r*L, head + (r+1)*L), r < nchunks   (the 2-D TMA tensor;
-//         L a multiple of 256, so each row's 256-B L2 lines are whole)
-//   tail  [tail_start, n)                     < L bytes
-// CTA b runs rows [b*rows_per_cta, (b+1)*rows_per_cta).
+//         L a multiple of 64 and >= 256)
+//   tail  [tail_start, n)                     the rest (< 8 L bytes)
 // Every piece is a chunk of Alg. 5 (any division, Theorem 3).
+// Rows are split over the CTAs so that every SM scans nearly the same number
+// (the launch lasts as long as its busiest CTA): the first m CTAs get rc_hi
+// rows, the others rc_lo = rc_hi - 8, rc_hi = the average rounded up to 8.  A
+// CTA loads its rows as NB TMA boxes per stage: NB - 1 boxes of bh rows and a
+// last box of bl_hi or bl_lo rows (heights multiples of 8, the swizzle
+// atom).  When no such split exists (few rows) every CTA gets rc_hi = NB * bh
+// rows (rc_lo = rc_hi, m = ctas) and the last CTA's rows past nchunks are
+// TMA zero fill.
 struct TmaPlan {
+    uint64_t n = 0;
     uint64_t head = 0;
-    uint64_t L = 0;           // row length, multiple of 16
-    uint32_t nchunks = 0;     // rows
-    uint32_t ctas = 0;
-    uint32_t rows_per_cta = 0;
-    uint64_t tail_start = 0;  // head + nchunks * L
+    uint64_t L = 0;            // row length
+    uint32_t nchunks = 0;      // rows
+    uint32_t ctas = 0;         // CTAs that own rows (the launch may have more)
+    uint32_t rc_hi = 0, rc_lo = 0, m = 0;
+    uint32_t bh = 0, bl_hi = 0, bl_lo = 0;
+    uint64_t tail_start = 0;   // head + nchunks * L
+    uint64_t len = 0;          // batch of equal texts: their length (0: offsets / one text)
+    __host__ __device__ uint32_t cta_rows(uint32_t b) const { return b < m ? rc_hi : (b < ctas ? rc_lo : 0u); }
+    __host__ __device__ uint64_t cta_row0(uint32_t b) const {
+        return b < m ? static_cast<uint64_t>(b) * rc_hi : static_cast<uint64_t>(m) * rc_hi + static_cast<uint64_t>(b - m) * rc_lo;
+    }
 };
+
+// The plan of a TMA scan of n bytes starting at device address `addr` on G
+// CTAs of at most R rows (NB boxes per stage, rowb bytes per row per stage).
+// row_align: 0 = choose (256/128/64 B, the fewest idle compute rows after a
+// measured DRAM cost of 64-B rows), else force.  Host and device (the batch
+// plan kernel runs it on the GPU).
+__host__ __device__ inline void make_plan(uint64_t addr, uint64_t n, uint32_t G, uint32_t R, uint32_t NB, uint32_t rowb,
+                                          uint32_t row_align, TmaPlan* p) {
+    *p = TmaPlan{};
+    p->n = n;
+    uint64_t head = (256 - (addr & 255)) & 255;
+    if (head > n) head = n;
+    const uint64_t body = n - head;
+    const uint64_t GR = static_cast<uint64_t>(G) * R;
+    uint64_t L = 256;
+    double best = -1;
+    const uint64_t cand[3] = {256, 128, 64};
+    for (int ci = 0; ci < 3; ++ci) {
+        if (row_align && ci) break;
+        uint64_t al = row_align ? row_align : cand[ci];
+        if (al < rowb) al = rowb;
+        uint64_t Lc = al * ((body + al * GR - 1) / (al * GR));
+        if (Lc < 256) Lc = 256;
+        const double used = static_cast<double>(body / Lc) / static_cast<double>(GR);
+        const double score = used * (al >= 128 ? 1.0 : 0.977);
+        if (score > best + 1e-9) {
+            best = score;
+            L = Lc;
+        }
+    }
+    p->head = head;
+    p->L = L;
+    p->tail_start = head;
+    const uint64_t rows = body / L;
+    if (rows == 0) return;
+    uint64_t used = rows;
+    // rc_hi = ceil(rows / G) rounded up to 8; NB - 1 boxes of bh rows and a
+    // last box of rc_hi - (NB-1) bh >= 16 rows (so rc_lo's last box keeps >= 8)
+    const uint32_t hi = static_cast<uint32_t>(8 * ((rows + 8ull * G - 1) / (8ull * G)));
+    const uint32_t bh = 8 * ((hi + 8 * NB - 1) / (8 * NB));
+    if (hi <= R && bh <= 256 && hi >= (NB - 1) * bh + 16) {
+        p->rc_hi = hi;
+        p->rc_lo = hi - 8;
+        p->bh = bh;
+        p->bl_hi = hi - (NB - 1) * bh;
+        p->bl_lo = p->bl_hi - 8;
+        const uint64_t mm = (rows - static_cast<uint64_t>(p->rc_lo) * G) / 8;  // rows/G in (hi - 8, hi]
+        p->m = static_cast<uint32_t>(mm < G ? mm : G);
+        p->ctas = G;
+        used = static_cast<uint64_t>(p->rc_lo) * G + 8ull * p->m;
+    } else {  // few rows: equal CTAs of NB whole boxes
+        const uint32_t gran = 8 * NB;
+        const uint32_t rc = static_cast<uint32_t>(gran * ((rows + static_cast<uint64_t>(gran) * G - 1) / (static_cast<uint64_t>(gran) * G)));
+        p->rc_hi = p->rc_lo = rc;
+        p->bh = p->bl_hi = p->bl_lo = rc / NB;
+        p->ctas = static_cast<uint32_t>((rows + rc - 1) / rc);
+        p->m = p->ctas;
+    }
+    p->nchunks = static_cast<uint32_t>(used);
+    p->tail_start = head + used * L;
+}
 
 }  // namespace sfa

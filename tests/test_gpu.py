@@ -233,22 +233,20 @@ def test_batch_count_zero_is_noop(torch_cuda):
 
 
 # --------------------------------------------------------------------------- residency modes
-@pytest.mark.parametrize("factor", ["1", "0"])
-@pytest.mark.parametrize("hot_rows", [None, "7"])
+@pytest.mark.parametrize("factor", [1, 0])
+@pytest.mark.parametrize("hot_rows", [0, 7])
 @pytest.mark.parametrize("rx,alpha,modes", [(*CFG1, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
                                             (*CFG2, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
-                                            (*CFG4, (P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
+                                            (*CFG4, (P.RES_SMEM_PRIVATE, P.RES_SMEM_SHARED, P.RES_HOT_L2, P.RES_L2)),
                                             (W.cfg3_regex(), None, (P.RES_HOT_L2, P.RES_L2))])
-def test_every_residency_mode(torch_cuda, rx, alpha, modes, hot_rows, factor, monkeypatch):
-    """A6: every table placement gives the oracle's result; hot_rows='7'
-    keeps only 7 renumbered rows in smem so nearly every HOT lookup takes the
-    global (L2) path."""
-    if hot_rows:
-        monkeypatch.setenv("SFA_HOT_ROWS", hot_rows)
-    monkeypatch.setenv("SFA_FACTOR", factor)   # read when the handle is created below
+def test_every_residency_mode(torch_cuda, rx, alpha, modes, hot_rows, factor):
+    """A6: every table placement gives the oracle's result; hot_rows=7 keeps
+    only 7 renumbered rows in smem so nearly every HOT lookup takes the
+    global (L2) path; factor=0 disables the FACTORED step."""
     torch = torch_cuda
     d = oracle_pair(rx, alpha)
     sfa = P.SFA(rx, alpha)
+    sfa.set_tuning(hot_rows=hot_rows, no_factor=1 - factor)
     rng = np.random.default_rng(6)
     al = np.frombuffer(alpha if alpha else b"abcdefghijklmnopqrstuvwxyz", np.uint8)
     texts = [al[rng.integers(0, al.size, size=n)] for n in (1, 1000, 5_000_000)]
@@ -335,21 +333,29 @@ def test_match_host_replay_mode(torch_cuda):
 
 # --------------------------------------------------------------------------- every TMA pipeline shape
 @pytest.mark.parametrize("shape", ["1,16,0", "1,32,0", "2,16,0", "2,32,0", "1,64,0", "1,16,2", "2,16,2",
-                                   "1,32,3", "1,32,0,-1,256", "1,64,0,0,128", "2,32,0,-1,0"])
-def test_every_tma_shape(torch_cuda, shape, monkeypatch):
-    """k_scan_tma for each (K chunks/thread, bytes/row/stage, ring depth) the
-    launcher can pick (SFA_TMA_CONFIG forces one), on texts spanning several
-    rows per thread and ragged tails."""
+                                   "1,32,3", "1,32,0,256", "1,64,0,128", "2,32,0,0"])
+def test_every_tma_shape(torch_cuda, shape):
+    """k_scan_tma for each (K chunks/thread, bytes/row/stage, ring depth, L2
+    promotion) the launcher can pick (sfa_set_tuning forces one), on texts
+    spanning several rows per thread and ragged tails, and a batch."""
     torch = torch_cuda
-    monkeypatch.setenv("SFA_TMA_CONFIG", shape)
+    v = [int(x) for x in shape.split(",")]
+    knobs = dict(tma_k=v[0], tma_rowb=v[1], tma_ring=v[2])
+    if len(v) > 3:
+        knobs["tma_promo"] = v[3]
     for rx, alpha, text in [(*CFG2, W.cfg2_accepted(2_000_000)), (*CFG1, W.cfg1_accepted(5_000_000)),
                             (*CFG4, W.cfg4_text(20_000_000))]:
         d = oracle_pair(rx, alpha)
         sfa = P.SFA(rx, alpha)
+        sfa.set_tuning(**knobs)
         for n in (text.size, text.size - 1, 4_200_001, 9_999_937):
             t = text[:n]
             for pad in (0, 5):
                 check_text(torch, sfa, d, t, pad)
+        texts, off = W.ragged_batch(17, 300, 60_000, alpha)
+        q, acc = _batch(torch, sfa, texts, off)
+        qo, ao = d.run_batch(texts, off)
+        assert (q == qo).all() and (acc == ao).all(), shape
 
 
 # --------------------------------------------------------------------------- every composition mode
