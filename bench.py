@@ -1,31 +1,47 @@
 """bench.py -- GB/s of text matched on B200 (SFA run + composition), % of roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference] [--all]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
 A step is one pass of the whole hot path (Alg. 5 of PAPER.md:552-576: byte ->
 column, chunk runs from f_I, composition f_1 . ... . f_p, finalisation) over
-one text of the workload, through the C-ABI (``sfa_match_async``), with the
-text already resident in HBM.  Default workload: BASELINE.json configs[1]
-(config 2: ``([0-4]{5}[5-9]{5})*`` over a 268,435,450-byte accepted text).
-The text (256 MiB) is larger than the 126 MB L2, so no flush is needed between
-steps.  ``--all`` adds per-config numbers for configs 1, 3, 4 and 5; ``--spec``
-adds the paper's baseline (Alg. 3, speculative DFA) timed on the same texts;
-``--rn`` runs the paper's r_n scalability family (1 GiB accepted texts).
+one batch of the workload through the C-ABI, inputs resident in HBM.
 
-Multi-GPU (torchrun): every rank matches its own copy of the workload (the
-texts are independent problems; no data-path collective), weak scaling;
-value = all ranks' bytes / the max over ranks of the device time.
+Default workload (the headline): BASELINE.json configs[4] = cfg5, the largest
+single-GPU configuration -- cfg3's 32-word contains-match DFA over 65,536
+texts of 64 KiB (4 GiB) -- through north_star's ``sfa_match_batch`` (device
+offsets; one k_batch_plan + one segmented k_scan_tma launch per step).  The
+texts (4 GiB) are far larger than the 126 MB L2, so no flush is needed.
 
-``--impl reference``: there is no reference implementation (the paper ships
-no code); the reference arm is the CPU oracle (Alg. 2, sequential DFA run,
-oracle/) timed on the host cores on a bounded sample of the same workload.
+Beside it, on rank 0:
+  * ``uniform_api``: the same batch through ``sfa_match_batch_uniform`` (host
+    plan: the scan kernel alone);
+  * ``per_config``: cfg2 (256 MiB), cfg3 and cfg4 (1 GiB) through
+    ``sfa_match_async``, each with its roofline, the back-to-back step time
+    (mean and median of the per-step events) and the single-launch time
+    (launch to result, synchronised before each launch, median of >= 10);
+  * ``single_launch`` of the headline itself;
+  * ``cpu_baseline``: the oracle (Alg. 2, oracle/) on a bounded sample of the
+    same workload on one host core, with nproc and the CPU model;
+  * ``e2e``: the same batch end to end from pinned host memory through
+    ``sfa_match_batch_host`` (H2D of texts and offsets, D2H of the results in
+    the timed region).
+``--spec`` adds the paper's baseline (Alg. 3) on cfg2-4; ``--rn`` the r_n
+family; ``--shard`` one text over the ranks.
+
+Multi-GPU (torchrun): every rank matches its own copy of the workload
+(independent problems, no data-path collective), weak scaling; value = all
+ranks' bytes / the max over ranks of the device time.
+
+``--impl reference``: there is no reference implementation (the paper ships no
+code); the reference arm is the CPU oracle (Alg. 2, oracle/) timed on the host
+cores on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
-import subprocess
+import statistics
 import sys
 import threading
 import time
@@ -37,17 +53,19 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GB/s of text matched on 1 B200 (SFA run + composition); % of roofline"
 UNIT = "GB/s"
+HBM_SPEC_GBS = 8000.0
 CONFIG_NAMES = {
     1: "cfg1: (ab|ba)*c over {a,b,c}, 1 MiB accepted text",
     2: "cfg2: ([0-4]{5}[5-9]{5})* over digits, 268,435,450-byte accepted text",
     3: "cfg3: .*(w1|...|w32).* over all bytes, 1 GiB scrubbed a-z text, one planted word",
     4: "cfg4: .*a[ab]{8} over {a,b}, 1 GiB i.i.d. text",
-    5: "cfg5: cfg3's DFA, batch of 65,536 x 64 KiB texts (4 GiB), 10% planted",
+    5: "cfg5: cfg3's DFA, batch of 65,536 x 64 KiB texts (4 GiB), 10% planted, through sfa_match_batch",
 }
+EXPECTED = {1: (3, True), 2: (0, True)}
 
 
 def workload(cfg: int):
-    """(regex, alphabet, text or (texts, offsets)) of a BASELINE.json config."""
+    """(regex, alphabet, text or (texts, offsets, planted)) of a BASELINE.json config."""
     import workloads as W
     if cfg == 1:
         return W.REGEX[1], W.ALPHABET[1], W.cfg1_accepted()
@@ -58,8 +76,7 @@ def workload(cfg: int):
     if cfg == 4:
         return W.REGEX[4], W.ALPHABET[4], W.cfg4_text()
     if cfg == 5:
-        t, off, _ = W.cfg5_batch()
-        return W.cfg3_regex(), None, (t, off)
+        return W.cfg3_regex(), None, W.cfg5_batch()
     raise ValueError(cfg)
 
 
@@ -73,58 +90,68 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)", {}
 
 
+def host_info():
+    model = "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons, sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled through NVML every ~2 ms while the
+    timed region runs (an nvidia-smi loop is too coarse for a ~0.1 s region)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.reasons, self.mx = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.hdl = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(self.hdl, N.NVML_CLOCK_SM))
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(self.hdl, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.hdl)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.ok:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "NVML, 2 ms period, during the timed region"}
 
 
 def dist_setup():
@@ -134,15 +161,94 @@ def dist_setup():
     return world, rank, local
 
 
-def ncu_traffic(cfg: int):
+def ncu_traffic(key: str):
     """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(f"cfg{cfg}", {}).get("dram_bytes_per_launch")
+        return d.get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+# --------------------------------------------------------------------------- timing
+def steady(torch, fn, stream, steps, warmup):
+    """K back-to-back steps on `stream`: (mean ms over the bracketing events, median of per-step events)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        fn()
+        ev[i + 1].record(stream)
+    ev[-1].synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[-1]) / steps, statistics.median(per)
+
+
+def single(torch, fn, stream, reps):
+    """Launch-to-result device time of one isolated call (the device idle before
+    it: no overlap with a previous launch), median of `reps`."""
+    out = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return statistics.median(out)
+
+
+def smem_peaks(nsm, sm_mhz):
+    """Shared-memory ceilings: one conflict-free LDS wavefront per
+    32 lookups -> 32 B/clk/SM; with the staged text (TMA write + LDS.128 read,
+    1/128 wavefront each per byte) -> 21.33 B/clk/SM."""
+    hz = sm_mhz * 1e6
+    return nsm * 32 * hz / 1e9, nsm * (1.0 / (1 / 32 + 2 / 128)) * hz / 1e9
+
+
+def roofline(gbs, peak, peak_kind, nsm, sm_mhz, kernel, traffic, per_launch_bytes):
+    lk, dp = smem_peaks(nsm, sm_mhz)
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "traffic": traffic, "traffic_source": "profiles/ncu_summary.json (ncu --set full of the same kernel)",
+            "algorithmic_bytes_per_launch": per_launch_bytes,
+            "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+            "frac_of_spec_8tbs": gbs / HBM_SPEC_GBS, "kernel": kernel,
+            "smem_lookup_peak_gbs": lk, "smem_datapath_peak_gbs": dp, "sm_mhz_for_smem_peaks": sm_mhz,
+            "frac_of_min_roofline": gbs / min(peak, lk), "frac_of_min_datapath": gbs / min(peak, dp)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def cpu_sample(cfg, rx, alpha, text, budget_s):
+    """The oracle (Alg. 2) on a bounded sample of the workload, one host core."""
+    import oracle as O
+    d = O.OracleDFA(rx, alpha)
+    if cfg == 5:
+        texts, off, _ = text
+        k = 1024                                            # 64 MiB: the first 1,024 texts
+        sample, soff = texts[: int(off[k])], off[: k + 1].copy()
+        run = lambda: d.run_batch(sample, soff)           # noqa: E731
+        what = f"the first {k} texts ({sample.size} bytes) of the cfg5 batch"
+    else:
+        sample = text[: min(text.size, 64 << 20)]
+        run = lambda: d.run(sample)                        # noqa: E731
+        what = f"the first {sample.size} bytes of the cfg{cfg} text"
+    run()
+    done, passes, t0 = 0, 0, time.perf_counter()
+    while True:
+        run()
+        done += sample.size
+        passes += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    el = time.perf_counter() - t0
+    nproc, model = host_info()
+    return {"value": done / el / 1e9, "unit": UNIT, "cores": 1, "nproc": nproc, "cpu_model": model, "kind": "oracle",
+            "sample": f"{passes} passes over {what} ({el:.1f} s), Alg. 2 byte-at-a-time, single thread"}
 
 
 def run_reference(args, world, rank):
@@ -153,99 +259,49 @@ def run_reference(args, world, rank):
     cfg = args.config
     rx, alpha, text = workload(cfg)
     d = O.OracleDFA(rx, alpha)
-    sample = text[: min(text.size, args.ref_bytes)]
+    if cfg == 5:
+        texts, off, _ = text
+        k = max(1, min(off.size - 1, args.ref_bytes // int(off[1] - off[0])))
+        sample, soff = texts[: int(off[k])], off[: k + 1].copy()
+        run = lambda: d.run_batch(sample, soff)   # noqa: E731
+        what = f"the first {k} texts ({sample.size} bytes) of the cfg5 batch per step"
+        nbytes = sample.size
+    else:
+        sample = text[: min(text.size, args.ref_bytes)]
+        run = lambda: d.run(sample)               # noqa: E731
+        what = f"the first {sample.size} bytes of the cfg{cfg} text per step"
+        nbytes = sample.size
     for _ in range(args.warmup):
-        d.run(sample[: 1 << 20])
+        run()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        d.run(sample)
+        run()
         times.append(time.perf_counter() - t0)
     tot = sum(times)
-    gbs = sample.size * len(times) / tot / 1e9
+    gbs = nbytes * len(times) / tot / 1e9
+    nproc, model = host_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded, DESIGN.md input recipe)",
-        "config": {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(sample.size)},
-        "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"first {sample.size} bytes of the config-{cfg} text per step, "
-                                   f"Alg. 2 byte-at-a-time (oracle/oracle.c)"},
+        "config": {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(nbytes)},
+        "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": 1, "nproc": nproc, "cpu_model": model, "kind": "oracle",
+                         "sample": f"{what}, Alg. 2 byte-at-a-time (oracle/oracle.c)"},
         "e2e": {"value": gbs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, rx, alpha, text, budget_s):
-    import oracle as O
-    d = O.OracleDFA(rx, alpha)
-    sample = text[: min(text.size, 64 << 20)]
-    d.run(sample[: 1 << 20])
-    done, t0 = 0, time.perf_counter()
-    passes = 0
-    while True:
-        d.run(sample)
-        done += sample.size
-        passes += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    el = time.perf_counter() - t0
-    return {"value": done / el / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{passes} passes over the first {sample.size} bytes of the config-{cfg} text "
-                      f"({el:.1f} s), Alg. 2 byte-at-a-time, single thread"}
-
-
-def time_single(torch, P, sfa, dtext, stream, steps, warmup, res):
-    for _ in range(warmup):
-        sfa.match_async(dtext, res, stream)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        sfa.match_async(dtext, res, stream)
-    e1.record(stream)
-    e1.synchronize()
-    return e0.elapsed_time(e1) / steps  # ms
-
-
-def time_batch(torch, P, sfa, dtexts, doff, count, stream, steps, warmup, res):
-    for _ in range(warmup):
-        sfa.match_batch(dtexts, doff, count, res, stream)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        sfa.match_batch(dtexts, doff, count, res, stream)
-    e1.record(stream)
-    e1.synchronize()
-    return e0.elapsed_time(e1) / steps
-
-
-def time_spec(torch, sfa, dtext, stream, steps, warmup, res):
-    """The paper's baseline, Alg. 3 (speculative DFA, |D| lookups per byte) on the same text."""
-    for _ in range(warmup):
-        sfa.match_speculative(dtext, res, 0, None, stream)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        sfa.match_speculative(dtext, res, 0, None, stream)
-    e1.record(stream)
-    e1.synchronize()
-    return e0.elapsed_time(e1) / steps
-
-
+# --------------------------------------------------------------------------- per-config (single texts)
 def spec_compare(torch, sfa, dtext, nbytes, sfa_ms, stream, warmup, expected):
     """Alg. 3 beside the SFA on one text: GB/s, lookups per byte, and the SFA's speedup."""
     res = torch.zeros(2, dtype=torch.int32, device="cuda")
     nd = sfa.info()["dfa_states"]
-    # ~0.5 s of work at most: the speculative run does |D| lookups per byte
     steps = max(1, min(50, int(0.5 / max(1e-6, nbytes * nd / 5e12))))
-    ms = time_spec(torch, sfa, dtext, stream, steps, min(warmup, 3), res)
+    fn = lambda: sfa.match_speculative(dtext, res, 0, None, stream)  # noqa: E731
+    ms, med = steady(torch, fn, stream, steps, min(warmup, 3))
     got = tuple(int(x) for x in res.cpu().numpy().view(np.uint32))
     if expected is not None and got != (expected[0], int(expected[1])):
         raise SystemExit(f"speculative result {got} != {expected}")
@@ -253,6 +309,36 @@ def spec_compare(torch, sfa, dtext, nbytes, sfa_ms, stream, warmup, expected):
     return {"value": gbs, "unit": UNIT, "ms_per_step": ms, "steps": steps, "lookups_per_byte": nd,
             "lookups_per_s": gbs * 1e9 * nd, "sfa_speedup": ms / sfa_ms,
             "kernel": "k_spec_scan (Alg. 3, PAPER.md:293-328: the DFA from every state per chunk)"}
+
+
+def single_text_config(torch, P, cfg, stream, steps, warmup, reps, peak, peak_kind, nsm, sm_mhz, spec=False,
+                       text_in=None):
+    rx, alpha, text = workload(cfg) if text_in is None else text_in
+    sfa = P.SFA(rx, alpha)
+    dt = torch.from_numpy(text).cuda()
+    res = torch.zeros(2, dtype=torch.int32, device="cuda")
+    q, acc = sfa.match(dt, stream)
+    if cfg in EXPECTED and (q, acc) != EXPECTED[cfg]:
+        raise SystemExit(f"cfg{cfg}: wrong result {(q, acc)}")
+    fn = lambda: sfa.match_async(dt, res, stream)  # noqa: E731
+    ms, med = steady(torch, fn, stream, steps, warmup)
+    one = single(torch, fn, stream, reps)
+    n = text.size
+    gbs = n / (ms * 1e-3) / 1e9
+    info = sfa.info()
+    out = {"workload": CONFIG_NAMES[cfg], "bytes": int(n), "result": [q, bool(acc)],
+           "value": gbs, "unit": UNIT, "ms_per_step": ms, "median_ms_per_step": med, "steps": steps,
+           "single_launch": {"ms": one, "gbs": n / (one * 1e-3) / 1e9, "frac": n / (one * 1e-3) / 1e9 / peak,
+                             "reps": reps, "how": "synchronised before each launch; launch-to-result events; median"},
+           "roofline": roofline(gbs, peak, peak_kind, nsm, sm_mhz, "k_scan_tma (one launch per step)",
+                                ncu_traffic(f"cfg{cfg}"), int(n)),
+           "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
+           "dfa_states": info["dfa_states"], "api": "sfa_match_async", "gpu_launches_per_step": 1}
+    if spec:
+        out["alg3_speculative"] = spec_compare(torch, sfa, dt, n, ms, stream, warmup, (q, acc))
+    del dt
+    sfa.close()
+    return out
 
 
 def rn_family(torch, P, stream, warmup, peak, nbytes):
@@ -271,8 +357,8 @@ def rn_family(torch, P, stream, warmup, peak, nbytes):
         q, acc = sfa.match(dt, stream)
         if not acc:
             raise SystemExit(f"{name}: the accepted text was rejected ({q})")
-        steps = 50
-        ms = time_single(torch, P, sfa, dt, stream, steps, warmup, res)
+        fn = lambda: sfa.match_async(dt, res, stream)  # noqa: E731
+        ms, _ = steady(torch, fn, stream, 50, warmup)
         gbs = text.size / (ms * 1e-3) / 1e9
         info = sfa.info()
         out[name] = {"regex": rx, "bytes": int(text.size), "dfa_states": info["dfa_states"],
@@ -284,52 +370,98 @@ def rn_family(torch, P, stream, warmup, peak, nbytes):
     return out
 
 
-def extra_config(torch, P, cfg, stream, steps, warmup, peak, spec=False):
-    rx, alpha, text = workload(cfg)
+# --------------------------------------------------------------------------- headline: a batch
+def bench_batch(args, torch, P, stream, world, rank, local, peak, peak_kind, nsm):
+    rx, alpha, (texts, off, planted) = workload(5)
+    count = off.size - 1
     sfa = P.SFA(rx, alpha)
-    if cfg == 5:
-        texts, off = text
+    with torch.cuda.stream(stream):
         dt = torch.from_numpy(texts).cuda()
         do = torch.from_numpy(off.astype(np.int64)).cuda()
-        count = off.size - 1
         res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
-        ms_off = time_batch(torch, P, sfa, dt, do, count, stream, steps, warmup, res)
-        length = int(off[1] - off[0])
-        for _ in range(warmup):
-            sfa.match_batch_uniform(dt, length, count, res, stream)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
-            sfa.match_batch_uniform(dt, length, count, res, stream)
-        e1.record(stream)
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / steps
-        nbytes = texts.size
-    else:
-        dt = torch.from_numpy(text).cuda()
-        res = torch.zeros(2, dtype=torch.int32, device="cuda")
-        ms = time_single(torch, P, sfa, dt, stream, steps, warmup, res)
-        nbytes = text.size
-    gbs = nbytes / (ms * 1e-3) / 1e9
+    torch.cuda.synchronize()
+    fn = lambda: sfa.match_batch(dt, do, count, res, stream)  # noqa: E731
+    fn()
+    torch.cuda.synchronize()
+    r = res.view(count, 2).cpu().numpy().view(np.uint32)
+    acc_idx = np.flatnonzero(r[:, 1])
+    if acc_idx.tolist() != planted.tolist():              # exact: the planted texts and no other
+        raise SystemExit("cfg5: the accepted texts are not exactly the planted ones")
+    ref = res.clone()
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            fn()
+            ev[i + 1].record(stream)
+        ev[-1].synchronize()
+    torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    if not torch.equal(ref, res):
+        raise SystemExit("cfg5: results changed between steps")
+    ms_per_step = ms / args.steps
+    n = texts.size
+    per_rank_gbs = n / (ms_per_step * 1e-3) / 1e9
+    extra = {}
+    if rank == 0:
+        one = single(torch, fn, stream, args.single_reps)
+        extra["single_launch"] = {"ms": one, "gbs": n / (one * 1e-3) / 1e9, "frac": n / (one * 1e-3) / 1e9 / peak,
+                                  "reps": args.single_reps,
+                                  "how": "synchronised before each call (k_batch_plan + k_scan_tma); median"}
+        ufn = lambda: sfa.match_batch_uniform(dt, int(off[1] - off[0]), count, res, stream)  # noqa: E731
+        ums, umed = steady(torch, ufn, stream, max(5, args.steps // 2), 3)
+        if not torch.equal(ref, res):
+            raise SystemExit("cfg5: sfa_match_batch_uniform differs from sfa_match_batch")
+        extra["uniform_api"] = {"api": "sfa_match_batch_uniform (host plan; the scan kernel alone)",
+                                "value": n / (ums * 1e-3) / 1e9, "ms_per_step": ums, "median_ms_per_step": umed}
+        # end to end from pinned host memory through the library's host call
+        if args.e2e_steps > 0:
+            htexts = torch.from_numpy(texts).pin_memory()
+            hoff = torch.from_numpy(off.view(np.int64)).pin_memory()
+            hres = torch.zeros(2 * count, dtype=torch.int32).pin_memory()
+            sfa.match_batch_host(htexts, hoff, count, hres, stream)
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                sfa.match_batch_host(htexts, hoff, count, hres, stream)
+            e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+            if not torch.equal(hres, ref.cpu()):
+                raise SystemExit("cfg5: sfa_match_batch_host differs")
+            extra["e2e"] = {"value": world * n / e2e_s / 1e9, "unit": UNIT,
+                            "h2d_bytes_per_step": int(n + off.nbytes), "d2h_bytes_per_step": int(8 * count),
+                            "api": "sfa_match_batch_host (pinned host texts/offsets; slices of whole texts copied "
+                                   "on a copy stream while the previous slice is matched; results read back)",
+                            "timer": "host wall clock around the blocking call", "steps": args.e2e_steps}
     info = sfa.info()
-    out = {"workload": CONFIG_NAMES[cfg], "value": gbs, "unit": UNIT, "ms_per_step": ms, "bytes": int(nbytes),
-           "roofline_frac": gbs / peak, "residency": P.RES_NAMES.get(info["residency"], "?"),
-           "sfa_states": info["sfa_states"], "dfa_states": info["dfa_states"]}
-    if cfg == 5:
-        out["api"] = "sfa_match_batch_uniform"
-        out["offsets_api_gbs"] = nbytes / (ms_off * 1e-3) / 1e9
-    elif spec:
-        q, acc = sfa.match(dt, stream)
-        out["alg3_speculative"] = spec_compare(torch, sfa, dt, nbytes, ms, stream, warmup, (q, acc))
-    return out
+    med = statistics.median(per)
+    return sfa, dt, {
+        "value": world * per_rank_gbs, "ms_per_step": ms_per_step, "per_rank_gbs": per_rank_gbs,
+        "median_ms_per_step": med, "clocks": clk.summary(), "bytes": n, "count": count,
+        "accepted": int(acc_idx.size), "residency": P.RES_NAMES.get(info["residency"], "?"),
+        "sfa_states": info["sfa_states"], "dfa_states": info["dfa_states"], "wl": (rx, alpha, (texts, off, planted)),
+        **extra}
 
 
-def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, peak_kind):
+def bench_sharded(args, torch, P, stream, world, rank, local, peak, peak_kind):
     """--shard: ONE text split over the ranks (strong scaling).  Per step every
     rank runs sfa_match_map on its shard, the ranks all-gather the |D|-entry
     mappings (NCCL) and fold them in text order (sfa_combine_maps)."""
     from paper_1405_0562_b200 import parallel as PL
+    cfg = args.config if args.config != 5 else 2
+    rx, alpha, text = workload(cfg)
+    sfa = P.SFA(rx, alpha)
     a, b = PL.shard_bounds(text.size, world, rank)
     nD = sfa.info()["dfa_states"]
     with torch.cuda.stream(stream):
@@ -341,10 +473,7 @@ def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, p
     def step():
         with torch.cuda.stream(stream):
             sfa.match_map(dshard, local_map, stream)
-            if world > 1:
-                maps = PL.gather_maps(local_map)
-            else:
-                maps = local_map.view(1, -1)
+            maps = PL.gather_maps(local_map) if world > 1 else local_map.view(1, -1)
             sfa.combine_maps(maps, maps.shape[0], res, stream)
 
     for _ in range(args.warmup):
@@ -356,7 +485,6 @@ def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, p
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        time.sleep(0.3)
         e0.record(stream)
         for _ in range(args.steps):
             step()
@@ -375,7 +503,7 @@ def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, p
         "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic (seeded, DESIGN.md input recipe)",
-        "config": {"workload": CONFIG_NAMES[args.config], "bytes_per_step": int(text.size),
+        "config": {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(text.size),
                    "parallelism": f"text sharded over {world} ranks; |D|-entry map all-gather (NCCL)",
                    "result": [q, bool(acc)]},
         "roofline": {"bound": "hbm", "achieved": gbs / world, "peak": peak, "unit": "GB/s",
@@ -385,93 +513,25 @@ def bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, p
     print(json.dumps(line), flush=True)
 
 
-def bench_batch(args, torch, P, sfa, rx, alpha, batch, stream, world, rank, local, peak, peak_kind, peaks):
-    """Config 5 as the timed workload: one step = sfa_match_batch over the whole batch."""
-    texts, off = batch
-    count = off.size - 1
-    with torch.cuda.stream(stream):
-        dt = torch.from_numpy(texts).cuda()
-        do = torch.from_numpy(off.astype(np.int64)).cuda()
-        res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
-    torch.cuda.synchronize()
-    length = int(off[1] - off[0])
-    assert (np.diff(off) == length).all()
-    # the offsets API (sfa_match_batch) as a secondary number
-    for _ in range(args.warmup):
-        sfa.match_batch(dt, do, count, res, stream)
-    torch.cuda.synchronize()
-    ok_off = res.clone()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(max(1, args.steps // 2)):
-        sfa.match_batch(dt, do, count, res, stream)
-    e1.record(stream)
-    e1.synchronize()
-    offsets_gbs = texts.size / (e0.elapsed_time(e1) / max(1, args.steps // 2) * 1e-3) / 1e9
-    # timed: equal texts through sfa_match_batch_uniform (the TMA scan, per-text fold)
-    for _ in range(args.warmup):
-        sfa.match_batch_uniform(dt, length, count, res, stream)
-    torch.cuda.synchronize()
-    if not torch.equal(ok_off, res):
-        raise SystemExit("uniform batch results differ from the offsets path")
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    with ClockSampler(local) as clk:
-        time.sleep(0.3)
-        e0.record(stream)
-        for _ in range(args.steps):
-            sfa.match_batch_uniform(dt, length, count, res, stream)
-        e1.record(stream)
-        e1.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
-    gbs = texts.size / (ms_per_step * 1e-3) / 1e9
-    accepts = int(res.view(count, 2)[:, 1].sum().item())
-    if rank != 0:
-        return
-    info = sfa.info()
-    line = {
-        "metric": METRIC, "value": world * gbs, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded, DESIGN.md input recipe)",
-        "config": {"workload": CONFIG_NAMES[5], "bytes_per_step": int(texts.size), "texts": count,
-                   "accepted": accepts, "l2": "4 GiB input > 126 MB L2: no flush needed",
-                   "api": "sfa_match_batch_uniform (TMA scan, per-text fold)",
-                   "offsets_api_gbs": offsets_gbs,
-                   "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
-                   "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                     "traffic": ncu_traffic(5), "peak_kind": f"{peak_kind} copy bandwidth"},
-        "clocks": clk.summary(), "gpu_launches": args.steps,
-    }
-    print(json.dumps(line), flush=True)
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5, help="5 (default): the batch headline; 1-4: one text")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--all", action="store_true", help="also time configs 1, 3, 4, 5")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--per-config", default="2,3,4", help="single-text configs timed beside the headline ('' = none)")
+    ap.add_argument("--single-reps", type=int, default=15)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-bytes", type=int, default=64 << 20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shard", action="store_true", help="split ONE text over the ranks (strong scaling)")
-    ap.add_argument("--residency", type=int, default=0,
-                    help="diagnostic: force a residency mode (1 PRIVATE, 2 SHARED, 3 HOT, 4 L2; 0 = auto)")
     ap.add_argument("--rn", action="store_true",
                     help="also run the r_n scalability family (r5..r127, r_a) with Alg. 3 beside it")
     ap.add_argument("--rn-bytes", type=int, default=1 << 30)
     ap.add_argument("--spec", action="store_true",
-                    help="also time the paper's baseline, Alg. 3 (speculative DFA), on each config's text")
+                    help="also time the paper's baseline, Alg. 3 (speculative DFA), on each per-config text")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -487,125 +547,79 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind, peaks = load_peaks()
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    stream = torch.cuda.Stream()
+    if args.shard:
+        return bench_sharded(args, torch, P, stream, world, rank, local, peak, peak_kind)
 
     cfg = args.config
-    rx, alpha, text = workload(cfg)
-    sfa = P.SFA(rx, alpha)
-    if args.residency:
-        sfa.set_residency(args.residency)
-    stream = torch.cuda.Stream()
     if cfg == 5:
-        return bench_batch(args, torch, P, sfa, rx, alpha, text, stream, world, rank, local, peak, peak_kind, peaks)
-    if args.shard:
-        return bench_sharded(args, torch, P, sfa, text, stream, world, rank, local, peak, peak_kind)
-    with torch.cuda.stream(stream):
-        dtext = torch.from_numpy(text).cuda()
-        res = torch.zeros(2, dtype=torch.int32, device="cuda")
-    torch.cuda.synchronize()
-    # parity of the timed configuration (exact; the oracle is not called here)
-    q, acc = sfa.match(dtext, stream)
-    expected = {1: (3, True), 2: (0, True)}.get(cfg)
-    if os.environ.get("SFA_DIAG_STRIDE"):
-        expected = None  # diagnostic overlapped-rows mode: results are meaningless
-    if expected is not None and (q, acc) != expected:
-        raise SystemExit(f"wrong result {(q, acc)} != {expected}")
-
-    for _ in range(args.warmup):
-        sfa.match_async(dtext, res, stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        time.sleep(0.3)  # let the sampler start
-        e0.record(stream)
-        for _ in range(args.steps):
-            sfa.match_async(dtext, res, stream)
-        e1.record(stream)
-        e1.synchronize()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
-    per_rank_gbs = text.size / (ms_per_step * 1e-3) / 1e9
-    value = world * per_rank_gbs
-
-    # end to end: host (pinned) -> device copies inside the timed region, result read back
-    pinned = torch.from_numpy(text).pin_memory()
-    sfa.match_host(pinned, stream)
-    torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.e2e_steps):
-        got = sfa.match_host(pinned, stream)
-    t1.record(stream)
-    t1.synchronize()
-    e2e_ms = t0.elapsed_time(t1) / args.e2e_steps
-    if expected is not None and got != expected:
-        raise SystemExit(f"wrong e2e result {got}")
-    e2e_val = world * text.size / (e2e_ms * 1e-3) / 1e9
-
-    extras = {}
-    if args.all and rank == 0:
-        for c in (1, 3, 4, 5):
-            if c != cfg:
-                steps = 200 if c != 5 else 20
-                extras[f"cfg{c}"] = extra_config(torch, P, c, stream, steps, args.warmup, peak, args.spec)
-    rn = rn_family(torch, P, stream, args.warmup, peak, args.rn_bytes) if args.rn and rank == 0 else None
-    spec_line = None
-    if args.spec and rank == 0:
-        spec_line = spec_compare(torch, sfa, dtext, text.size, ms_per_step, stream, args.warmup, expected)
+        sfa, dkeep, h = bench_batch(args, torch, P, stream, world, rank, local, peak, peak_kind, nsm)
+        nbytes, api, launches = h["bytes"], "sfa_match_batch (device offsets; k_batch_plan + segmented k_scan_tma)", 2
+        kernel = "k_batch_plan + k_scan_tma<SEG> (achieved = text bytes / step time, both launches included)"
+        cfgd = {"workload": CONFIG_NAMES[5], "bytes_per_step": int(nbytes), "texts": h["count"],
+                "accepted": h["accepted"], "l2": "4 GiB input > 126 MB L2: no flush needed", "api": api,
+                "residency": h["residency"], "sfa_states": h["sfa_states"], "dfa_states": h["dfa_states"],
+                "parallelism": f"replicas x{world}"}
+        rx, alpha, wl = h.pop("wl")
+        del dkeep
+        sfa.close()
+    else:
+        rx, alpha, text = workload(cfg)
+        per_rank = single_text_config(torch, P, cfg, stream, args.steps, args.warmup, args.single_reps, peak,
+                                      peak_kind, nsm, peaks.get("sm_max_mhz", 1965.0), text_in=(rx, alpha, text))
+        h = {"value": world * per_rank["value"], "ms_per_step": per_rank["ms_per_step"],
+             "per_rank_gbs": per_rank["value"], "median_ms_per_step": per_rank["median_ms_per_step"],
+             "clocks": {"sm_mhz": None, "reasons": [], "samples": 0}, "single_launch": per_rank["single_launch"]}
+        nbytes, launches, kernel = text.size, 1, "k_scan_tma (one launch per step)"
+        cfgd = {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(nbytes), "api": "sfa_match_async",
+                "l2": "input > 126 MB L2: no flush needed" if nbytes > (126 << 20) else "input smaller than L2",
+                "residency": per_rank["residency"], "parallelism": f"replicas x{world}"}
+        wl = text
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    clocks = clk.summary()
-    info = sfa.info()
-    sm_hz = (clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    # shared-memory ceilings: one conflict-free LDS wavefront per 32
-    # lookups (1 lookup per text byte) -> 32 B/clk/SM; with the staged text
-    # (TMA write + LDS.128 read, 1/128 wavefront each per byte) -> 21.33 B/clk/SM
-    smem_peak = nsm * 32 * sm_hz / 1e9
-    smem_dp_peak = nsm * (1.0 / (1 / 32 + 2 / 128)) * sm_hz / 1e9
+    clocks = h["clocks"]
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded, DESIGN.md input recipe)",
-        "config": {"workload": CONFIG_NAMES[cfg], "bytes_per_step": int(text.size),
-                   "l2": "input 256 MiB-4 GiB > 126 MB L2: no flush needed" if text.size > (126 << 20)
-                   else "input smaller than L2 (L2-warm)",
-                   "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
-                   "dfa_states": info["dfa_states"], "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": per_rank_gbs / peak, "traffic": ncu_traffic(cfg),
-                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "kernel": "k_scan_tma (one launch per step; achieved = text bytes / launch time)",
-                     "smem_lookup_peak_gbs": smem_peak, "smem_datapath_peak_gbs": smem_dp_peak,
-                     "sm_mhz_for_smem_peaks": sm_hz / 1e6,
-                     "frac_of_min_roofline": per_rank_gbs / min(peak, smem_peak),
-                     "frac_of_min_datapath": per_rank_gbs / min(peak, smem_dp_peak)},
-        "clocks": clocks,
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(text.size), "d2h_bytes_per_step": 8,
-                "api": "sfa_match_host (pinned host text, 64 MiB slices copied and matched in a pipeline)"},
-        "gpu_launches": args.steps,
+        "metric": METRIC, "value": h["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "median_ms_per_step": h["median_ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded, DESIGN.md input recipe)", "config": cfgd,
+        "roofline": roofline(h["per_rank_gbs"], peak, peak_kind, nsm, sm_mhz, kernel,
+                             ncu_traffic(f"cfg{cfg}"), int(nbytes)),
+        "clocks": clocks, "gpu_launches": launches * args.steps,
     }
-    if rn:
-        line["rn_family"] = rn
-    if spec_line:
-        line["alg3_speculative"] = spec_line
-    if extras:
-        line["per_config"] = extras
+    for k in ("single_launch", "uniform_api"):
+        if k in h:
+            line[k] = h[k]
+    line["e2e"] = h.get("e2e")
+    if cfg != 5:
+        sfa = P.SFA(rx, alpha)
+        pinned = torch.from_numpy(wl).pin_memory()
+        sfa.match_host(pinned, stream)
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.e2e_steps)):
+            sfa.match_host(pinned, stream)
+        e2e_s = (time.perf_counter() - t0) / max(1, args.e2e_steps)
+        line["e2e"] = {"value": world * wl.size / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(wl.size),
+                       "d2h_bytes_per_step": 8, "api": "sfa_match_host (pinned host text, sliced pipeline)"}
+        sfa.close()
+    pcs = [int(c) for c in args.per_config.split(",") if c.strip()] if args.per_config else []
+    per = {}
+    for c in pcs:
+        if c != cfg:
+            per[f"cfg{c}"] = single_text_config(torch, P, c, stream, min(args.steps, 100) if c != 1 else 200,
+                                                args.warmup, args.single_reps, peak, peak_kind, nsm, sm_mhz,
+                                                spec=args.spec)
+    if per:
+        line["per_config"] = per
+    if args.rn:
+        line["rn_family"] = rn_family(torch, P, stream, args.warmup, peak, args.rn_bytes)
     if not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, rx, alpha, text, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_sample(cfg, rx, alpha, wl, args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

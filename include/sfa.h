@@ -225,6 +225,17 @@ SFA_API int sfa_match_host(const sfa_handle* h, const uint8_t* h_text, size_t n,
                    uint32_t* final_state, int* accept);
 
 /*
+ * sfa_match_batch_host -- end-to-end sfa_match_batch on HOST buffers (pinned
+ * or pageable): texts h_texts[h_offsets[i] : h_offsets[i+1]) (h_offsets:
+ * count+1 uint64, host, non-decreasing: checked, INVALID_ARG otherwise), the
+ * results to h_results (count entries, host).  The texts go to the device in
+ * slices of whole texts (<= max(64 MiB, the longest text), <= 2^20 texts) on a
+ * copy stream while the previous slice is matched on `stream`.  Blocking.
+ */
+SFA_API int sfa_match_batch_host(const sfa_handle* h, const uint8_t* h_texts, const uint64_t* h_offsets, size_t count,
+                                 sfa_stream_t stream, sfa_result* h_results);
+
+/*
  * Test / diagnostic knobs.
  *
  * sfa_match_chunked -- divides the text into exactly `nchunks` chunks by

@@ -71,7 +71,7 @@ INVALID_STATE = 0xFFFFFFFF
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
            "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform", "sfa_match_speculative",
-           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows")
+           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows", "sfa_match_batch_host")
 
 _lib = None
 
@@ -102,6 +102,7 @@ def lib() -> C.CDLL:
         L.sfa_combine_maps.argtypes = [vp, vp, C.c_size_t, vp, vp]
         L.sfa_match_speculative.argtypes = [vp, vp, C.c_size_t, C.c_uint64, vp, vp, vp]
         L.sfa_set_tuning.argtypes = [vp, C.POINTER(sfa_tuning_t)]
+        L.sfa_match_batch_host.argtypes = [vp, vp, vp, C.c_size_t, vp, vp]
         L.sfa_match_rows.argtypes = [vp, vp, C.c_size_t, vp, vp, C.c_size_t, C.POINTER(sfa_rows_plan), vp]
         L.sfa_export_dfa.argtypes = [vp, u32p, u8p]
         L.sfa_export_sfa.argtypes = [vp, u32p, u32p, u8p]
@@ -230,6 +231,29 @@ def sfa_match_host(h: int, h_text, stream=None):
     return q.value, bool(a.value)
 
 
+def _hptr(x) -> int:
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise ValueError("expected a contiguous array")
+        return x.ctypes.data
+    if x.is_cuda:
+        raise ValueError("expected host memory")
+    return x.data_ptr()
+
+
+def sfa_match_batch_host(h: int, h_texts, h_offsets, count: int | None = None, h_results=None, stream=None):
+    """End to end from host memory (numpy arrays or CPU tensors, pinned or not):
+    -> (final_states uint32[count], accepts uint32[count]); blocking."""
+    off = h_offsets
+    count = (off.size if isinstance(off, np.ndarray) else off.numel()) - 1 if count is None else count
+    res = np.zeros((max(count, 1), 2), np.uint32) if h_results is None else h_results
+    if count:
+        _check(lib().sfa_match_batch_host(h, _hptr(h_texts), _hptr(off), count, _stream(stream), _hptr(res)))
+    r = res if isinstance(res, np.ndarray) else res.numpy()
+    r = r.view(np.uint32).reshape(-1, 2)[:count]
+    return r[:, 0], r[:, 1]
+
+
 def sfa_match_chunked(h: int, d_text, nchunks: int, n: int | None = None, stream=None, want_states: bool = True):
     """Forced SPEC chunking (test knob): -> (final_state, accept, chunk_states or None)."""
     n = _nbytes(d_text) if n is None else n
@@ -356,6 +380,9 @@ class SFA:
 
     def match_speculative(self, d_text, d_result, nchunks=0, d_chunk_maps=None, stream=None):
         return sfa_match_speculative(self.h, d_text, d_result, nchunks, d_chunk_maps, None, stream)
+
+    def match_batch_host(self, h_texts, h_offsets, count=None, h_results=None, stream=None):
+        return sfa_match_batch_host(self.h, h_texts, h_offsets, count, h_results, stream)
 
     def match_host(self, h_text, stream=None):
         return sfa_match_host(self.h, h_text, stream)

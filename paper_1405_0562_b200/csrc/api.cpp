@@ -114,7 +114,12 @@ struct sfa_handle {
     void* gmaps = nullptr;            // batch: 3 tensor maps rewritten on the device
     uint32_t* berr = nullptr;         // batch: error word (== epoch: bad offsets)
     uint32_t epoch = 0;
-    uint8_t* stage[2] = {nullptr, nullptr};   // sfa_match_host staging
+    uint8_t* stage[2] = {nullptr, nullptr};   // sfa_match_host / sfa_match_batch_host staging
+    size_t stage_cap = 0;
+    uint64_t* soff[2] = {nullptr, nullptr};   // sfa_match_batch_host: offsets of the staged slices
+    size_t soff_cap = 0;
+    sfa_result* bres = nullptr;               // sfa_match_batch_host: device results
+    size_t bres_cap = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
     cudaEvent_t ev_done = nullptr;    // orders uses of the shared scratch across streams
@@ -131,7 +136,7 @@ struct sfa_handle {
         cudaDeviceSynchronize();
         for (void** pp : {(void**)&dT, (void**)&dcls, (void**)&dTrange, (void**)&dmaps32, (void**)&dmaps16, (void**)&dimg0,
                           (void**)&dfinal, (void**)&drep_off, (void**)&drep, (void**)&partials, (void**)&ticket, (void**)&dres,
-                          (void**)&dplan, (void**)&gmaps, (void**)&berr, (void**)&stage[0], (void**)&stage[1],
+                          (void**)&dplan, (void**)&gmaps, (void**)&berr, (void**)&stage[0], (void**)&stage[1], (void**)&soff[0], (void**)&soff[1], (void**)&bres,
                           (void**)&dcomp, (void**)&dpairs, (void**)&dTdev, (void**)&dfam, (void**)&dfg, (void**)&dftab,
                           (void**)&ddwin, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
                           (void**)&spec_maps, (void**)&spec_ticket, (void**)&daux[0], (void**)&daux[1]}) {
@@ -152,6 +157,7 @@ struct sfa_handle {
         priv_R = dwin_bytes = nfam = dwin_R = dwin_X = 0;
         aux_bytes[0] = aux_bytes[1] = 0;
         spec_cap = 0;
+        stage_cap = soff_cap = bres_cap = 0;
         dev_bytes = 0;
         has_last = false;
         uploaded = false;
@@ -629,6 +635,28 @@ struct sfa_handle {
             e = sfa::launch_scan_tma(mode, vec(), a, cfg, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "scan launch");
+        return SFA_OK;
+    }
+
+    // Host-call staging: two device slices of >= bytes each, the copy stream and its events.
+    int ensure_staging(size_t bytes) {
+        if (!copy_stream) {
+            for (int i = 0; i < 2; ++i) {
+                CU(cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&ev_used[i], cudaEventDisableTiming));
+            }
+            CU(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        }
+        if (stage_cap < bytes) {
+            if (has_last) CU(cudaStreamSynchronize(last_stream));
+            for (int i = 0; i < 2; ++i) {
+                if (stage[i]) CU(cudaFree(stage[i]));
+                stage[i] = nullptr;
+            }
+            stage_cap = 0;
+            for (int i = 0; i < 2; ++i) CU(cudaMalloc(&stage[i], bytes));
+            stage_cap = bytes;
+        }
         return SFA_OK;
     }
 
@@ -1118,14 +1146,8 @@ int sfa_match_host(const sfa_handle* hc, const uint8_t* h_text, size_t n, sfa_st
     int rc = h->begin(s);
     if (rc) return rc;
     if (!h->dmaps16) return fail(SFA_ERR_CAPACITY, "mapping table too large for sliced host matching");
-    if (!h->stage[0]) {
-        for (int i = 0; i < 2; ++i) {
-            CU(cudaMalloc(&h->stage[i], kSlice));
-            CU(cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&h->ev_used[i], cudaEventDisableTiming));
-        }
-        CU(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-    }
+    rc = h->ensure_staging(kSlice);
+    if (rc) return rc;
     // The copy stream must not overwrite a staging buffer before earlier work
     // on `s` (from a previous call) is done with it.
     CU(cudaEventRecord(h->ev_used[0], s));
@@ -1150,6 +1172,75 @@ int sfa_match_host(const sfa_handle* hc, const uint8_t* h_text, size_t n, sfa_st
     CU(cudaStreamSynchronize(s));
     *final_state = h->hres[0].final_state;
     *accept = static_cast<int>(h->hres[0].accept);
+    return SFA_OK;
+}
+
+int sfa_match_batch_host(const sfa_handle* hc, const uint8_t* h_texts, const uint64_t* h_offsets, size_t count,
+                         sfa_stream_t stream, sfa_result* h_results) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (count == 0) return SFA_OK;
+    if (!h_offsets || !h_results) return fail(SFA_ERR_INVALID_ARG, "NULL offsets or results");
+    if (count > (1ull << 31)) return fail(SFA_ERR_INVALID_ARG, "count too large");
+    uint64_t longest = 0;
+    for (size_t i = 0; i < count; ++i) {
+        if (h_offsets[i + 1] < h_offsets[i]) return fail(SFA_ERR_INVALID_ARG, "offsets decrease");
+        longest = std::max<uint64_t>(longest, h_offsets[i + 1] - h_offsets[i]);
+    }
+    if (!h_texts && h_offsets[count] > h_offsets[0]) return fail(SFA_ERR_INVALID_ARG, "h_texts is NULL");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = h->begin(s);
+    if (rc) return rc;
+    // slices of whole texts, at most max(kSlice, longest text) bytes and 2^20 texts
+    const uint64_t cap = std::max<uint64_t>(kSlice, (longest + 255) & ~uint64_t(255));
+    rc = h->ensure_staging(cap);
+    if (rc) return rc;
+    const size_t kMaxTexts = 1u << 20;
+    const size_t ntexts_cap = std::min<size_t>(count, kMaxTexts) + 1;
+    if (h->soff_cap < ntexts_cap) {
+        if (h->has_last) CU(cudaStreamSynchronize(h->last_stream));
+        for (int i = 0; i < 2; ++i) {
+            if (h->soff[i]) CU(cudaFree(h->soff[i]));
+            h->soff[i] = nullptr;
+        }
+        h->soff_cap = 0;
+        for (int i = 0; i < 2; ++i) CU(cudaMalloc(&h->soff[i], ntexts_cap * sizeof(uint64_t)));
+        h->soff_cap = ntexts_cap;
+    }
+    if (h->bres_cap < count) {
+        if (h->has_last) CU(cudaStreamSynchronize(h->last_stream));
+        if (h->bres) CU(cudaFree(h->bres));
+        h->bres = nullptr;
+        h->bres_cap = 0;
+        CU(cudaMalloc(&h->bres, count * sizeof(sfa_result)));
+        h->bres_cap = count;
+    }
+    // the copy stream must not overwrite a staging slice before earlier work on `s` is done with it
+    CU(cudaEventRecord(h->ev_used[0], s));
+    CU(cudaEventRecord(h->ev_used[1], s));
+    size_t i0 = 0;
+    for (int k = 0; i0 < count; ++k) {
+        const int b = k & 1;
+        size_t i1 = i0 + 1;
+        while (i1 < count && i1 - i0 < kMaxTexts && h_offsets[i1 + 1] - h_offsets[i0] <= cap) ++i1;
+        const uint64_t a0 = h_offsets[i0], bytes = h_offsets[i1] - a0;
+        CU(cudaStreamWaitEvent(h->copy_stream, h->ev_used[b], 0));
+        if (bytes) CU(cudaMemcpyAsync(h->stage[b], h_texts + a0, bytes, cudaMemcpyHostToDevice, h->copy_stream));
+        CU(cudaMemcpyAsync(h->soff[b], h_offsets + i0, (i1 - i0 + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                           h->copy_stream));
+        CU(cudaEventRecord(h->ev_copied[b], h->copy_stream));
+        CU(cudaStreamWaitEvent(s, h->ev_copied[b], 0));
+        // text i of the slice = stage[b][off[i] - a0 ...): the kernels only add off[i] to the base
+        rc = h->launch_seg(h->stage[b] - a0, h->soff[b], 0, i1 - i0, h->bres + i0, s);
+        if (rc) return rc;
+        CU(cudaEventRecord(h->ev_used[b], s));
+        i0 = i1;
+    }
+    CU(cudaMemcpyAsync(h_results, h->bres, count * sizeof(sfa_result), cudaMemcpyDeviceToHost, s));
+    rc = h->end(s);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(s));
     return SFA_OK;
 }
 

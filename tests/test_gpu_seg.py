@@ -290,3 +290,33 @@ def test_random_regexes_tma_sizes(torch_cuda):
         off = np.zeros(51, np.uint64)
         off[1:] = np.minimum(np.cumsum(lens), n)
         check_batch(torch, sfa, d, t, off)
+
+
+def test_batch_host_end_to_end(torch_cuda):
+    """sfa_match_batch_host: host texts in slices of whole texts (one text longer
+    than a 64 MiB slice included), pinned and pageable, == Alg. 2 per text;
+    decreasing host offsets are refused with INVALID_ARG."""
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    d = odfa(rx, None)
+    sfa = P.SFA(rx, None)
+    rng = np.random.default_rng(41)
+    lens = np.concatenate([rng.integers(0, 100_000, size=3000), [70 << 20], rng.integers(0, 50, size=5000)])
+    off = np.zeros(lens.size + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    texts = W.cfg3_text(int(off[-1]), plant=True)
+    word = np.frombuffer(W.cfg3_words()[9], np.uint8)
+    for o in rng.integers(0, texts.size - 8, size=500):
+        texts[o:o + word.size] = word
+    qo, ao = d.run_batch(texts, off)
+    q, a = sfa.match_batch_host(texts, off)
+    assert (q == qo).all() and (a == ao).all()
+    ht = torch.from_numpy(texts).pin_memory()
+    ho = torch.from_numpy(off.view(np.int64)).pin_memory()
+    q, a = sfa.match_batch_host(ht, ho)
+    assert (q == qo).all() and (a == ao).all()
+    bad = off.copy()
+    bad[5], bad[6] = bad[6], bad[5]
+    with pytest.raises(P.SFAError) as e:
+        sfa.match_batch_host(texts, bad)
+    assert e.value.code == P.SFA_ERR_INVALID_ARG
