@@ -30,8 +30,14 @@ def _inputs():
             + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "sfa.h"), __file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+DIAG_LIB = os.path.join(LIBDIR, "libsfa_diag.so")
+
+
+def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+    """diag: the diagnostic library (-DSFA_STAMPS: per-CTA phase stamps of the
+    TMA scan, sfa_diag_stamps) -- never loaded by the product, tests or bench."""
     os.makedirs(LIBDIR, exist_ok=True)
+    LIB = DIAG_LIB if diag else globals()["LIB"]
     if not force and os.path.exists(LIB):
         newest = max(os.path.getmtime(p) for p in _inputs())
         if os.path.getmtime(LIB) >= newest:
@@ -39,8 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs, cmds = [], []
     for src_name in SOURCES:
         src = os.path.join(CSRC, src_name)
-        obj = os.path.join(LIBDIR, src_name + f".{os.getpid()}.o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        obj = os.path.join(LIBDIR, src_name + f".{os.getpid()}{'.diag' if diag else ''}.o")
+        cmd = [NVCC, *ARCH, *FLAGS, *(["-DSFA_STAMPS"] if diag else []), "-c", src, "-o", obj]
         if src_name.endswith(".cu") and verbose:
             cmd[1:1] = ["-Xptxas", "-v"]
         if verbose:
@@ -65,4 +71,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, diag="--diag" in sys.argv))

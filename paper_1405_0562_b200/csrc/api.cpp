@@ -110,6 +110,9 @@ struct sfa_handle {
     uint32_t* ticket = nullptr;
     sfa_result* dres = nullptr;       // 2 results (single-text matches and the slice ring)
     sfa_result* hres = nullptr;       // pinned
+#ifdef SFA_STAMPS
+    uint64_t* dstamps = nullptr;      // diagnostic builds: 8 stamps per CTA of the last TMA scan
+#endif
     sfa::TmaPlan* dplan = nullptr;    // batch: the plan k_batch_plan writes
     void* gmaps = nullptr;            // batch: 3 tensor maps rewritten on the device
     uint32_t* berr = nullptr;         // batch: error word (== epoch: bad offsets)
@@ -523,6 +526,9 @@ struct sfa_handle {
         CU(cudaMalloc(&ticket, sizeof(uint32_t)));
         CU(cudaMemset(ticket, 0, sizeof(uint32_t)));
         CU(cudaMalloc(&dres, 2 * sizeof(sfa_result)));
+#ifdef SFA_STAMPS
+        CU(cudaMalloc(&dstamps, kMaxSlots * 8 * sizeof(uint64_t)));
+#endif
         CU(cudaMalloc(&dplan, sizeof(sfa::TmaPlan)));
         CU(cudaMalloc(&gmaps, 512));
         CU(cudaMalloc(&berr, 16));
@@ -627,6 +633,10 @@ struct sfa_handle {
             a.result = d_result;
             a.map_out = map_out;
             a.row_ids = row_ids;
+#ifdef SFA_STAMPS
+            a.stamps = dstamps;
+            CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 8 * sizeof(uint64_t), stream));
+#endif
             sfa::TmaConfig cfg;
             rc = tma_plan(mode, a.t, d_text, n, &cfg, &a.plan);
             if (rc) return rc;
@@ -679,6 +689,10 @@ struct sfa_handle {
         a.off = d_off;
         a.count = count;
         a.results = d_results;
+#ifdef SFA_STAMPS
+        a.stamps = dstamps;
+        CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 8 * sizeof(uint64_t), stream));
+#endif
         sfa::TmaConfig cfg;
         if (!sfa::tma_choose(mode, a.t, smem_optin, ktune(), &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
         const uint32_t G = static_cast<uint32_t>(sm_count);
@@ -1243,5 +1257,15 @@ int sfa_match_batch_host(const sfa_handle* hc, const uint8_t* h_texts, const uin
     CU(cudaStreamSynchronize(s));
     return SFA_OK;
 }
+
+#ifdef SFA_STAMPS
+// Diagnostic builds only (include/sfa_diag.h): the stamps of the last TMA scan.
+SFA_API int sfa_diag_stamps(const sfa_handle* h, uint64_t* host, size_t n) {
+    if (!h || !h->dstamps) return fail(SFA_ERR_INVALID_ARG, "no stamps");
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(host, h->dstamps, std::min<size_t>(n, kMaxSlots * 8) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return SFA_OK;
+}
+#endif
 
 }  // extern "C"

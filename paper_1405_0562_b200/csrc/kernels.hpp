@@ -34,6 +34,7 @@ struct ScanArgs {
     sfa_result* results;
     const uint32_t* err;  // batch error word: == epoch when k_batch_plan found bad offsets
     uint32_t epoch;
+    uint64_t* stamps;     // diagnostic builds (-DSFA_STAMPS) only: 8 %globaltimer stamps per CTA
 };
 
 struct DirectArgs {

@@ -44,6 +44,26 @@
 
 namespace sfa {
 
+// Diagnostic builds (libsfa_diag.so, -DSFA_STAMPS): per-CTA phase times of
+// k_scan_tma (scripts/stamps.py).  The product library compiles them out.
+#ifdef SFA_STAMPS
+#define SFA_STAMP(i)                                                                 \
+    do {                                                                             \
+        if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 8 + (i)] = globaltimer(); \
+    } while (0)
+#define SFA_STAMP_P(i)                                                               \
+    do {                                                                             \
+        if (a.stamps) a.stamps[blockIdx.x * 8 + (i)] = globaltimer();                \
+    } while (0)
+#else
+#define SFA_STAMP(i) \
+    do {             \
+    } while (0)
+#define SFA_STAMP_P(i) \
+    do {               \
+    } while (0)
+#endif
+
 template <class Step>
 __host__ __device__ size_t table_bytes(const DevTables& t) {
     return (Step::smem_bytes(t) + 15) & ~size_t(15);
@@ -591,6 +611,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + kMaxRing * 8;
     pdl_launch_dependents();
+    SFA_STAMP(0);
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < nring; ++s) {
             mbar_init(full0 + 8 * s, 1);
@@ -630,6 +651,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             }
             prefetch_tmap(mload);
             prefetch_tmap(mlast);
+            SFA_STAMP_P(7);  // producer: first TMA about to be issued
             const uint64_t policy = policy_evict_first();
             const int y0 = static_cast<int>(P.cta_row0(blockIdx.x));
             const uint32_t nstages = static_cast<uint32_t>(P.L / ROWB);
@@ -669,6 +691,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     __syncwarp();
     if (lane == 0) mbar_arrive(rbar);
     bar_compute(kNW * 32);
+    SFA_STAMP(1);  // tables built
     // Everything below reads the text, the plan or the scratch shared with
     // the previous launch of the stream: wait for it (the prologue above
     // overlapped its tail).
@@ -686,7 +709,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     const uint32_t nstages = rc ? static_cast<uint32_t>(P.L / ROWB) : 0u;
     const Bounds B{a.off, a.off ? __ldg(a.off) : 0ull, a.count, P.len};
     const uint8_t* const text = a.text + B.off0;  // the range: one text, or the batch's texts back to back
-    if (t.aux_bytes) mbar_wait(abar, 0);
+    SFA_STAMP(2);  // after griddepcontrol.wait
 
     // The last CTA also runs the ragged tail [tail_start, n) (< (1 + 8 NB) L
     // bytes), split over its compute threads; its value goes to slot
@@ -694,6 +717,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     uint32_t tail_acc = 0;
     SegEl tail_el = seg_identity();
     if (blockIdx.x == gridDim.x - 1) {
+        if (t.aux_bytes) mbar_wait(abar, 0);
         const uint64_t len = P.n - P.tail_start;
         const uint64_t per = (len + kNW * 32 - 1) / (kNW * 32);
         const uint64_t p0 = min(P.n, P.tail_start + threadIdx.x * per), p1 = min(P.n, p0 + per);
@@ -818,6 +842,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
         if constexpr (SEG) scan_stages_seg<K, ROWB, Sh>(S, st, rsrc, rrow, ring, 0, nstages, lane, rs.nb, close_sfa);
         else scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, 0, nstages, lane);
     }
+    SFA_STAMP(3);  // thread 0's rows scanned
+    if (t.aux_bytes) mbar_wait(abar, 0);  // the composition image (bulk copy issued at entry)
     // canonical value of each row's running piece
     uint32_t val[K];
 #pragma unroll
@@ -849,6 +875,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 if (blockIdx.x == gridDim.x - 1) parts[gridDim.x] = make_uint4(tail_el.h, tail_el.t, tail_el.tl, tail_el.b);
             }
         }
+        SFA_STAMP(4);  // CTA folded
         // last CTA to finish: head piece . CTA 0 . ... . CTA G-1 . tail
         if (warp == 0) {
             __threadfence();
@@ -867,6 +894,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 *a.sc.ticket = 0;
             }
         }
+        SFA_STAMP(5);  // epilogue done (last CTA)
         return;
     } else {
         if (a.row_ids) {
@@ -887,8 +915,10 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             if (blockIdx.x == gridDim.x - 1) store_partial<VEC>(a.sc.partials, gridDim.x, tail_acc);
         }
         bar_compute(kNW * 32);
+        SFA_STAMP(4);  // CTA folded
         grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, P.head, gridDim.x + 1, a.q_in, kNW, red, flag,
                                  a.map_out);
+        SFA_STAMP(5);
     }
 }
 

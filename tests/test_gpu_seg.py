@@ -227,7 +227,11 @@ def test_batch_async_does_not_synchronise(torch_cuda):
     r1 = torch.zeros(2, dtype=torch.int32, device="cuda")
     empty = torch.empty(0, dtype=torch.uint8, device="cuda")
     s = torch.cuda.Stream()
-    sfa.match(vt, s)                                 # uploads tables outside the check
+    # first calls upload the tables and load the kernels (CUDA lazy loading): outside the check
+    sfa.match(vt, s)
+    sfa.match_batch(vt, off, 3, res, s)
+    sfa.match_async(vt, r1, s)
+    sfa.match_async(empty, r1, s)
     torch.cuda.synchronize()
     with torch.cuda.stream(s):
         torch.cuda._sleep(2_000_000_000)             # ~1 s of GPU time
