@@ -109,7 +109,7 @@ static bool tma_choose_once(Res mode, const DevTables& t, size_t smem_optin, con
 // ((q0 = 0, [eps in L])); thread 0 plans the scan of [off[0], off[count]) as
 // one range (make_plan) and rewrites the two tensor maps in global memory
 // from the host-encoded template (tensormap.replace: base, dims, row stride,
-// box height; three maps for the box heights bh, bl_hi, bl_lo), then
+// box height; three maps for the box heights bh, rc_hi % bh, rc_lo % bh), then
 // publishes them to the TMA proxy.
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void tmap_store(void* dst, const CUtensorMap& src) {
@@ -147,10 +147,11 @@ static __global__ void __launch_bounds__(1024) k_batch_plan(const __grid_constan
         if (p.nchunks == 0) base &= ~uint64_t(255);
         const uint32_t rows = p.nchunks ? p.nchunks : 1u;
         uint8_t* m = static_cast<uint8_t*>(a.gmaps);
-        const uint32_t heights[3] = {p.bh, p.bl_hi, p.bl_lo};
+        uint32_t heights[3];
+        detail::box_heights(p, heights);
         for (int k = 0; k < 3; ++k) {
             tmap_store(m + k * sizeof(CUtensorMap), tmpl.load);
-            tmap_retarget(m + k * sizeof(CUtensorMap), base, static_cast<uint32_t>(p.L), rows, heights[k] ? heights[k] : 8u);
+            tmap_retarget(m + k * sizeof(CUtensorMap), base, static_cast<uint32_t>(p.L), rows, heights[k]);
         }
         asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
     }

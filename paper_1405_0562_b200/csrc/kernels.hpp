@@ -21,7 +21,7 @@ struct ScanArgs {
     uint64_t n;
     TmaPlan plan;         // the host's plan (dplan == nullptr)
     const TmaPlan* dplan; // batch: the plan k_batch_plan wrote (read after griddepcontrol.wait)
-    const void* gmaps;    // batch: its three tensor maps in global memory (load, last_hi, last_lo), else nullptr
+    const void* gmaps;    // batch: its three tensor maps in global memory (load, part_hi, part_lo), else nullptr
     Scratch sc;
     const uint32_t* q_in;
     sfa_result* result;

@@ -470,9 +470,9 @@ struct TmaShape {
 };
 
 struct TmaMaps {
-    CUtensorMap load;      // box [ROWB x bh]: the first NB - 1 boxes of a stage
-    CUtensorMap last_hi;   // box [ROWB x bl_hi]: the last box of CTAs with rc_hi rows
-    CUtensorMap last_lo;   // box [ROWB x bl_lo]: ... with rc_lo rows
+    CUtensorMap load;      // box [ROWB x bh]: the full boxes of a stage
+    CUtensorMap part_hi;   // box [ROWB x (rc_hi % bh)]: the last box of CTAs with rc_hi rows
+    CUtensorMap part_lo;   // box [ROWB x (rc_lo % bh)]: ... with rc_lo rows
 };
 
 // The consumer side of the stage ring: full/empty mbarriers, slot, phase.
@@ -612,6 +612,13 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + kMaxRing * 8;
     pdl_launch_dependents();
     SFA_STAMP(0);
+#ifdef SFA_STAMPS
+    if (a.stamps && threadIdx.x == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.stamps[blockIdx.x * 8 + 6] = smid;
+    }
+#endif
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < nring; ++s) {
             mbar_init(full0 + 8 * s, 1);
@@ -644,13 +651,14 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             if (rc == 0) return;
             const CUtensorMap* gm = static_cast<const CUtensorMap*>(a.gmaps);
             const CUtensorMap* mload = gm ? gm : &maps.load;
-            const CUtensorMap* mlast = gm ? gm + (rc == P.rc_hi ? 1 : 2) : (rc == P.rc_hi ? &maps.last_hi : &maps.last_lo);
+            const CUtensorMap* mpart = gm ? gm + (rc == P.rc_hi ? 1 : 2) : (rc == P.rc_hi ? &maps.part_hi : &maps.part_lo);
+            const uint32_t nfull = rc / P.bh, part = rc - nfull * P.bh;  // boxes of bh rows, then one of `part`
             if (gm) {
                 tmap_acquire(mload);
-                tmap_acquire(mlast);
+                tmap_acquire(mpart);
             }
             prefetch_tmap(mload);
-            prefetch_tmap(mlast);
+            if (part) prefetch_tmap(mpart);
             SFA_STAMP_P(7);  // producer: first TMA about to be issued
             const uint64_t policy = policy_evict_first();
             const int y0 = static_cast<int>(P.cta_row0(blockIdx.x));
@@ -664,11 +672,10 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 if (i >= nring) mbar_wait(empty0 + 8 * slot, phase ^ 1);
                 mbar_expect_tx(full0 + 8 * slot, rc * ROWB);
                 const uint32_t dst = ring0 + slot * Sh::kStageBytes;
-#pragma unroll
-                for (int j = 0; j < Sh::NB - 1; ++j)
+                for (uint32_t j = 0; j < nfull; ++j)
                     tma_load_2d(dst + j * P.bh * ROWB, mload, full0 + 8 * slot, i * ROWB, y0 + j * P.bh, policy);
-                tma_load_2d(dst + (Sh::NB - 1) * P.bh * ROWB, mlast, full0 + 8 * slot, i * ROWB,
-                            y0 + (Sh::NB - 1) * P.bh, policy);
+                if (part)
+                    tma_load_2d(dst + nfull * P.bh * ROWB, mpart, full0 + 8 * slot, i * ROWB, y0 + nfull * P.bh, policy);
                 if (++slot == nring) {
                     slot = 0;
                     phase ^= 1;
@@ -718,8 +725,9 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     SegEl tail_el = seg_identity();
     if (blockIdx.x == gridDim.x - 1) {
         if (t.aux_bytes) mbar_wait(abar, 0);
+        // 16-byte pieces from the (16-aligned) tail start: one vector load each
         const uint64_t len = P.n - P.tail_start;
-        const uint64_t per = (len + kNW * 32 - 1) / (kNW * 32);
+        const uint64_t per = 16 * ((len + 16 * kNW * 32 - 1) / (16 * kNW * 32));
         const uint64_t p0 = min(P.n, P.tail_start + threadIdx.x * per), p1 = min(P.n, p0 + per);
         if constexpr (SEG) {
             SegEl e = SG::fold_warp(S, t, a.results, SG::run_piece(S, t, a.results, B, text, p0, p1));
@@ -1035,16 +1043,25 @@ inline cudaError_t encode_map(CUtensorMap* m, void* base, uint64_t L, uint64_t r
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Box heights of a plan's three maps (0: unused, encoded as 8).
+__host__ __device__ inline void box_heights(const TmaPlan& P, uint32_t h[3]) {
+    h[0] = P.bh;
+    h[1] = P.bh ? P.rc_hi % P.bh : 0;
+    h[2] = P.bh ? P.rc_lo % P.bh : 0;
+    for (int k = 0; k < 3; ++k)
+        if (h[k] == 0) h[k] = 8;
+}
+
 // The host's maps for a host plan: the last encoding is reused when the
 // geometry repeats (repeated matches of one buffer: host overhead).
 inline cudaError_t host_maps(const ScanArgs& a, const TmaConfig& cfg, TmaMaps* out) {
     struct Key {
         const void* base;
         uint64_t L, rows;
-        uint32_t bh, bl_hi, bl_lo, rowb;
+        uint32_t h0, h1, h2, rowb;
         int promo;
         bool operator==(const Key& o) const {
-            return base == o.base && L == o.L && rows == o.rows && bh == o.bh && bl_hi == o.bl_hi && bl_lo == o.bl_lo &&
+            return base == o.base && L == o.L && rows == o.rows && h0 == o.h0 && h1 == o.h1 && h2 == o.h2 &&
                    rowb == o.rowb && promo == o.promo;
         }
     };
@@ -1053,12 +1070,14 @@ inline cudaError_t host_maps(const ScanArgs& a, const TmaConfig& cfg, TmaMaps* o
     const TmaPlan& P = a.plan;
     void* base = const_cast<uint8_t*>(a.text + P.head);
     if (P.nchunks == 0) base = reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(base) & ~uintptr_t(255));
-    const Key key{base, P.L, P.nchunks, P.bh, P.bl_hi, P.bl_lo, static_cast<uint32_t>(cfg.rowb), cfg.promo};
+    uint32_t h[3];
+    box_heights(P, h);
+    const Key key{base, P.L, P.nchunks, h[0], h[1], h[2], static_cast<uint32_t>(cfg.rowb), cfg.promo};
     if (!(key == last)) {
         last = Key{nullptr, 0, 0, 0, 0, 0, 0, -9};
-        cudaError_t e = encode_map(&maps.load, base, P.L, P.nchunks, cfg.rowb, P.bh, cfg.promo);
-        if (e == cudaSuccess) e = encode_map(&maps.last_hi, base, P.L, P.nchunks, cfg.rowb, P.bl_hi, cfg.promo);
-        if (e == cudaSuccess) e = encode_map(&maps.last_lo, base, P.L, P.nchunks, cfg.rowb, P.bl_lo, cfg.promo);
+        cudaError_t e = encode_map(&maps.load, base, P.L, P.nchunks, cfg.rowb, h[0], cfg.promo);
+        if (e == cudaSuccess) e = encode_map(&maps.part_hi, base, P.L, P.nchunks, cfg.rowb, h[1], cfg.promo);
+        if (e == cudaSuccess) e = encode_map(&maps.part_lo, base, P.L, P.nchunks, cfg.rowb, h[2], cfg.promo);
         if (e != cudaSuccess) return e;
         last = key;
     }
@@ -1080,8 +1099,7 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, unsigned grid,
         std::memset(&maps, 0, sizeof(maps));  // unused: the kernel reads a.gmaps
     } else {
         const TmaPlan& P = a.plan;
-        for (uint32_t h : {P.bh, P.bl_hi, P.bl_lo})
-            if (P.nchunks && (h == 0 || h > 256 || h % 8)) return cudaErrorInvalidValue;
+        if (P.nchunks && (P.bh == 0 || P.bh > 256 || P.bh % 8)) return cudaErrorInvalidValue;
         e = host_maps(a, cfg, &maps);
         if (e != cudaSuccess) return e;
     }

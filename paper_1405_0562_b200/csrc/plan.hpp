@@ -84,16 +84,13 @@ struct Scratch {
 //   head  [0, head)                           < 256 bytes, up to 256-B alignment
 //   rows  [head + r*L, head + (r+1)*L), r < nchunks   (the 2-D TMA tensor;
 //         L a multiple of 64 and >= 256)
-//   tail  [tail_start, n)                     the rest (< 8 L bytes)
+//   tail  [tail_start, n)                     < L bytes
 // Every piece is a chunk of Alg. 5 (any division, Theorem 3).
-// Rows are split over the CTAs so that every SM scans nearly the same number
-// (the launch lasts as long as its busiest CTA): the first m CTAs get rc_hi
-// rows, the others rc_lo = rc_hi - 8, rc_hi = the average rounded up to 8.  A
-// CTA loads its rows as NB TMA boxes per stage: NB - 1 boxes of bh rows and a
-// last box of bl_hi or bl_lo rows (heights multiples of 8, the swizzle
-// atom).  When no such split exists (few rows) every CTA gets rc_hi = NB * bh
-// rows (rc_lo = rc_hi, m = ctas) and the last CTA's rows past nchunks are
-// TMA zero fill.
+// The rows are split over the CTAs as evenly as possible (the launch lasts as
+// long as its busiest CTA): the first m CTAs get rc_hi = ceil(rows / G) rows,
+// the others rc_lo = floor(rows / G).  A CTA loads its rc rows per stage as
+// rc / bh TMA boxes of bh rows (bh a multiple of 8, the swizzle atom) and one
+// last box of rc % bh rows (any height: nothing follows it in the stage).
 struct TmaPlan {
     uint64_t n = 0;
     uint64_t head = 0;
@@ -101,7 +98,7 @@ struct TmaPlan {
     uint32_t nchunks = 0;      // rows
     uint32_t ctas = 0;         // CTAs that own rows (the launch may have more)
     uint32_t rc_hi = 0, rc_lo = 0, m = 0;
-    uint32_t bh = 0, bl_hi = 0, bl_lo = 0;
+    uint32_t bh = 0;           // full box height; the last box of a CTA is rc % bh rows
     uint64_t tail_start = 0;   // head + nchunks * L
     uint64_t len = 0;          // batch of equal texts: their length (0: offsets / one text)
     __host__ __device__ uint32_t cta_rows(uint32_t b) const { return b < m ? rc_hi : (b < ctas ? rc_lo : 0u); }
@@ -141,34 +138,16 @@ __host__ __device__ inline void make_plan(uint64_t addr, uint64_t n, uint32_t G,
     }
     p->head = head;
     p->L = L;
-    p->tail_start = head;
-    const uint64_t rows = body / L;
+    const uint64_t rows = body / L;  // <= G * R
+    p->nchunks = static_cast<uint32_t>(rows);
+    p->tail_start = head + rows * L;
     if (rows == 0) return;
-    uint64_t used = rows;
-    // rc_hi = ceil(rows / G) rounded up to 8; NB - 1 boxes of bh rows and a
-    // last box of rc_hi - (NB-1) bh >= 16 rows (so rc_lo's last box keeps >= 8)
-    const uint32_t hi = static_cast<uint32_t>(8 * ((rows + 8ull * G - 1) / (8ull * G)));
-    const uint32_t bh = 8 * ((hi + 8 * NB - 1) / (8 * NB));
-    if (hi <= R && bh <= 256 && hi >= (NB - 1) * bh + 16) {
-        p->rc_hi = hi;
-        p->rc_lo = hi - 8;
-        p->bh = bh;
-        p->bl_hi = hi - (NB - 1) * bh;
-        p->bl_lo = p->bl_hi - 8;
-        const uint64_t mm = (rows - static_cast<uint64_t>(p->rc_lo) * G) / 8;  // rows/G in (hi - 8, hi]
-        p->m = static_cast<uint32_t>(mm < G ? mm : G);
-        p->ctas = G;
-        used = static_cast<uint64_t>(p->rc_lo) * G + 8ull * p->m;
-    } else {  // few rows: equal CTAs of NB whole boxes
-        const uint32_t gran = 8 * NB;
-        const uint32_t rc = static_cast<uint32_t>(gran * ((rows + static_cast<uint64_t>(gran) * G - 1) / (static_cast<uint64_t>(gran) * G)));
-        p->rc_hi = p->rc_lo = rc;
-        p->bh = p->bl_hi = p->bl_lo = rc / NB;
-        p->ctas = static_cast<uint32_t>((rows + rc - 1) / rc);
-        p->m = p->ctas;
-    }
-    p->nchunks = static_cast<uint32_t>(used);
-    p->tail_start = head + used * L;
+    p->rc_lo = static_cast<uint32_t>(rows / G);
+    p->m = static_cast<uint32_t>(rows - static_cast<uint64_t>(p->rc_lo) * G);
+    p->rc_hi = p->rc_lo + (p->m ? 1u : 0u);
+    if (!p->m) p->m = G;  // every CTA rc_hi (= rc_lo) rows
+    p->ctas = p->rc_lo ? G : p->m;
+    p->bh = 8 * ((p->rc_hi + 8 * NB - 1) / (8 * NB));
 }
 
 }  // namespace sfa

@@ -7,9 +7,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_1405_0562_b200 import _build  # noqa: E402
-
-os.environ["SFA_LIB"] = _build.build(diag=True)
+# the diagnostic library (built by `python -m paper_1405_0562_b200._build --diag`), set before the
+# package reads SFA_LIB at import
+os.environ["SFA_LIB"] = os.path.join(ROOT, "paper_1405_0562_b200", "_lib", "libsfa_diag.so")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -26,6 +26,8 @@ def report(name, h, G):
     st = st.reshape(G, 8).astype(np.int64)
     live = st[:, 0] > 0
     st = st[live]
+    smid = st[:, 6].copy()
+    st[:, 6] = 0
     t0 = st[:, 0].min()
     rel = (st - t0) / 1e3
     rel[st == 0] = np.nan
@@ -37,6 +39,12 @@ def report(name, h, G):
         print(f"  {what:18s} min {mn:8.2f}  median {md:8.2f}  max {mx:8.2f} us")
     scan = rel[:, 3] - rel[:, 2]
     print(f"  scan duration      min {np.nanmin(scan):.2f} median {np.nanmedian(scan):.2f} max {np.nanmax(scan):.2f}")
+    order = np.argsort(scan)
+    print("  slowest CTAs (cta, smid, us):", [(int(b), int(smid[b]), round(float(scan[b]), 1)) for b in order[-12:]])
+    print("  fastest CTAs (cta, smid, us):", [(int(b), int(smid[b]), round(float(scan[b]), 1)) for b in order[:8]])
+    by_sm = np.full(int(smid.max()) + 1, np.nan)
+    by_sm[smid] = scan
+    print("  scan us by smid:", " ".join(f"{x:.0f}" for x in by_sm))
 
 
 def main():

@@ -5,10 +5,9 @@ use, and checked on many sizes and alignments.
 Invariants: the head brings the rows to 256-B alignment; the rows are cut at
 multiples of L (a multiple of 64, >= 256) and the pieces head | rows | tail
 tile [0, n) exactly (every byte is read once); every CTA
-gets rc_hi or rc_lo rows whose TMA boxes (NB per stage, heights multiples of
-8 rows and <= 256) cover them exactly; all G SMs get rows once the text is big
-enough (the uneven split), their loads differ by less than 8*NB rows; the
-tail stays small."""
+gets ceil or floor of rows / G rows (all G SMs scan once there are G rows),
+loaded as at most NB TMA boxes per stage (full boxes of bh rows, bh a multiple
+of 8 and <= 256, then one partial box); the tail is less than one row."""
 import os
 import subprocess
 
@@ -27,8 +26,8 @@ int main(int argc, char** argv) {
     while (scanf("%llu %llu %u %u %u %u %u", &addr, &n, &G, &R, &NB, &rowb, &al) == 7) {
         sfa::TmaPlan p;
         sfa::make_plan(addr, n, G, R, NB, rowb, al, &p);
-        printf("%llu %llu %u %u %u %u %u %u %u %u %llu\n", (unsigned long long)p.head, (unsigned long long)p.L,
-               p.nchunks, p.ctas, p.rc_hi, p.rc_lo, p.m, p.bh, p.bl_hi, p.bl_lo, (unsigned long long)p.tail_start);
+        printf("%llu %llu %u %u %u %u %u %u %llu\n", (unsigned long long)p.head, (unsigned long long)p.L,
+               p.nchunks, p.ctas, p.rc_hi, p.rc_lo, p.m, p.bh, (unsigned long long)p.tail_start);
     }
 }
 '''
@@ -69,40 +68,30 @@ def test_plan_invariants(planner):
                       int(rng.integers(1, 160)), R, NB, rowb, 0))
     out = planner(cases)
     assert len(out) == len(cases)
-    for (addr, n, G, R, NB, rowb, al), (head, L, rows, ctas, hi, lo, m, bh, bl_hi, bl_lo, tail) in zip(cases, out):
+    for (addr, n, G, R, NB, rowb, al), (head, L, rows, ctas, hi, lo, m, bh, tail) in zip(cases, out):
         assert head < 256 and head <= n
         if head < n:
             assert (addr + head) % 256 == 0
         assert L >= 256 and L % 64 == 0 and L % rowb == 0
         if al:
             assert L % al == 0
-        assert tail == head + rows * L and tail <= n
+        assert tail == head + rows * L and tail <= n and n - tail < max(L, 256)   # the tail is < one row
         assert rows <= G * R
         if rows == 0:
-            assert n - head < 256
             continue
-        assert 1 <= ctas <= G
-        assert hi <= R and hi % 8 == 0 and bh % 8 == 0 and 8 <= bh <= 256
-        assert bl_hi % 8 == 0 and bl_lo % 8 == 0 and 8 <= bl_lo <= bl_hi <= 256
-        assert (NB - 1) * bh + bl_hi == hi and (NB - 1) * bh + bl_lo == lo   # the boxes tile each CTA's rows
-        # rows per CTA: m CTAs with hi rows, then lo rows
+        assert 1 <= ctas <= G and hi <= R and hi - lo <= 1
+        assert bh % 8 == 0 and 8 <= bh <= 256 and hi <= NB * bh       # <= NB boxes per stage
         per = [hi if b < m else lo for b in range(ctas)]
-        if lo < hi:
-            assert ctas == G and sum(per) == rows         # every SM scans; the split tiles the rows exactly
-            assert hi - lo == 8
-            assert hi * G - rows < 8 * G + 8 * G          # busiest CTA within 8 rows of the average
-        else:
-            assert m == ctas and (ctas - 1) * hi < rows <= ctas * hi   # last CTA's extra rows are TMA zero fill
-        # the tail (plus the < 8 rows the split leaves over) stays below 8 rows
-        assert n - tail < 8 * L + (L if lo == hi else 0)
-        if n >= 64 * G * R:
-            assert ctas == G and lo < hi
+        assert sum(per) == rows and min(per) >= 1                     # the split tiles the rows exactly
+        assert max(per) == -(-rows // G)                              # busiest CTA: the ceiling of the average
+        if rows >= G:
+            assert ctas == G
 
 
 def test_plan_uses_every_sm_on_the_configs(planner):
     """cfg2 (256 MiB) and the 1 GiB / 4 GiB ranges: all 148 SMs get rows and
     the busiest carries < 1% more than the average (round 1 left 2 idle)."""
     for n in (268_435_450, 1 << 30, 1 << 32):
-        (head, L, rows, ctas, hi, lo, m, bh, bl_hi, bl_lo, tail), = planner([(0x7f0000000000, n, 148, 992, 4, 32, 0)])
+        (head, L, rows, ctas, hi, lo, m, bh, tail), = planner([(0x7f0000000000, n, 148, 992, 4, 32, 0)])
         assert ctas == 148
-        assert hi * L <= 1.01 * n / 148 + L
+        assert hi * L <= n / 148 + L
