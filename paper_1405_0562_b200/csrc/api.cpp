@@ -82,7 +82,7 @@ struct sfa_handle {
     uint16_t* dperm = nullptr;                // HOT: canonical -> device id
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
     uint16_t *dfam = nullptr, *dfg = nullptr, *dftab = nullptr, *ddwin = nullptr;  // FACTORED step tables
-    uint32_t dwin_bytes = 0, nfam = 0, dwin_R = 0, dwin_X = 0;
+    uint32_t dwin_bytes = 0, nfam = 0, dwin_R = 0, dwin_X = 0, dwin_u8 = 0;
     sfa_tuning_t tuning{};                    // shape knobs (sfa_set_tuning); zero = automatic
     bool factor_on() const { return tuning.no_factor == 0; }
     sfa::Tuning ktune() const {
@@ -157,7 +157,7 @@ struct sfa_handle {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         ev_done = nullptr;
         copy_stream = nullptr;
-        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = 0;
+        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = 0;
         aux_bytes[0] = aux_bytes[1] = 0;
         spec_cap = 0;
         stage_cap = soff_cap = bres_cap = 0;
@@ -222,6 +222,7 @@ struct sfa_handle {
             t.dwin_bytes = dwin_bytes;
             t.dwin_R = dwin_R;
             t.dwin_X = dwin_X;
+            t.dwin_u8 = dwin_u8;
         }
         t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin, tuning.hot_rows) : 0;
         return t;
@@ -366,26 +367,43 @@ struct sfa_handle {
                 const uint32_t b = j + 1 < W ? lo + j : ob;
                 dw[static_cast<size_t>(q) * W + j] = static_cast<uint16_t>(A.dfa[static_cast<size_t>(q) * 256 + b]);
             }
+        // Layout: 32 bank-private u16 copies when they fit (cfg4: 4 instr/byte,
+        // conflict-free); else 32 bank-private u8 copies for |D| <= 256 (cfg3/5:
+        // conflict-free at 3 more ALU ops per byte); else R < 32 u16 copies.
         uint32_t R = 32, X = 0;
-        const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R
-        for (; R >= 1; R /= 2) {
-            X = sfa::dfa_X(nD, R);
-            if (R <= Rmax && static_cast<uint64_t>(X) * W <= (kDfaMax) && X <= 65535u) break;
+        const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R (< 32: no u8 layout)
+        const bool u16_32 = Rmax >= 32 && static_cast<uint64_t>(sfa::dfa_X(nD, 32)) * W <= kDfaMax;
+        const bool u8_32 = !u16_32 && Rmax >= 32 && nD <= 256 && static_cast<uint64_t>(sfa::dfa8_X(nD)) * W <= kDfaMax;
+        if (u8_32) {
+            X = sfa::dfa8_X(nD);
+        } else {
+            for (; R >= 1; R /= 2) {
+                X = sfa::dfa_X(nD, R);
+                if (R <= Rmax && static_cast<uint64_t>(X) * W <= (kDfaMax) && X <= 65535u) break;
+            }
+            if (R == 0) return SFA_OK;
         }
-        if (R == 0) return SFA_OK;
         dwin_R = R;
         dwin_X = X;
+        dwin_u8 = u8_32 ? 1u : 0u;
         CU(upload(&dfam, fam.data(), fam.size()));
         CU(upload(&dfg, g.data(), g.size()));
         CU(upload(&dftab, tab.data(), tab.size()));
         dwin_bytes = (X * W + 15) & ~15u;
-        std::vector<uint16_t> img(dwin_bytes / 2, 0);
+        std::vector<uint8_t> img(dwin_bytes, 0);
         for (uint32_t j = 0; j < W; ++j)
-            for (uint32_t q = 0; q < nD; ++q)
-                for (uint32_t c = 0; c < R; ++c)
-                    img[(j * X + sfa::dfa_enc(q, c, R)) / 2] =
-                        static_cast<uint16_t>(sfa::dfa_enc(dw[static_cast<size_t>(q) * W + j], c, R));
-        CU(upload(&ddwin, img.data(), img.size()));
+            for (uint32_t q = 0; q < nD; ++q) {
+                const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
+                for (uint32_t c = 0; c < R; ++c) {
+                    if (u8_32) {
+                        img[j * X + sfa::enc8(q, c)] = static_cast<uint8_t>(nq);
+                    } else {
+                        const uint16_t v = static_cast<uint16_t>(sfa::dfa_enc(nq, c, R));
+                        std::memcpy(&img[j * X + sfa::dfa_enc(q, c, R)], &v, 2);
+                    }
+                }
+            }
+        CU(upload(reinterpret_cast<uint8_t**>(&ddwin), img.data(), img.size()));
         nfam = static_cast<uint32_t>(fams.size());
         dev_bytes += fam.size() * 4 + tab.size() * 2 + dw.size() * 2;
         return SFA_OK;

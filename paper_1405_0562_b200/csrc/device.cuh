@@ -35,6 +35,7 @@ namespace sfa {
 extern __shared__ __align__(1024) uint8_t dsmem[];
 
 __device__ __forceinline__ uint32_t ld_tbl_u16(uint32_t off) { return *reinterpret_cast<const uint16_t*>(dsmem + off); }
+__device__ __forceinline__ uint32_t ld_tbl_u8(uint32_t off) { return dsmem[off]; }
 __device__ __forceinline__ uint32_t ld_tbl_u32(uint32_t off) { return *reinterpret_cast<const uint32_t*>(dsmem + off); }
 
 // ------------------------------------------------------------------------------------------
@@ -407,14 +408,32 @@ struct StepDfa {
     }
 };
 
+// The same with the u8 layout (plan.hpp enc8): 32 bank-private byte copies,
+// state = enc8(g, lane); one step = PRMT + VIADDMNMX + IMAD + LDS.U8 + the
+// re-encoding of the loaded id (3 ALU ops), conflict-free where the u16
+// layout only fits 16 copies (2-way conflicts).
+struct StepDfa8 {
+    uint32_t neg_lo, wmax, X, lane4;
+    __device__ void params(const DevTables& t) {
+        neg_lo = 0u - t.lo;
+        wmax = t.W - 1;
+        X = t.dwin_X;
+        lane4 = lane_id() << 2;
+    }
+    __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
+        const uint32_t v = ld_tbl_u8(window_col(byte, neg_lo, wmax) * X + st);
+        return ((v >> 2) << 7) + (v & 3u) + lane4;
+    }
+};
+
 // SFA id -> factored state and family; false if s is not factorable
 __device__ __forceinline__ bool fact_from_id(const DevTables& t, uint32_t s, uint32_t& fam, uint32_t& st) {
     fam = __ldg(t.fact_fam + s);
-    st = dfa_enc(__ldg(t.fact_g + s), lane_id() % t.dwin_R, t.dwin_R);
+    st = dw_enc(t, __ldg(t.fact_g + s), lane_id());
     return fam != 0xffffu;
 }
 __device__ __forceinline__ uint32_t fact_to_id(const DevTables& t, uint32_t fam, uint32_t st) {
-    return __ldg(t.fact_tab + fam * t.nD + dfa_dec(st, lane_id() % t.dwin_R, t.dwin_R));
+    return __ldg(t.fact_tab + fam * t.nD + dw_dec(t, st, lane_id()));
 }
 
 // 4 text bytes of one word, in text order (little-endian)

@@ -334,12 +334,19 @@ struct Seg {
     // window table (smem; kTag values only come from FACTORED warps, which have it)
     __device__ __noinline__ static uint32_t apply(const DevTables& t, uint32_t s, uint32_t q) {
         if (t.maps16) return __ldg(t.maps16 + static_cast<uint64_t>(s) * t.nD + q);
-        const uint32_t R = t.dwin_R, c = lane_id() % R, neg_lo = 0u - t.lo, wmax = t.W - 1;
-        uint32_t st = dfa_enc(q, c, R);
+        const uint32_t lane = lane_id();
+        uint32_t st = dw_enc(t, q, lane);
         const uint32_t e = __ldg(t.rep_off + s + 1);
-        for (uint32_t k = __ldg(t.rep_off + s); k < e; ++k)
-            st = ld_tbl_u16(window_col(__ldg(t.rep + k), neg_lo, wmax) * t.dwin_X + st);
-        return dfa_dec(st, c, R);
+        if (t.dwin_u8) {
+            StepDfa8 D;
+            D.params(t);
+            for (uint32_t k = __ldg(t.rep_off + s); k < e; ++k) st = D.step(st, __ldg(t.rep + k));
+        } else {
+            StepDfa D;
+            D.params(t);
+            for (uint32_t k = __ldg(t.rep_off + s); k < e; ++k) st = D.step(st, __ldg(t.rep + k));
+        }
+        return dw_dec(t, st, lane);
     }
     // a . b for two values of one text in order (b is never tagged)
     __device__ static uint32_t cval(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
@@ -821,26 +828,36 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 const uint32_t sid = S.id(st[k], lane);
                 if (SEG && rs.ts[k]) {
                     fam[k] = kTagFam;
-                    g[k] = dfa_enc(t.img0[sid], lane % t.dwin_R, t.dwin_R);
+                    g[k] = dw_enc(t, t.img0[sid], lane);
                 } else {
                     ok &= fact_from_id(t, sid, fam[k], g[k]);
                 }
             }
             if (__all_sync(kFull, ok)) {
-                StepDfa D;
-                D.params(t);
-                if constexpr (SEG) {
-                    const uint32_t g0 = dfa_enc(0u, lane % t.dwin_R, t.dwin_R);
-                    auto close_fact = [&](int k) {
-                        const uint32_t v = fam[k] == kTagFam ? (kTag | dfa_dec(g[k], lane % t.dwin_R, t.dwin_R))
-                                                             : fact_to_id(t, fam[k], g[k]);
-                        seg_close(k, v);
-                        fam[k] = kTagFam;
-                        g[k] = g0;
-                    };
-                    scan_stages_seg<K, ROWB, Sh>(D, g, rsrc, rrow, ring, i, nstages, lane, rs.nb, close_fact);
+                // the rest of the rows through the DFA window table (u8 or u16 layout)
+                auto run_dfa = [&](const auto& D) {
+                    if constexpr (SEG) {
+                        const uint32_t g0 = dw_enc(t, 0u, lane);
+                        auto close_fact = [&](int k) {
+                            const uint32_t v = fam[k] == kTagFam ? (kTag | dw_dec(t, g[k], lane))
+                                                                 : fact_to_id(t, fam[k], g[k]);
+                            seg_close(k, v);
+                            fam[k] = kTagFam;
+                            g[k] = g0;
+                        };
+                        scan_stages_seg<K, ROWB, Sh>(D, g, rsrc, rrow, ring, i, nstages, lane, rs.nb, close_fact);
+                    } else {
+                        scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i, nstages, lane);
+                    }
+                };
+                if (t.dwin_u8) {
+                    StepDfa8 D;
+                    D.params(t);
+                    run_dfa(D);
                 } else {
-                    scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i, nstages, lane);
+                    StepDfa D;
+                    D.params(t);
+                    run_dfa(D);
                 }
                 factored = true;
                 break;
@@ -857,8 +874,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (factored) {
-            val[k] = (SEG && fam[k] == kTagFam) ? (kTag | dfa_dec(g[k], lane % t.dwin_R, t.dwin_R))
-                                                : fact_to_id(t, fam[k], g[k]);
+            val[k] = (SEG && fam[k] == kTagFam) ? (kTag | dw_dec(t, g[k], lane)) : fact_to_id(t, fam[k], g[k]);
         } else {
             val[k] = S.id(st[k], lane);
         }
