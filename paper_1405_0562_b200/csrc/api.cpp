@@ -367,13 +367,16 @@ struct sfa_handle {
                 const uint32_t b = j + 1 < W ? lo + j : ob;
                 dw[static_cast<size_t>(q) * W + j] = static_cast<uint16_t>(A.dfa[static_cast<size_t>(q) * 256 + b]);
             }
-        // Layout: 32 bank-private u16 copies when they fit (cfg4: 4 instr/byte,
-        // conflict-free); else 32 bank-private u8 copies for |D| <= 256 (cfg3/5:
-        // conflict-free at 3 more ALU ops per byte); else R < 32 u16 copies.
+        // Layout: the largest R of 32, 16, ... lane-group u16 copies that fits
+        // (cfg4: R = 32, conflict-free, 4 instr/byte; cfg3/5: R = 16, 2-way
+        // conflicts).  Tuning dfa_u8 = 1 takes 32 bank-private u8 copies instead
+        // when |D| <= 256 and 32 u16 copies do not fit: conflict-free but 3 more
+        // ALU ops per byte -- measured 17% slower than R = 16 on cfg5.
         uint32_t R = 32, X = 0;
-        const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R (< 32: no u8 layout)
+        const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R
         const bool u16_32 = Rmax >= 32 && static_cast<uint64_t>(sfa::dfa_X(nD, 32)) * W <= kDfaMax;
-        const bool u8_32 = !u16_32 && Rmax >= 32 && nD <= 256 && static_cast<uint64_t>(sfa::dfa8_X(nD)) * W <= kDfaMax;
+        const bool u8_32 = tuning.dfa_u8 && !u16_32 && Rmax >= 32 && nD <= 256 &&
+                           static_cast<uint64_t>(sfa::dfa8_X(nD)) * W <= kDfaMax;
         if (u8_32) {
             X = sfa::dfa8_X(nD);
         } else {
@@ -914,7 +917,7 @@ int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* tu) {
         (t.row_align && t.row_align != 64 && t.row_align != 128 && t.row_align != 256) ||
         (t.dfa_copies & (t.dfa_copies - 1)) || t.dfa_copies > 32 ||
         (t.private_copies & (t.private_copies - 1)) || t.private_copies > 32 ||
-        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)))
+        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)) || t.dfa_u8 > 1)
         return fail(SFA_ERR_INVALID_ARG, "bad tuning value");
     if (!tu) t.tma_promo = -1;
     std::lock_guard<std::mutex> lk(h->mu);

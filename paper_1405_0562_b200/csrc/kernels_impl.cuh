@@ -654,6 +654,11 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             pdl_wait();
             if (SEG && a.err && *a.err == a.epoch) return;  // bad offsets: the compute warps report
             const TmaPlan P = a.dplan ? *a.dplan : a.plan;
+            if (blockIdx.x == gridDim.x - 1) {  // the tail this CTA runs after its rows: into L2 now
+                const uint8_t* tp = a.text + (a.off ? __ldg(a.off) : 0ull) + P.tail_start;
+                const uint32_t tb = static_cast<uint32_t>((P.n - P.tail_start) & ~uint64_t(15));
+                if (tb) bulk_prefetch_l2(tp, tb);
+            }
             const uint32_t rc = P.cta_rows(blockIdx.x);
             if (rc == 0) return;
             const CUtensorMap* gm = static_cast<const CUtensorMap*>(a.gmaps);
@@ -725,12 +730,13 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     const uint8_t* const text = a.text + B.off0;  // the range: one text, or the batch's texts back to back
     SFA_STAMP(2);  // after griddepcontrol.wait
 
-    // The last CTA also runs the ragged tail [tail_start, n) (< (1 + 8 NB) L
-    // bytes), split over its compute threads; its value goes to slot
-    // gridDim.x of the partials.
+    // The last CTA also runs the ragged tail [tail_start, n) (< L bytes) after
+    // its rows (its bytes were prefetched to L2 by the producer), split over
+    // its compute threads in 16-byte pieces; its value goes to slot gridDim.x
+    // of the partials.
     uint32_t tail_acc = 0;
     SegEl tail_el = seg_identity();
-    if (blockIdx.x == gridDim.x - 1) {
+    auto run_tail = [&]() {
         if (t.aux_bytes) mbar_wait(abar, 0);
         // 16-byte pieces from the (16-aligned) tail start: one vector load each
         const uint64_t len = P.n - P.tail_start;
@@ -747,7 +753,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             const uint32_t s = S.id(run_range(S, S.init(lane), text, p0, p1), lane);
             tail_acc = block_fold<Step, VEC>(S, t, s, kNW, red);
         }
-    }
+    };
 
     uint32_t st[K];
 #pragma unroll
@@ -869,6 +875,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     }
     SFA_STAMP(3);  // thread 0's rows scanned
     if (t.aux_bytes) mbar_wait(abar, 0);  // the composition image (bulk copy issued at entry)
+    if (blockIdx.x == gridDim.x - 1) run_tail();
     // canonical value of each row's running piece
     uint32_t val[K];
 #pragma unroll
@@ -908,11 +915,26 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
         bar_compute(kNW * 32);
         if (*flag == 0) return;
         __threadfence();
+        // two levels: warp w folds parts [w*per, (w+1)*per) (warp 0 after the
+        // head piece), then warp 0 folds the kNW warp values
+        const uint32_t nparts = gridDim.x + 1, per = (nparts + kNW - 1) / kNW;  // <= 32
+        SegEl e = seg_identity();
+        const uint32_t u = warp * per + lane;
+        if (lane < per && u < nparts) {
+            const uint4 v = __ldcg(parts + u);
+            e = SegEl{v.x, v.y, v.z, v.w};
+        }
+        e = SG::fold_warp(S, t, a.results, e);
         if (warp == 0) {
             const uint64_t hp = (P.head + 31) / 32;
             const uint64_t h0 = min(P.head, lane * hp), h1 = min(P.head, h0 + hp);
-            SegEl acc = SG::fold_warp(S, t, a.results, SG::run_piece(S, t, a.results, B, text, h0, h1));
-            acc = SG::fold_slots(S, t, a.results, parts, gridDim.x + 1, acc, true);
+            const SegEl hd = SG::fold_warp(S, t, a.results, SG::run_piece(S, t, a.results, B, text, h0, h1));
+            if (lane == 0) e = SG::comb(S, t, a.results, hd, e);
+        }
+        if (lane == 0) slots[warp] = make_uint4(e.h, e.t, e.tl, e.b);
+        bar_compute(kNW * 32);
+        if (warp == 0) {
+            const SegEl acc = SG::fold_slots(S, t, a.results, slots, kNW, seg_identity(), false);
             if (lane == 0) {
                 if (acc.b) SG::emit(t, a.results, acc.tl, acc.t);  // the range's last text
                 *a.sc.ticket = 0;

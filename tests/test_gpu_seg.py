@@ -95,12 +95,13 @@ def test_rows_private_cfg4_r16(torch_cuda):
     rows_vs_oracle(torch, sfa, *CFG4, W.cfg4_text(64 << 20), 3)
 
 
-@pytest.mark.parametrize("which", ["cfg3", "cfg4"])
+@pytest.mark.parametrize("which", ["cfg3", "cfg4", "cfg3-u8"])
 def test_rows_hot_factored(torch_cuda, which):
     """HOT + FACTORED: rows switch to the DFA step after their first stages;
-    their canonical ids come back through fact_tab."""
+    their canonical ids come back through fact_tab (u16 lane-group copies of
+    the DFA window, or the u8 bank-private layout)."""
     torch = torch_cuda
-    if which == "cfg3":
+    if which.startswith("cfg3"):
         rx, alpha = W.cfg3_regex(), None
         t = W.cfg3_text(64 << 20, plant=True)
         words = W.cfg3_words()
@@ -113,8 +114,13 @@ def test_rows_hot_factored(torch_cuda, which):
         rx, alpha = CFG4
         t = W.cfg4_text(64 << 20)
     sfa = P.SFA(rx, alpha)
+    if which.endswith("u8"):
+        sfa.set_tuning(dfa_u8=1)
     rows_vs_oracle(torch, sfa, rx, alpha, t, 0)
     assert P.sfa_info(sfa.h)["residency"] == P.RES_HOT_L2
+    if which.endswith("u8"):   # and a batch through the u8 layout
+        texts, off = W.ragged_batch(19, 2000, 40_000, b"abcdefghijklmnopqrstuvwxyz")
+        check_batch(torch, sfa, odfa(rx, alpha), texts, off)
 
 
 # --------------------------------------------------------------------------- batches (segmented scan)
