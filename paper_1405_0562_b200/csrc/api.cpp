@@ -734,6 +734,8 @@ struct sfa_handle {
             p.epoch = ++epoch ? epoch : ++epoch;  // never 0 (the error word starts at 0)
             p.results = d_results;
             p.eps_accept = A.dfa_final[0];
+            p.slots = reinterpret_cast<uint4*>(partials);  // the scan uses them only after griddepcontrol.wait
+            p.ticket = berr + 1;
             e = sfa::launch_batch_plan(p, cfg, sm_count, stream);
             if (e != cudaSuccess) return cuda_fail(e, "batch plan launch");
             a.dplan = dplan;
@@ -743,8 +745,10 @@ struct sfa_handle {
             e = sfa::launch_scan_seg(mode, a, cfg, G, stream);
         } else {
             a.n = len * count;
-            sfa::make_plan(reinterpret_cast<uintptr_t>(base), a.n, G, cfg.rows_per_cta, cfg.nb,
-                           static_cast<uint32_t>(cfg.rowb), tuning.row_align, &a.plan);
+            if (!sfa::make_plan_uniform(reinterpret_cast<uintptr_t>(base), len, count, G, cfg.rows_per_cta, cfg.nb,
+                                        static_cast<uint32_t>(cfg.rowb), &a.plan))
+                sfa::make_plan(reinterpret_cast<uintptr_t>(base), a.n, G, cfg.rows_per_cta, cfg.nb,
+                               static_cast<uint32_t>(cfg.rowb), tuning.row_align, &a.plan);
             a.plan.len = len;
             e = sfa::launch_scan_seg(mode, a, cfg, G, stream);
         }

@@ -105,9 +105,11 @@ static bool tma_choose_once(Res mode, const DevTables& t, size_t smem_optin, con
 // k_batch_plan -- the batch's launch plan on the device (SURVEY s8(b):
 // sfa_match_batch is asynchronous, so the host never reads the offsets).
 // Every thread checks its texts' offsets (a decreasing pair -> *err = epoch:
-// the scan then reports every result as invalid) and answers empty texts
-// ((q0 = 0, [eps in L])); thread 0 plans the scan of [off[0], off[count]) as
-// one range (make_plan) and rewrites the two tensor maps in global memory
+// the scan then reports every result as invalid), answers empty texts
+// ((q0 = 0, [eps in L])) and tracks the text lengths; the last block to finish
+// plans the scan of [off[0], off[count]) as one range -- rows of len / mm
+// bytes when every text has the same length (make_plan_uniform: no boundary
+// inside a row), else make_plan -- and rewrites the tensor maps in global memory
 // from the host-encoded template (tensormap.replace: base, dims, row stride,
 // box height; three maps for the box heights bh, rc_hi % bh, rc_lo % bh), then
 // publishes them to the TMA proxy.
@@ -129,33 +131,71 @@ __device__ __forceinline__ void tmap_retarget(void* m, uint64_t addr, uint32_t L
 
 static __global__ void __launch_bounds__(1024) k_batch_plan(const __grid_constant__ TmaMaps tmpl, const BatchPlanArgs a) {
     pdl_launch_dependents();
+    __shared__ unsigned long long s_min, s_max;
+    __shared__ uint32_t s_bad, s_last;
+    if (threadIdx.x == 0) {
+        s_min = ~0ull;
+        s_max = 0;
+        s_bad = 0;
+    }
+    __syncthreads();
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    bool bad = false;
+    uint64_t mn = ~0ull, mx = 0;
+    uint32_t bad = 0;
     for (uint64_t i = tid; i < a.count; i += nth) {
         const uint64_t s = __ldg(a.off + i), e = __ldg(a.off + i + 1);
-        if (e < s) bad = true;
-        else if (e == s) a.results[i] = sfa_result{0u, a.eps_accept};
-    }
-    if (tid == 0) {
-        const uint64_t s = __ldg(a.off), e = __ldg(a.off + a.count);
-        if (e < s) bad = true;
-        TmaPlan p;
-        make_plan(reinterpret_cast<uint64_t>(a.texts + s), e >= s ? e - s : 0, a.G, a.R, a.NB, a.rowb, a.row_align, &p);
-        *a.dplan = p;
-        uint64_t base = reinterpret_cast<uint64_t>(a.texts + s + p.head);
-        if (p.nchunks == 0) base &= ~uint64_t(255);
-        const uint32_t rows = p.nchunks ? p.nchunks : 1u;
-        uint8_t* m = static_cast<uint8_t*>(a.gmaps);
-        uint32_t heights[3];
-        detail::box_heights(p, heights);
-        for (int k = 0; k < 3; ++k) {
-            tmap_store(m + k * sizeof(CUtensorMap), tmpl.load);
-            tmap_retarget(m + k * sizeof(CUtensorMap), base, static_cast<uint32_t>(p.L), rows, heights[k]);
+        if (e < s) {
+            bad = 1;
+            continue;
         }
-        asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+        if (e == s) a.results[i] = sfa_result{0u, a.eps_accept};
+        mn = min(mn, e - s);
+        mx = max(mx, e - s);
     }
-    if (bad) *a.err = a.epoch;
+    atomicMin(&s_min, mn);
+    atomicMax(&s_max, mx);
+    if (bad) atomicOr(&s_bad, 1u);
+    __syncthreads();
+    // the last block to finish reduces the blocks' (min, max, bad) and plans
+    if (threadIdx.x == 0) {
+        a.slots[blockIdx.x] = make_uint4(static_cast<uint32_t>(s_min), static_cast<uint32_t>(s_min >> 32),
+                                         static_cast<uint32_t>(s_max), static_cast<uint32_t>(s_max >> 32) | (s_bad << 31));
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    uint64_t gmin = ~0ull, gmax = 0;
+    uint32_t gbad = 0;
+    for (uint32_t b = 0; b < gridDim.x; ++b) {
+        const uint4 v = __ldcg(a.slots + b);
+        gmin = min(gmin, static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32));
+        gmax = max(gmax, static_cast<uint64_t>(v.z) | (static_cast<uint64_t>(v.w & 0x7fffffffu) << 32));
+        gbad |= v.w >> 31;
+    }
+    *a.ticket = 0;  // self-resetting
+    const uint64_t s = __ldg(a.off), e = __ldg(a.off + a.count);
+    if (e < s) gbad = 1;
+    TmaPlan p;
+    const uint64_t addr = reinterpret_cast<uint64_t>(a.texts + s);
+    // equal texts: rows of len / mm bytes (no boundary inside a row); else the general cut
+    if (gbad || gmin != gmax || !make_plan_uniform(addr, gmin, a.count, a.G, a.R, a.NB, a.rowb, &p))
+        make_plan(addr, !gbad ? e - s : 0, a.G, a.R, a.NB, a.rowb, a.row_align, &p);
+    *a.dplan = p;
+    uint64_t base = reinterpret_cast<uint64_t>(a.texts + s + p.head);
+    if (p.nchunks == 0) base &= ~uint64_t(255);
+    const uint32_t rows = p.nchunks ? p.nchunks : 1u;
+    uint8_t* m = static_cast<uint8_t*>(a.gmaps);
+    uint32_t heights[3];
+    detail::box_heights(p, heights);
+    for (int k = 0; k < 3; ++k) {
+        tmap_store(m + k * sizeof(CUtensorMap), tmpl.load);
+        tmap_retarget(m + k * sizeof(CUtensorMap), base, static_cast<uint32_t>(p.L), rows, heights[k]);
+    }
+    asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+    if (gbad) *a.err = a.epoch;
 }
 
 cudaError_t launch_batch_plan(const BatchPlanArgs& a, const TmaConfig& cfg, int sm_count, cudaStream_t stream) {
@@ -175,7 +215,7 @@ cudaError_t launch_batch_plan(const BatchPlanArgs& a, const TmaConfig& cfg, int 
         last = Key{dev, cfg.rowb, cfg.promo, a.gmaps};
     }
     const uint64_t want = (a.count + 1023) / 1024;
-    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 2ull * sm_count)));
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count))));
     k_batch_plan<<<grid, 1024, 0, stream>>>(tmpl, a);
     return cudaGetLastError();
 }

@@ -62,6 +62,8 @@ struct BatchPlanArgs {
     uint32_t epoch;
     sfa_result* results;
     uint32_t eps_accept;   // [eps in L]: the result of an empty text is (q0 = 0, eps_accept)
+    uint4* slots;          // scratch: one (min len, max len | bad) per block (>= G)
+    uint32_t* ticket;      // scratch: last-block-done counter (self-resetting, starts 0)
 };
 
 // Shape of a k_scan_tma launch: K chunks per compute thread, ROWB bytes of

@@ -726,8 +726,10 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     const uint32_t rc = P.cta_rows(blockIdx.x);
     const uint64_t crow0 = P.cta_row0(blockIdx.x);
     const uint32_t nstages = rc ? static_cast<uint32_t>(P.L / ROWB) : 0u;
-    const Bounds B{a.off, a.off ? __ldg(a.off) : 0ull, a.count, P.len};
-    const uint8_t* const text = a.text + B.off0;  // the range: one text, or the batch's texts back to back
+    // boundaries by arithmetic when the texts have equal length (plan.len), else from the offsets
+    const uint64_t off0 = a.off ? __ldg(a.off) : 0ull;
+    const Bounds B{P.len ? nullptr : a.off, off0, a.count, P.len};
+    const uint8_t* const text = a.text + off0;  // the range: one text, or the batch's texts back to back
     SFA_STAMP(2);  // after griddepcontrol.wait
 
     // The last CTA also runs the ragged tail [tail_start, n) (< L bytes) after

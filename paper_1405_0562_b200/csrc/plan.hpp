@@ -123,6 +123,19 @@ struct TmaPlan {
     }
 };
 
+// rows (<= G * R) over G CTAs: ceil / floor of rows / G each; full boxes of bh rows.
+__host__ __device__ inline void split_rows(uint64_t rows, uint32_t G, uint32_t NB, TmaPlan* p) {
+    p->nchunks = static_cast<uint32_t>(rows);
+    p->tail_start = p->head + rows * p->L;
+    if (rows == 0) return;
+    p->rc_lo = static_cast<uint32_t>(rows / G);
+    p->m = static_cast<uint32_t>(rows - static_cast<uint64_t>(p->rc_lo) * G);
+    p->rc_hi = p->rc_lo + (p->m ? 1u : 0u);
+    if (!p->m) p->m = G;  // every CTA rc_hi (= rc_lo) rows
+    p->ctas = p->rc_lo ? G : p->m;
+    p->bh = 8 * ((p->rc_hi + 8 * NB - 1) / (8 * NB));
+}
+
 // The plan of a TMA scan of n bytes starting at device address `addr` on G
 // CTAs of at most R rows (NB boxes per stage, rowb bytes per row per stage).
 // row_align: 0 = choose (256/128/64 B, the fewest idle compute rows after a
@@ -154,16 +167,36 @@ __host__ __device__ inline void make_plan(uint64_t addr, uint64_t n, uint32_t G,
     }
     p->head = head;
     p->L = L;
-    const uint64_t rows = body / L;  // <= G * R
-    p->nchunks = static_cast<uint32_t>(rows);
-    p->tail_start = head + rows * L;
-    if (rows == 0) return;
-    p->rc_lo = static_cast<uint32_t>(rows / G);
-    p->m = static_cast<uint32_t>(rows - static_cast<uint64_t>(p->rc_lo) * G);
-    p->rc_hi = p->rc_lo + (p->m ? 1u : 0u);
-    if (!p->m) p->m = G;  // every CTA rc_hi (= rc_lo) rows
-    p->ctas = p->rc_lo ? G : p->m;
-    p->bh = 8 * ((p->rc_hi + 8 * NB - 1) / (8 * NB));
+    split_rows(body / L, G, NB, p);
+}
+
+// Equal texts of `len` bytes back to back (count of them at `addr`): rows of
+// L = len / mm bytes, so every text is mm whole rows and no text boundary
+// falls inside a row (the batch scan then never takes its byte-by-byte
+// boundary path).  mm is the largest divisor of len with count * mm <= G * R
+// (the most rows in flight) and L >= 256 a multiple of rowb and 16; needs
+// addr % 32 == 0 (each 32-B stage piece one DRAM sector).  false: no such cut
+// (use make_plan).
+__host__ __device__ inline bool make_plan_uniform(uint64_t addr, uint64_t len, uint64_t count, uint32_t G, uint32_t R,
+                                                  uint32_t NB, uint32_t rowb, TmaPlan* p) {
+    if (len == 0 || count == 0 || (addr & 31) != 0) return false;
+    const uint64_t GR = static_cast<uint64_t>(G) * R;
+    if (count > GR) return false;
+    uint64_t mm = GR / count;
+    if (mm > len / 256) mm = len / 256;
+    for (; mm >= 1; --mm) {
+        if (len % mm) continue;
+        const uint64_t L = len / mm;
+        if (L % rowb || L % 16) continue;
+        *p = TmaPlan{};
+        p->n = len * count;
+        p->head = 0;
+        p->L = L;
+        p->len = len;
+        split_rows(count * mm, G, NB, p);
+        return true;
+    }
+    return false;
 }
 
 }  // namespace sfa

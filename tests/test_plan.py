@@ -21,11 +21,15 @@ SRC = r'''
 #include <cstdlib>
 #include "plan.hpp"
 int main(int argc, char** argv) {
-    // stdin: addr n G R NB rowb align ; stdout: the plan fields
-    unsigned long long addr, n; unsigned G, R, NB, rowb, al;
-    while (scanf("%llu %llu %u %u %u %u %u", &addr, &n, &G, &R, &NB, &rowb, &al) == 7) {
+    // stdin: addr n G R NB rowb align [len: equal texts of len bytes, n = their count] ; stdout: the plan fields
+    unsigned long long addr, n, len; unsigned G, R, NB, rowb, al;
+    while (scanf("%llu %llu %u %u %u %u %u %llu", &addr, &n, &G, &R, &NB, &rowb, &al, &len) == 8) {
         sfa::TmaPlan p;
-        sfa::make_plan(addr, n, G, R, NB, rowb, al, &p);
+        if (len) {
+            if (!sfa::make_plan_uniform(addr, len, n, G, R, NB, rowb, &p)) { printf("none\n"); continue; }
+        } else {
+            sfa::make_plan(addr, n, G, R, NB, rowb, al, &p);
+        }
         printf("%llu %llu %u %u %u %u %u %u %llu\n", (unsigned long long)p.head, (unsigned long long)p.L,
                p.nchunks, p.ctas, p.rc_hi, p.rc_lo, p.m, p.bh, (unsigned long long)p.tail_start);
     }
@@ -44,9 +48,9 @@ def planner(tmp_path_factory):
                            "-I", "/usr/local/cuda/include", str(src), "-o", str(exe)])
 
     def run(cases):
-        inp = "".join(" ".join(str(x) for x in c) + "\n" for c in cases)
+        inp = "".join(" ".join(str(x) for x in (c if len(c) == 8 else (*c, 0))) + "\n" for c in cases)
         out = subprocess.run([str(exe)], input=inp, capture_output=True, text=True, check=True).stdout.split("\n")
-        return [tuple(int(x) for x in line.split()) for line in out if line.strip()]
+        return [None if line.strip() == "none" else tuple(int(x) for x in line.split()) for line in out if line.strip()]
     return run
 
 
@@ -95,3 +99,24 @@ def test_plan_uses_every_sm_on_the_configs(planner):
         (head, L, rows, ctas, hi, lo, m, bh, tail), = planner([(0x7f0000000000, n, 148, 992, 4, 32, 0)])
         assert ctas == 148
         assert hi * L <= n / 148 + L
+
+
+def test_plan_equal_texts(planner):
+    """Equal texts (make_plan_uniform): every text is mm whole rows (no text
+    boundary inside a row), the rows tile the batch exactly, no head or tail;
+    refused for unaligned bases, lengths that no row length divides, and
+    batches whose texts outnumber the rows."""
+    cases = [(0x7f0000000000, 65536, 148, 992, 4, 16, 0, 65536), (0x7f0000000000, 300, 148, 992, 4, 32, 0, 65536),
+             (0x7f0000000000, 5000, 148, 1984, 8, 32, 0, 4096), (0x7f0000000020, 777, 148, 992, 4, 32, 0, 1024),
+             (0x7f0000000010, 300, 148, 992, 4, 32, 0, 65536), (0x7f0000000000, 100, 148, 992, 4, 32, 0, 1000),
+             (0x7f0000000000, 200_000, 148, 992, 4, 32, 0, 256), (0x7f0000000000, 3, 148, 992, 4, 16, 0, 1 << 24), (0x7f0000000000, 146816, 148, 992, 4, 16, 0, 256)]
+    out = planner(cases)
+    for (addr, count, G, R, NB, rowb, _, ln), o in zip(cases, out):
+        if addr % 32 or ln % 16 or count > G * R or ln < 256:
+            assert o is None, (addr, count, ln)
+            continue
+        head, L, rows, ctas, hi, lo, m, bh, tail = o
+        assert head == 0 and ln % L == 0 and L % rowb == 0 and L >= 256 and rows == count * (ln // L)
+        assert tail == count * ln
+        assert rows <= G * R and hi - lo <= 1 and hi <= NB * bh
+    assert out[0][1] == 32768          # cfg5: two rows of 32 KiB per 64 KiB text
