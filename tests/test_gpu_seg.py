@@ -330,3 +330,24 @@ def test_batch_host_end_to_end(torch_cuda):
     with pytest.raises(P.SFAError) as e:
         sfa.match_batch_host(texts, bad)
     assert e.value.code == P.SFA_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(cuda_ok, tool):
+    """compute-sanitizer over every kernel (scripts/sanitize_case.py): no
+    out-of-bounds or misaligned access, no shared-memory race, no barrier
+    misuse (results must not depend on scheduling)."""
+    import os
+    import shutil
+    import subprocess
+    import sys
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [cs, "--tool", tool, "--error-exitcode", "9", "--print-limit", "20"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "all"]
+    r = subprocess.run(cmd + [sys.executable, os.path.join(root, "scripts", "sanitize_case.py")],
+                       capture_output=True, text=True, timeout=1500)
+    tail = (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0 and "sanitize case ok" in r.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
