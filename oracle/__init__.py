@@ -18,6 +18,12 @@ passages it follows) through ctypes:
   DFA baseline, per-chunk mappings and the sequential reduction.
 * ``OracleSFA(dfa)`` -- Alg. 4, for SFA-level pins, and
   ``.run_chunked`` -- Alg. 5 with both reductions.
+* ``OracleNFA(regex, alphabet)`` / ``OracleNFA.explicit(...)`` -- the
+  eps-free view of the Thompson NFA, or an explicit NFA (the paper's Ex. 3);
+  ``.run`` is the NFA run by definition.
+* ``OracleNSFA(nfa)`` -- Alg. 4 in its general form (set-valued mappings, the
+  N-SFA) and Alg. 5 over it, the parallel reduction by
+  logical matrix products.
 """
 from __future__ import annotations
 
@@ -88,6 +94,23 @@ def lib():
         L.oracle_sfa_export.argtypes = [vp, u32p, u32p, u8p]
         L.oracle_sfa_run_chunked.argtypes = [vp, u8p, u64p, C.c_int, u32p, u32p, u32p]
         L.oracle_sfa_run_chunked.restype = C.c_int
+        L.oracle_nfa_compile.argtypes = [C.c_char_p, u8p, C.c_int, C.POINTER(vp), C.c_char_p, C.c_int]
+        L.oracle_nfa_compile.restype = C.c_int
+        L.oracle_nfa_explicit.argtypes = [C.c_int, u64p, C.c_uint64, C.c_uint64, u8p, C.c_int, C.POINTER(vp)]
+        L.oracle_nfa_explicit.restype = C.c_int
+        L.oracle_nfa_free.argtypes = [vp]
+        L.oracle_nfa_size.argtypes = [vp]
+        L.oracle_nfa_size.restype = C.c_uint32
+        L.oracle_nfa_run.argtypes = [vp, u8p, C.c_uint64, u64p]
+        L.oracle_nfa_run.restype = C.c_int
+        L.oracle_nfa_word_map.argtypes = [vp, u8p, C.c_int, u64p]
+        L.oracle_nsfa_build.argtypes = [vp, C.c_uint32, C.POINTER(vp)]
+        L.oracle_nsfa_build.restype = C.c_int
+        L.oracle_nsfa_free.argtypes = [vp]
+        L.oracle_nsfa_states.argtypes = [vp]
+        L.oracle_nsfa_states.restype = C.c_uint32
+        L.oracle_nsfa_run_chunked.argtypes = [vp, u8p, u64p, C.c_int, u32p, u64p, u64p]
+        L.oracle_nsfa_run_chunked.restype = C.c_int
         _lib = L
     return _lib
 
@@ -269,4 +292,107 @@ class OracleSFA:
         h = getattr(self, "_h", None)
         if h is not None and _lib is not None:
             _lib.oracle_sfa_free(h)
+            self._h = None
+
+
+def _bits_to_int(words: np.ndarray) -> int:
+    v = 0
+    for i, w in enumerate(words.tolist()):
+        v |= int(w) << (64 * i)
+    return v
+
+
+class OracleNFA:
+    """eps-free NFA (Thompson states; delta(q, b) = closure(move({q}, b)))."""
+
+    def __init__(self, regex=None, alphabet=None, _h=None):
+        L = lib()
+        if _h is None:
+            self._sig, slen = _sigma(alphabet)
+            h = C.c_void_p()
+            err = C.create_string_buffer(256)
+            rc = L.oracle_nfa_compile(regex.encode("latin-1"),
+                                      None if self._sig is None else _ptr(self._sig, C.c_uint8), slen, C.byref(h),
+                                      err, 256)
+            if rc != 0:
+                raise OracleError(rc, err.value.decode(errors="replace"))
+            _h = h
+        self._h = _h
+        self.n = L.oracle_nfa_size(_h)
+        self.W = (self.n + 63) // 64
+
+    @classmethod
+    def explicit(cls, n: int, delta: dict, initial: set, final: set, alphabet=None):
+        """delta: {(q, byte): set of successors}; states 0..n-1 (n <= 64)."""
+        d = np.zeros(n * 256, np.uint64)
+        for (q, b), succ in delta.items():
+            for t in succ:
+                d[q * 256 + b] |= np.uint64(1 << t)
+        sig, slen = _sigma(alphabet)
+        h = C.c_void_p()
+        rc = lib().oracle_nfa_explicit(n, _ptr(d, C.c_uint64), sum(1 << q for q in initial),
+                                       sum(1 << q for q in final), None if sig is None else _ptr(sig, C.c_uint8),
+                                       slen, C.byref(h))
+        if rc != 0:
+            raise OracleError(rc, "explicit NFA")
+        obj = cls(_h=h)
+        obj._sig = sig
+        return obj
+
+    def run(self, text):
+        """The NFA run: (accept, final set as an int bitmask over states)."""
+        a = _text(text)
+        buf = a if a.size else np.zeros(1, np.uint8)
+        out = np.zeros(self.W, np.uint64)
+        rc = lib().oracle_nfa_run(self._h, _ptr(buf, C.c_uint8), a.size, _ptr(out, C.c_uint64))
+        if rc < 0:
+            raise OracleError(-rc, "nfa run")
+        return bool(rc), _bits_to_int(out)
+
+    def word_map(self, w):
+        """f_w by simulation from every state: tuple of n int bitmasks."""
+        a = _text(w)
+        buf = a if a.size else np.zeros(1, np.uint8)
+        out = np.zeros(self.n * self.W, np.uint64)
+        lib().oracle_nfa_word_map(self._h, _ptr(buf, C.c_uint8), a.size, _ptr(out, C.c_uint64))
+        return tuple(_bits_to_int(out[q * self.W:(q + 1) * self.W]) for q in range(self.n))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.oracle_nfa_free(h)
+            self._h = None
+
+
+class OracleNSFA:
+    """N-SFA: Alg. 4 in its general form over an OracleNFA; canonical ids (C3)."""
+
+    def __init__(self, nfa: OracleNFA, cap: int = 1 << 20):
+        h = C.c_void_p()
+        rc = lib().oracle_nsfa_build(nfa._h, cap, C.byref(h))
+        if rc != 0:
+            raise OracleError(rc, "N-SFA construction")
+        self._h = h
+        self.nfa = nfa
+        self.n = lib().oracle_nsfa_states(h)
+
+    def run_chunked(self, text, bounds):
+        """Alg. 5: (chunk_ids, (acc_seq, set_seq), (acc_par, set_par))."""
+        a = _text(text)
+        b = np.ascontiguousarray(bounds, np.uint64)
+        p = b.size - 1
+        ids = np.zeros(max(p, 1), np.uint32)
+        ss = np.zeros(self.nfa.W, np.uint64)
+        sp = np.zeros(self.nfa.W, np.uint64)
+        buf = a if a.size else np.zeros(1, np.uint8)
+        rc = lib().oracle_nsfa_run_chunked(self._h, _ptr(buf, C.c_uint8), _ptr(b, C.c_uint64), p,
+                                           _ptr(ids, C.c_uint32), _ptr(ss, C.c_uint64), _ptr(sp, C.c_uint64))
+        if rc < 0:
+            raise OracleError(-rc, "nsfa run_chunked")
+        return ids[:p], (bool(rc & 1), _bits_to_int(ss)), (bool(rc & 2), _bits_to_int(sp))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.oracle_nsfa_free(h)
             self._h = None

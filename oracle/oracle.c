@@ -1008,3 +1008,302 @@ int oracle_sfa_run_chunked(const oracle_sfa* s, const uint8_t* text, const uint6
     free(ids); free(ff); free(tmp);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NFA and N-SFA                                       */
+/*                                                                          */
+/* The NFA is either the Thompson NFA of a regex, seen eps-free (PAPER.md:   */
+/* 156-169): Q = the Thompson states, delta(q, b) = closure(move({q}, b)),   */
+/* I = closure({start}), F = {end}; or an explicit eps-free NFA given by its */
+/* transition bitsets (the paper's Ex. 3 NFA).            */
+/* The N-SFA is Alg. 4 in its general form: a state is a  */
+/* mapping f: Q -> 2^Q, f_I(q) = {q}, line 6: f_next(q) = U_{q' in f(q)}     */
+/* delta(q', sigma), line 11: F_s = {f | exists q in I: f(q) cap F != 0};    */
+/* its composition f . g is the logical matrix product.      */
+/* ------------------------------------------------------------------------ */
+
+struct oracle_nfa {
+    int n, W;            /* states, words per bitset */
+    word* delta;         /* n * 256 * W: delta(q, b) */
+    word* I;             /* W */
+    word* F;             /* W */
+    uint8_t sigma[32];
+};
+
+void oracle_nfa_free(oracle_nfa* a) {
+    if (!a) return;
+    free(a->delta); free(a->I); free(a->F);
+    free(a);
+}
+
+uint32_t oracle_nfa_size(const oracle_nfa* a) { return (uint32_t)a->n; }
+
+static oracle_nfa* nfa_alloc(int n) {
+    oracle_nfa* a = (oracle_nfa*)calloc(1, sizeof(oracle_nfa));
+    if (!a) return NULL;
+    a->n = n;
+    a->W = (n + 63) / 64;
+    a->delta = (word*)calloc((size_t)n * 256 * a->W, sizeof(word));
+    a->I = (word*)calloc((size_t)a->W, sizeof(word));
+    a->F = (word*)calloc((size_t)a->W, sizeof(word));
+    if (!a->delta || !a->I || !a->F) { oracle_nfa_free(a); return NULL; }
+    return a;
+}
+
+int oracle_nfa_compile(const char* regex, const uint8_t* sigma, int sigma_len,
+                       oracle_nfa** out, char* err, int errlen) {
+    if (!regex || !out) { seterr(err, errlen, "null argument"); return E_ARG; }
+    *out = NULL;
+    Parser P;
+    int root = parse_regex(&P, regex, sigma, sigma_len);
+    if (root < 0) {
+        seterr(err, errlen, P.msg);
+        int e = P.err;
+        free(P.v);
+        return e;
+    }
+    Nfa N;
+    memset(&N, 0, sizeof N);
+    Frag f = build(&N, P.v, root);
+    if (N.err || N.n > 4096) { seterr(err, errlen, "NFA too large"); free(P.v); free(N.v); return E_CAP; }
+    oracle_nfa* a = nfa_alloc(N.n);
+    int* stack = (int*)malloc((size_t)N.n * sizeof(int));
+    if (!a || !stack) { oracle_nfa_free(a); free(stack); free(P.v); free(N.v); return E_CAP; }
+    int W = a->W;
+    for (int q = 0; q < N.n; q++) {
+        const NState* s = &N.v[q];
+        if (s->type != S_SET) continue;   /* eps / split states have no byte move */
+        for (int b = 0; b < 256; b++) {
+            if (!set_has(P.v[s->node].set, b)) continue;
+            word* d = a->delta + ((size_t)q * 256 + b) * W;
+            d[s->out1 >> 6] |= 1ull << (s->out1 & 63);
+            closure(&N, d, stack);
+        }
+    }
+    a->I[f.start >> 6] |= 1ull << (f.start & 63);
+    closure(&N, a->I, stack);
+    a->F[f.end >> 6] |= 1ull << (f.end & 63);
+    memcpy(a->sigma, P.sigma, 32);
+    free(stack); free(P.v); free(N.v);
+    *out = a;
+    return E_OK;
+}
+
+/* An explicit eps-free NFA of n <= 64 states: delta[q * 256 + b] = bitset of
+ * successors, I and F bitsets; Sigma as for oracle_compile. */
+int oracle_nfa_explicit(int n, const uint64_t* delta, uint64_t I, uint64_t F, const uint8_t* sigma,
+                        int sigma_len, oracle_nfa** out) {
+    *out = NULL;
+    if (n < 1 || n > 64 || !delta) return E_ARG;
+    oracle_nfa* a = nfa_alloc(n);
+    if (!a) return E_CAP;
+    for (size_t i = 0; i < (size_t)n * 256; i++) a->delta[i] = delta[i];
+    a->I[0] = I;
+    a->F[0] = F;
+    sigma_init(a->sigma, sigma, sigma_len);
+    *out = a;
+    return E_OK;
+}
+
+/* S <- U_{q in S} delta(q, b) */
+static void nfa_step(const oracle_nfa* a, const word* S, int b, word* out) {
+    memset(out, 0, (size_t)a->W * sizeof(word));
+    for (int w = 0; w < a->W; w++)
+        for (word m = S[w]; m; m &= m - 1) {
+            int q = w * 64 + __builtin_ctzll(m);
+            const word* d = a->delta + ((size_t)q * 256 + b) * a->W;
+            for (int v = 0; v < a->W; v++) out[v] |= d[v];
+        }
+}
+
+static int meets(const word* S, const word* F, int W) {
+    for (int w = 0; w < W; w++)
+        if (S[w] & F[w]) return 1;
+    return 0;
+}
+
+/* The NFA run (the definition): S <- I, then S <- U delta(q, b) per byte.
+ * Returns accept (0/1) or -E_CAP; final_set (W words, nullable). */
+int oracle_nfa_run(const oracle_nfa* a, const uint8_t* text, uint64_t n, uint64_t* final_set) {
+    word* S = (word*)malloc((size_t)a->W * sizeof(word));
+    word* T = (word*)malloc((size_t)a->W * sizeof(word));
+    if (!S || !T) { free(S); free(T); return -E_CAP; }
+    memcpy(S, a->I, (size_t)a->W * sizeof(word));
+    for (uint64_t i = 0; i < n; i++) {
+        nfa_step(a, S, text[i], T);
+        word* x = S; S = T; T = x;
+    }
+    int acc = meets(S, a->F, a->W);
+    if (final_set) memcpy(final_set, S, (size_t)a->W * sizeof(word));
+    free(S); free(T);
+    return acc;
+}
+
+struct oracle_nsfa {
+    const oracle_nfa* a;
+    uint32_t ns;
+    word* maps;        /* ns mappings of n rows of W words: maps + (s*n + q)*W = f_s(q) */
+    uint32_t* table;   /* ns * 256 */
+    uint8_t* finals;   /* ns */
+};
+
+void oracle_nsfa_free(oracle_nsfa* s) {
+    if (!s) return;
+    free(s->maps); free(s->table); free(s->finals);
+    free(s);
+}
+
+uint32_t oracle_nsfa_states(const oracle_nsfa* s) { return s->ns; }
+
+/* Alg. 4, general form; mapping rows as bitsets; canonical BFS numbering
+ * (C3: Sigma bytes ascending, then the out-of-Sigma bytes).  cap: at most
+ * that many mappings (3 = capacity otherwise). */
+int oracle_nsfa_build(const oracle_nfa* a, uint32_t cap, oracle_nsfa** out) {
+    *out = NULL;
+    const int n = a->n, W = a->W, MW = n * W;    /* words per mapping */
+    SetTab T;
+    memset(&T, 0, sizeof T);
+    T.W = MW;
+    word* f = (word*)calloc((size_t)MW, sizeof(word));
+    word* g = (word*)calloc((size_t)MW, sizeof(word));
+    uint32_t* tab = NULL;
+    size_t tabcap = 0;
+    int rc = E_OK, isnew;
+    if (!f || !g) { rc = E_CAP; goto fail; }
+    for (int q = 0; q < n; q++) f[(size_t)q * W + (q >> 6)] = 1ull << (q & 63);   /* f_I(q) = {q} */
+    if (settab_get(&T, f, &isnew) == UINT32_MAX) { rc = E_CAP; goto fail; }
+    uint32_t n0 = 0;
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) n0 = T.n;
+        for (uint32_t i = 0; i < T.n; i++) {
+            if ((size_t)(T.n + 1) * 256 > tabcap) {
+                size_t nc = tabcap ? tabcap : 256 * 64;
+                while (nc < (size_t)(T.n + 1) * 256) nc *= 2;
+                uint32_t* nt = (uint32_t*)realloc(tab, nc * sizeof(uint32_t));
+                if (!nt) { rc = E_CAP; goto fail; }
+                tab = nt;
+                tabcap = nc;
+            }
+            for (int b = 0; b < 256; b++) {
+                int in_sigma = set_has(a->sigma, b);
+                if (pass == 0 && !in_sigma) continue;
+                if (pass == 1 && in_sigma && i < n0) continue;
+                /* line 6: f_next(q) = U_{q' in f(q)} delta(q', sigma) */
+                for (int q = 0; q < n; q++) nfa_step(a, T.sets + (size_t)i * MW + (size_t)q * W, b, g + (size_t)q * W);
+                uint32_t id = settab_get(&T, g, &isnew);
+                if (id == UINT32_MAX) { rc = E_CAP; goto fail; }
+                if (T.n > cap) { rc = E_CAP; goto fail; }
+                tab[(size_t)i * 256 + b] = id;   /* line 7 */
+            }
+        }
+    }
+    {
+        oracle_nsfa* s = (oracle_nsfa*)calloc(1, sizeof(oracle_nsfa));
+        if (!s) { rc = E_CAP; goto fail; }
+        s->a = a;
+        s->ns = T.n;
+        s->maps = (word*)malloc((size_t)T.n * MW * sizeof(word));
+        s->table = (uint32_t*)malloc((size_t)T.n * 256 * sizeof(uint32_t));
+        s->finals = (uint8_t*)malloc(T.n);
+        word* S = (word*)calloc((size_t)W, sizeof(word));
+        if (!s->maps || !s->table || !s->finals || !S) { free(S); oracle_nsfa_free(s); rc = E_CAP; goto fail; }
+        memcpy(s->maps, T.sets, (size_t)T.n * MW * sizeof(word));
+        memcpy(s->table, tab, (size_t)T.n * 256 * sizeof(uint32_t));
+        for (uint32_t i = 0; i < T.n; i++) {
+            /* line 11: F_s = {f | exists q in I: f(q) cap F != 0} */
+            memset(S, 0, (size_t)W * sizeof(word));
+            for (int w = 0; w < W; w++)
+                for (word m = a->I[w]; m; m &= m - 1) {
+                    int q = w * 64 + __builtin_ctzll(m);
+                    for (int v = 0; v < W; v++) S[v] |= s->maps[(size_t)i * MW + (size_t)q * W + v];
+                }
+            s->finals[i] = (uint8_t)meets(S, a->F, W);
+        }
+        free(S);
+        *out = s;
+    }
+fail:
+    free(f); free(g); free(tab);
+    free(T.sets); free(T.slot);
+    return rc;
+}
+
+/* (f . g)(q) = U_{p in f(q)} g(p): the logical matrix product */
+static void bool_compose(const word* f, const word* g, int n, int W, word* out) {
+    memset(out, 0, (size_t)n * W * sizeof(word));
+    for (int q = 0; q < n; q++)
+        for (int w = 0; w < W; w++)
+            for (word m = f[(size_t)q * W + w]; m; m &= m - 1) {
+                int p = w * 64 + __builtin_ctzll(m);
+                for (int v = 0; v < W; v++) out[(size_t)q * W + v] |= g[(size_t)p * W + v];
+            }
+}
+
+/* Alg. 5 over an N-SFA with chunks [bounds[i], bounds[i+1]): per-chunk ids
+ * (lines 1-5), the sequential reduction S <- I, S <- U_{p in S} f_i(p)
+ * (right column) and the parallel one f_fin = f_1 . ... . f_p,
+ * S <- U_{q in I} f_fin(q) (left column).  Writes both final sets (W words
+ * each, nullable) and returns acc_seq | acc_par << 1, or -code. */
+int oracle_nsfa_run_chunked(const oracle_nsfa* s, const uint8_t* text, const uint64_t* bounds, int p,
+                            uint32_t* chunk_ids, uint64_t* set_seq, uint64_t* set_par) {
+    if (p < 1) return -E_ARG;
+    const oracle_nfa* a = s->a;
+    const int n = a->n, W = a->W, MW = n * W;
+    uint32_t* ids = (uint32_t*)malloc((size_t)p * sizeof(uint32_t));
+    word* S = (word*)malloc((size_t)W * sizeof(word));
+    word* T = (word*)malloc((size_t)W * sizeof(word));
+    word* ff = (word*)malloc((size_t)MW * sizeof(word));
+    word* tmp = (word*)malloc((size_t)MW * sizeof(word));
+    if (!ids || !S || !T || !ff || !tmp) { free(ids); free(S); free(T); free(ff); free(tmp); return -E_CAP; }
+    for (int i = 0; i < p; i++) {
+        uint32_t f = 0;
+        for (uint64_t j = bounds[i]; j < bounds[i + 1]; j++) f = s->table[(size_t)f * 256 + text[j]];
+        ids[i] = f;
+        if (chunk_ids) chunk_ids[i] = f;
+    }
+    memcpy(S, a->I, (size_t)W * sizeof(word));
+    for (int i = 0; i < p; i++) {
+        memset(T, 0, (size_t)W * sizeof(word));
+        for (int w = 0; w < W; w++)
+            for (word m = S[w]; m; m &= m - 1) {
+                int q = w * 64 + __builtin_ctzll(m);
+                for (int v = 0; v < W; v++) T[v] |= s->maps[(size_t)ids[i] * MW + (size_t)q * W + v];
+            }
+        memcpy(S, T, (size_t)W * sizeof(word));
+    }
+    int acc_seq = meets(S, a->F, W);
+    if (set_seq) memcpy(set_seq, S, (size_t)W * sizeof(word));
+    memcpy(ff, s->maps, (size_t)MW * sizeof(word));   /* id 0 = f_I */
+    for (int i = 0; i < p; i++) {
+        bool_compose(ff, s->maps + (size_t)ids[i] * MW, n, W, tmp);
+        memcpy(ff, tmp, (size_t)MW * sizeof(word));
+    }
+    memset(S, 0, (size_t)W * sizeof(word));
+    for (int w = 0; w < W; w++)
+        for (word m = a->I[w]; m; m &= m - 1) {
+            int q = w * 64 + __builtin_ctzll(m);
+            for (int v = 0; v < W; v++) S[v] |= ff[(size_t)q * W + v];
+        }
+    int acc_par = meets(S, a->F, W);
+    if (set_par) memcpy(set_par, S, (size_t)W * sizeof(word));
+    free(ids); free(S); free(T); free(ff); free(tmp);
+    return acc_seq | (acc_par << 1);
+}
+
+/* f_w for a word w by direct simulation from every state (brute-force pin
+ * for |N-SFA|: the distinct f_w over all words up to some length). */
+void oracle_nfa_word_map(const oracle_nfa* a, const uint8_t* w, int len, uint64_t* out) {
+    const int n = a->n, W = a->W;
+    word* S = (word*)malloc((size_t)W * sizeof(word));
+    word* T = (word*)malloc((size_t)W * sizeof(word));
+    for (int q = 0; q < n; q++) {
+        memset(S, 0, (size_t)W * sizeof(word));
+        S[q >> 6] = 1ull << (q & 63);
+        for (int i = 0; i < len; i++) {
+            nfa_step(a, S, w[i], T);
+            word* x = S; S = T; T = x;
+        }
+        memcpy(out + (size_t)q * W, S, (size_t)W * sizeof(word));
+    }
+    free(S); free(T);
+}

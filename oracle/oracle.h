@@ -86,6 +86,29 @@ void oracle_sfa_export(const oracle_sfa* s, uint32_t* table, uint32_t* maps, uin
 int oracle_sfa_run_chunked(const oracle_sfa* s, const uint8_t* text, const uint64_t* bounds,
                            int p, uint32_t* chunk_ids, uint32_t* q_seq, uint32_t* q_par);
 
+/* NFA and N-SFA (NEXT-3).  The NFA: the Thompson NFA of a regex seen
+ * eps-free (delta(q, b) = closure(move({q}, b)), I = closure({start}),
+ * F = {end}), or an explicit eps-free NFA (n <= 64, delta[q*256+b] successor
+ * bitsets).  The N-SFA: Alg. 4 in its general form (mappings Q -> 2^Q,
+ * PAPER.md:501-521), canonical BFS ids (C3); Alg. 5 with both reductions,
+ * the parallel one by logical matrix products.  Sets are
+ * bitsets of ceil(n/64) words. */
+typedef struct oracle_nfa oracle_nfa;
+typedef struct oracle_nsfa oracle_nsfa;
+int oracle_nfa_compile(const char* regex, const uint8_t* sigma, int sigma_len,
+                       oracle_nfa** out, char* err, int errlen);
+int oracle_nfa_explicit(int n, const uint64_t* delta, uint64_t I, uint64_t F, const uint8_t* sigma,
+                        int sigma_len, oracle_nfa** out);
+void oracle_nfa_free(oracle_nfa* a);
+uint32_t oracle_nfa_size(const oracle_nfa* a);
+int oracle_nfa_run(const oracle_nfa* a, const uint8_t* text, uint64_t n, uint64_t* final_set);
+void oracle_nfa_word_map(const oracle_nfa* a, const uint8_t* w, int len, uint64_t* out);
+int oracle_nsfa_build(const oracle_nfa* a, uint32_t cap, oracle_nsfa** out);
+void oracle_nsfa_free(oracle_nsfa* s);
+uint32_t oracle_nsfa_states(const oracle_nsfa* s);
+int oracle_nsfa_run_chunked(const oracle_nsfa* s, const uint8_t* text, const uint64_t* bounds, int p,
+                            uint32_t* chunk_ids, uint64_t* set_seq, uint64_t* set_par);
+
 #ifdef __cplusplus
 }
 #endif
