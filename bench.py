@@ -312,9 +312,9 @@ def spec_compare(torch, sfa, dtext, nbytes, sfa_ms, stream, warmup, expected):
 
 
 def single_text_config(torch, P, cfg, stream, steps, warmup, reps, peak, peak_kind, nsm, sm_mhz, spec=False,
-                       text_in=None):
+                       text_in=None, nsfa=False):
     rx, alpha, text = workload(cfg) if text_in is None else text_in
-    sfa = P.SFA(rx, alpha)
+    sfa = P.SFA(rx, alpha, nsfa=nsfa)
     dt = torch.from_numpy(text).cuda()
     res = torch.zeros(2, dtype=torch.int32, device="cuda")
     q, acc = sfa.match(dt, stream)
@@ -326,18 +326,37 @@ def single_text_config(torch, P, cfg, stream, steps, warmup, reps, peak, peak_ki
     n = text.size
     gbs = n / (ms * 1e-3) / 1e9
     info = sfa.info()
-    out = {"workload": CONFIG_NAMES[cfg], "bytes": int(n), "result": [q, bool(acc)],
+    out = {"workload": CONFIG_NAMES.get(cfg, rx), "bytes": int(n), "result": [q, bool(acc)],
            "value": gbs, "unit": UNIT, "ms_per_step": ms, "median_ms_per_step": med, "steps": steps,
            "single_launch": {"ms": one, "gbs": n / (one * 1e-3) / 1e9, "frac": n / (one * 1e-3) / 1e9 / peak,
                              "reps": reps, "how": "synchronised before each launch; launch-to-result events; median"},
            "roofline": roofline(gbs, peak, peak_kind, nsm, sm_mhz, "k_scan_tma (one launch per step)",
-                                ncu_traffic(f"cfg{cfg}"), int(n)),
+                                ncu_traffic(f"cfg{cfg}") if cfg else None, int(n)),
            "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
            "dfa_states": info["dfa_states"], "api": "sfa_match_async", "gpu_launches_per_step": 1}
     if spec:
         out["alg3_speculative"] = spec_compare(torch, sfa, dt, n, ms, stream, warmup, (q, acc))
     del dt
     sfa.close()
+    return out
+
+
+def nsfa_compare(torch, P, stream, steps, warmup, reps, peak, peak_kind, nsm, sm_mhz, n=11, nbytes=1 << 30):
+    """the paper's Ex. 3, matched with the
+    N-SFA built from the NFA (sfa_compile_nsfa) beside the D-SFA of its minimal
+    DFA (2^n states); both through the same kernels (1 GiB i.i.d. {a,l,p})."""
+    import workloads as W
+    rx, text = W.ex3_regex(n), W.ex3_text(n, nbytes)
+    out = {}
+    for name, nsfa in (("nsfa", True), ("dsfa", False)):
+        sfa = P.SFA(rx, b"alp", nsfa=nsfa)
+        info = sfa.info()
+        r = single_text_config(torch, P, 0, stream, steps, warmup, reps, peak, peak_kind, nsm, sm_mhz,
+                               text_in=(rx, b"alp", text), nsfa=nsfa)
+        r.update({"workload": f"Ex. 3, n = {n}: {rx} over {{a,l,p}}, 1 GiB i.i.d. text", "kind": name,
+                  "nfa_states": info["nfa_states"], "construction_s": info["dfa_seconds"] + info["sfa_seconds"]})
+        out[name] = r
+        sfa.close()
     return out
 
 
@@ -530,6 +549,8 @@ def main():
     ap.add_argument("--rn", action="store_true",
                     help="also run the r_n scalability family (r5..r127, r_a) with Alg. 3 beside it")
     ap.add_argument("--rn-bytes", type=int, default=1 << 30)
+    ap.add_argument("--no-nsfa", dest="nsfa", action="store_false",
+                    help="skip the N-SFA vs D-SFA line on the paper's Ex. 3")
     ap.add_argument("--spec", action="store_true",
                     help="also time the paper's baseline, Alg. 3 (speculative DFA), on each per-config text")
     args = ap.parse_args()
@@ -614,6 +635,9 @@ def main():
             per[f"cfg{c}"] = single_text_config(torch, P, c, stream, min(args.steps, 100) if c != 1 else 200,
                                                 args.warmup, args.single_reps, peak, peak_kind, nsm, sm_mhz,
                                                 spec=args.spec)
+    if args.nsfa:
+        per["ex3_n11"] = nsfa_compare(torch, P, stream, min(args.steps, 100), args.warmup, args.single_reps, peak,
+                                      peak_kind, nsm, sm_mhz)
     if per:
         line["per_config"] = per
     if args.rn:

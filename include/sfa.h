@@ -105,6 +105,9 @@ typedef struct {
     uint32_t range_lo, range_width; /* byte window of the PRIVATE layout (0 if n/a) */
     uint64_t device_table_bytes;    /* bytes of SFA tables held on the device    */
     double   dfa_seconds, sfa_seconds; /* host construction times (not the target) */
+    uint32_t kind;             /* 0: D-SFA (sfa_compile), 1: N-SFA (sfa_compile_nsfa) */
+    uint32_t nfa_states;       /* N-SFA: |Q_N| of the Glushkov NFA (positions + initial) */
+    uint32_t has_dfa;          /* 1: results carry the minimal DFA's canonical state */
 } sfa_info_t;
 
 /*
@@ -122,6 +125,23 @@ typedef struct {
  */
 SFA_API int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len,
                 uint32_t max_sfa, sfa_handle** out);
+
+/*
+ * sfa_compile_nsfa -- the N-SFA: Alg. 4 in its general form
+ * over the regex's Glushkov NFA N, a state being a mapping
+ * Q_N -> 2^Q_N (|Q_N| bitset rows), with no DFA in between; the composition
+ * '.' is the logical matrix product, built on the host into the
+ * composition table when |S| <= 4096 (else Lemma-1 replay on the device).
+ * Matching runs through the same kernels and calls as a D-SFA handle.  The
+ * minimal DFA is also built when it has <= 2^20 states (info.has_dfa): results
+ * then carry its canonical state (the DFA state of f_fin(I)); otherwise
+ * final_state is the N-SFA id and accept = [f_fin in F_s].  Not available on
+ * N-SFA handles (CAPACITY): VEC composition, sfa_match_map, sfa_match_host,
+ * sfa_match_speculative, sfa_export_sfa's maps.  Arguments and errors as
+ * sfa_compile.
+ */
+SFA_API int sfa_compile_nsfa(const char* regex, const uint8_t* alphabet, int alphabet_len,
+                             uint32_t max_sfa, sfa_handle** out);
 
 /* Releases the handle and its device memory (synchronises the device work
  * that used it).  NULL is a no-op. */

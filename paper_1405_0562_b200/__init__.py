@@ -52,6 +52,7 @@ class sfa_info_t(C.Structure):
         ("classes", C.c_uint32), ("sfa_depth", C.c_uint32), ("residency", C.c_uint32),
         ("compose_mode", C.c_uint32), ("range_lo", C.c_uint32), ("range_width", C.c_uint32),
         ("device_table_bytes", C.c_uint64), ("dfa_seconds", C.c_double), ("sfa_seconds", C.c_double),
+        ("kind", C.c_uint32), ("nfa_states", C.c_uint32), ("has_dfa", C.c_uint32),
     ]
 
 
@@ -72,7 +73,7 @@ INVALID_STATE = 0xFFFFFFFF
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
            "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform", "sfa_match_speculative",
-           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows", "sfa_match_batch_host")
+           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows", "sfa_match_batch_host", "sfa_compile_nsfa")
 
 _lib = None
 
@@ -86,6 +87,7 @@ def lib() -> C.CDLL:
         L = C.CDLL(LIB_PATH)
         vp, u8p, u32p, u64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
         L.sfa_compile.argtypes = [C.c_char_p, u8p, C.c_int, C.c_uint32, C.POINTER(vp)]
+        L.sfa_compile_nsfa.argtypes = [C.c_char_p, u8p, C.c_int, C.c_uint32, C.POINTER(vp)]
         L.sfa_free.argtypes = [vp]
         L.sfa_free.restype = None
         L.sfa_last_error.restype = C.c_char_p
@@ -144,17 +146,19 @@ def _nbytes(x) -> int:
 
 
 # --------------------------------------------------------------------------- C names
-def sfa_compile(regex, alphabet=None, max_sfa: int = 0) -> int:
-    """regex (str/bytes), alphabet (bytes or None = all 256 bytes) -> handle (int)."""
+def sfa_compile(regex, alphabet=None, max_sfa: int = 0, nsfa: bool = False) -> int:
+    """regex (str/bytes), alphabet (bytes or None = all 256 bytes) -> handle (int).
+    nsfa: the N-SFA of the Glushkov NFA (sfa_compile_nsfa) instead of the D-SFA."""
     rx = regex.encode("latin-1") if isinstance(regex, str) else bytes(regex)
     if b"\0" in rx:
         raise SFAError(SFA_ERR_INVALID_ARG, "regex contains NUL")
     h = C.c_void_p()
+    fn = lib().sfa_compile_nsfa if nsfa else lib().sfa_compile
     if alphabet is None:
-        rc = lib().sfa_compile(rx, None, 0, max_sfa, C.byref(h))
+        rc = fn(rx, None, 0, max_sfa, C.byref(h))
     else:
         al = np.frombuffer(bytes(alphabet), np.uint8).copy()
-        rc = lib().sfa_compile(rx, al.ctypes.data_as(C.POINTER(C.c_uint8)), al.size, max_sfa, C.byref(h))
+        rc = fn(rx, al.ctypes.data_as(C.POINTER(C.c_uint8)), al.size, max_sfa, C.byref(h))
     _check(rc)
     return h.value
 
@@ -320,6 +324,17 @@ def sfa_export_dfa(h: int):
     return table, finals
 
 
+def sfa_export_sfa_table(h: int):
+    """D-SFA or N-SFA: (table |S| x 256 ids, None, finals) -- no mapping export."""
+    info = sfa_info(h)
+    ns = info["sfa_states"]
+    table = np.zeros((ns, 256), np.uint32)
+    finals = np.zeros(ns, np.uint8)
+    _check(lib().sfa_export_sfa(h, table.ctypes.data_as(C.POINTER(C.c_uint32)), None,
+                                finals.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return table, None, finals
+
+
 def sfa_export_sfa(h: int):
     info = sfa_info(h)
     ns, nd = info["sfa_states"], info["dfa_states"]
@@ -336,8 +351,8 @@ def sfa_export_sfa(h: int):
 class SFA:
     """Owns one compiled handle: ``SFA(regex, alphabet)``."""
 
-    def __init__(self, regex, alphabet=None, max_sfa: int = 0):
-        self.h = sfa_compile(regex, alphabet, max_sfa)
+    def __init__(self, regex, alphabet=None, max_sfa: int = 0, nsfa: bool = False):
+        self.h = sfa_compile(regex, alphabet, max_sfa, nsfa)
         self._match_async = lib().sfa_match_async
 
     def close(self):

@@ -168,11 +168,13 @@ struct sfa_handle {
     }
 
     bool has_comp() const { return A.nS <= kCompMaxStates; }
+    // mapping vectors (VEC composition, sfa_match_map, q_in chaining): D-SFA only
+    bool can_vec() const { return !A.nsfa && A.nD <= 32; }
     // effective composition mode
     int compose_mode() const {
         if (compose != SFA_COMPOSE_AUTO) return compose;
         if (has_comp()) return SFA_COMPOSE_TABLE;
-        return A.nD <= 32 ? SFA_COMPOSE_VEC : SFA_COMPOSE_REPLAY;
+        return can_vec() ? SFA_COMPOSE_VEC : SFA_COMPOSE_REPLAY;
     }
     bool vec() const { return compose_mode() == SFA_COMPOSE_VEC; }
 
@@ -473,14 +475,14 @@ struct sfa_handle {
             CU(upload(&dTrange, padded.data(), padded.size()));
         }
         CU(upload(&dcls, A.cls, 256));
-        if (nD <= 32) {
+        if (can_vec()) {
             std::vector<uint8_t> m32(static_cast<size_t>(nS) * 32);
             for (uint32_t s = 0; s < nS; ++s)
                 for (uint32_t q = 0; q < 32; ++q)
                     m32[static_cast<size_t>(s) * 32 + q] = static_cast<uint8_t>(q < nD ? A.maps[static_cast<size_t>(s) * nD + q] : q);
             CU(upload(&dmaps32, m32.data(), m32.size()));
         }
-        if (nD <= 65535 && static_cast<uint64_t>(nS) * nD * 2 <= (1ull << 30)) {
+        if (!A.nsfa && nD <= 65535 && static_cast<uint64_t>(nS) * nD * 2 <= (1ull << 30)) {
             std::vector<uint16_t> m16(static_cast<size_t>(nS) * nD);
             for (size_t i = 0; i < m16.size(); ++i) m16[i] = static_cast<uint16_t>(A.maps[i]);
             CU(upload(&dmaps16, m16.data(), m16.size()));
@@ -494,8 +496,12 @@ struct sfa_handle {
             for (uint32_t a = 0; a < nS; ++a)
                 for (uint32_t b = 0; b < nS; ++b) {
                     uint32_t st = a;
-                    for (uint32_t k = A.rep_off[b]; k < A.rep_off[b + 1]; ++k)
-                        st = A.T[static_cast<size_t>(st) * C + A.cls[A.rep[k]]];
+                    if (!A.comp.empty()) {  // N-SFA: the logical matrix products of compile_nsfa
+                        st = A.comp[static_cast<size_t>(a) * nS + b];
+                    } else {
+                        for (uint32_t k = A.rep_off[b]; k < A.rep_off[b + 1]; ++k)
+                            st = A.T[static_cast<size_t>(st) * C + A.cls[A.rep[k]]];
+                    }
                     comp[static_cast<size_t>(a) * nS + b] = static_cast<uint16_t>(st);
                 }
             std::vector<uint8_t> bytes(cells * (u8 ? 1 : 2));
@@ -520,7 +526,7 @@ struct sfa_handle {
             }
             CU(upload(reinterpret_cast<uint8_t**>(&drep16), slots.data(), slots.size()));
         }
-        if (nD <= 32 && static_cast<size_t>(nS) * 32 <= kAuxMax) {
+        if (can_vec() && static_cast<size_t>(nS) * 32 <= kAuxMax) {
             std::vector<uint8_t> m32(static_cast<size_t>(nS) * 32);
             for (uint32_t st = 0; st < nS; ++st)
                 for (uint32_t q = 0; q < 32; ++q)
@@ -532,7 +538,7 @@ struct sfa_handle {
         {
             int rc = upload_hot(nullptr, 0);
             if (rc) return rc;
-            rc = upload_fact();
+            if (!A.nsfa) rc = upload_fact();
             if (rc) return rc;
             dev_bytes += static_cast<uint64_t>(nS) * W * 2 + 4ull * nS;
         }
@@ -767,6 +773,7 @@ struct sfa_handle {
     // window (one class, so any such byte represents it).
     int upload_spec() {
         if (dspecT) return SFA_OK;
+        if (!A.has_dfa || A.nsfa) return fail(SFA_ERR_CAPACITY, "Alg. 3 needs a D-SFA handle");
         const uint32_t nD = A.nD;
         uint32_t ob = 0;
         while (ob >= lo && ob + 1 < lo + W) ++ob;  // a byte outside [lo, lo + W - 2]
@@ -801,7 +808,8 @@ extern "C" {
 
 const char* sfa_last_error(void) { return g_err.c_str(); }
 
-int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa, sfa_handle** out) {
+static int compile_any(bool nsfa, const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa,
+                       sfa_handle** out) {
     if (!out) return fail(SFA_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (!regex) return fail(SFA_ERR_INVALID_ARG, "regex is NULL");
@@ -809,7 +817,8 @@ int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len, ui
     sfa_handle* h = new (std::nothrow) sfa_handle;
     if (!h) return fail(SFA_ERR_OOM, "host allocation failed");
     try {
-        h->A = sfa::compile_regex(regex, alphabet, alphabet ? alphabet_len : -1, max_sfa);
+        h->A = nsfa ? sfa::compile_nsfa(regex, alphabet, alphabet ? alphabet_len : -1, max_sfa)
+                    : sfa::compile_regex(regex, alphabet, alphabet ? alphabet_len : -1, max_sfa);
     } catch (const sfa::CompileError& e) {
         delete h;
         return fail(e.code, e.what());
@@ -842,6 +851,15 @@ int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len, ui
     return SFA_OK;
 }
 
+int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa, sfa_handle** out) {
+    return compile_any(false, regex, alphabet, alphabet_len, max_sfa, out);
+}
+
+int sfa_compile_nsfa(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa,
+                     sfa_handle** out) {
+    return compile_any(true, regex, alphabet, alphabet_len, max_sfa, out);
+}
+
 void sfa_free(sfa_handle* h) { delete h; }
 
 int sfa_info(const sfa_handle* h, sfa_info_t* info) {
@@ -867,6 +885,9 @@ int sfa_info(const sfa_handle* h, sfa_info_t* info) {
     info->device_table_bytes = h->dev_bytes;
     info->dfa_seconds = A.dfa_seconds;
     info->sfa_seconds = A.sfa_seconds;
+    info->kind = A.nsfa ? 1u : 0u;
+    info->nfa_states = A.nfa_states;
+    info->has_dfa = A.has_dfa ? 1u : 0u;
     return SFA_OK;
 }
 
@@ -904,7 +925,7 @@ int sfa_tune_residency(sfa_handle* h, const uint8_t* d_sample, size_t n, sfa_str
 int sfa_set_compose(sfa_handle* h, int mode) {
     if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
     if (mode < SFA_COMPOSE_AUTO || mode > SFA_COMPOSE_REPLAY) return fail(SFA_ERR_INVALID_ARG, "bad compose mode");
-    if (mode == SFA_COMPOSE_VEC && h->A.nD > 32) return fail(SFA_ERR_CAPACITY, "VEC composition needs |D| <= 32");
+    if (mode == SFA_COMPOSE_VEC && !h->can_vec()) return fail(SFA_ERR_CAPACITY, "VEC composition needs a D-SFA with |D| <= 32");
     if (mode == SFA_COMPOSE_TABLE && !h->has_comp()) return fail(SFA_ERR_CAPACITY, "composition table needs |S| <= 4096");
     std::lock_guard<std::mutex> lk(h->mu);
     h->compose = mode;
@@ -933,6 +954,7 @@ int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* tu) {
 
 int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals) {
     if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (!h->A.has_dfa) return fail(SFA_ERR_CAPACITY, "this N-SFA handle has no DFA (more than 2^20 states)");
     if (table) std::memcpy(table, h->A.dfa.data(), h->A.dfa.size() * sizeof(uint32_t));
     if (finals) std::memcpy(finals, h->A.dfa_final.data(), h->A.dfa_final.size());
     return SFA_OK;
@@ -944,6 +966,7 @@ int sfa_export_sfa(const sfa_handle* h, uint32_t* table, uint32_t* maps, uint8_t
     if (table)
         for (uint32_t s = 0; s < A.nS; ++s)
             for (int b = 0; b < 256; ++b) table[static_cast<size_t>(s) * 256 + b] = A.T[static_cast<size_t>(s) * A.C + A.cls[b]];
+    if (maps && A.nsfa) return fail(SFA_ERR_CAPACITY, "N-SFA states are set-valued mappings (no |D| map)");
     if (maps) std::memcpy(maps, A.maps.data(), A.maps.size() * sizeof(uint32_t));
     if (finals) std::memcpy(finals, A.acc.data(), A.acc.size());
     return SFA_OK;
@@ -1059,7 +1082,7 @@ int sfa_match_map(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_str
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int rc = h->begin(s);
     if (rc) return rc;
-    if (!h->vec() && !h->dmaps16) return fail(SFA_ERR_CAPACITY, "mapping table too large for sfa_match_map");
+    if (!h->vec() && !h->dmaps16) return fail(SFA_ERR_CAPACITY, "no mapping table for sfa_match_map (N-SFA or too large)");
     if (n == 0) {  // f_eps = identity
         cudaError_t e = sfa::launch_fill_result(nullptr, 0, 0, d_map, h->A.nD, s);
         if (e != cudaSuccess) return cuda_fail(e, "fill launch");

@@ -486,12 +486,20 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-}  // namespace
-
-Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa) {
-    auto t0 = std::chrono::steady_clock::now();
-    Automata A;
+// The parts of a compile shared by the D-SFA and the N-SFA: Sigma, the
+// Glushkov NFA and its byte classes (bytes no position set distinguishes).
+struct Front {
     ByteSet sig{};
+    Glushkov g;
+    std::array<uint32_t, 256> ncls{};
+    uint32_t K = 1;
+    std::vector<int> krep;
+    std::vector<std::vector<uint64_t>> posmask;  // positions whose set contains class k
+};
+
+Front make_front(Automata& A, const std::string& regex, const uint8_t* sigma, int sigma_len) {
+    Front F;
+    ByteSet& sig = F.sig;
     if (sigma == nullptr || sigma_len < 0) sig = bs_not(ByteSet{});
     else
         for (int i = 0; i < sigma_len; ++i) bs_set(sig, sigma[i]);
@@ -501,14 +509,14 @@ Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma
     // ---- parse + Glushkov ----
     std::vector<Node> nodes;
     int root = Parser(regex, sig, nodes).parse();
-    Glushkov g;
+    Glushkov& g = F.g;
     GlushkovBuilder(nodes, g).build(root);
     nodes.clear();
     nodes.shrink_to_fit();
     A.nfa_positions = g.m;
 
     // ---- NFA byte classes: bytes indistinguishable by every position's set ----
-    std::array<uint32_t, 256> ncls{};
+    std::array<uint32_t, 256>& ncls = F.ncls;
     uint32_t K = 1;
     for (uint32_t p = 1; p <= g.m; ++p) {
         std::unordered_map<uint64_t, uint32_t> remap;
@@ -523,15 +531,26 @@ Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma
         ncls = nc;
         K = k2;
     }
-    std::vector<int> krep(K, -1);
+    F.K = K;
+    F.krep.assign(K, -1);
     for (int b = 0; b < 256; ++b)
-        if (krep[ncls[b]] < 0) krep[ncls[b]] = b;
-    // positions whose set contains class k
-    std::vector<std::vector<uint64_t>> posmask(K, std::vector<uint64_t>(g.W, 0));
+        if (F.krep[ncls[b]] < 0) F.krep[ncls[b]] = b;
+    F.posmask.assign(K, std::vector<uint64_t>(g.W, 0));
     for (uint32_t k = 0; k < K; ++k)
         for (uint32_t p = 1; p <= g.m; ++p)
-            if (bs_has(g.chars[p], krep[k])) posmask[k][p >> 6] |= 1ull << (p & 63);
+            if (bs_has(g.chars[p], F.krep[k])) F.posmask[k][p >> 6] |= 1ull << (p & 63);
+    return F;
+}
 
+// Alg. 1 (subset construction over the NFA classes) ->
+// Hopcroft minimisation -> canonical numbering (C3): the DFA fields of A.
+// Throws CompileError(capacity) past kMaxDfa subsets.
+void build_min_dfa(Automata& A, const Front& F) {
+    const ByteSet& sig = F.sig;
+    const Glushkov& g = F.g;
+    const std::array<uint32_t, 256>& ncls = F.ncls;
+    const uint32_t K = F.K;
+    const std::vector<std::vector<uint64_t>>& posmask = F.posmask;
     // ---- Alg. 1: subset construction over NFA classes ----
     std::vector<std::vector<uint64_t>> dstates;
     std::unordered_map<std::vector<uint64_t>, uint32_t, VecHash> index;
@@ -618,6 +637,17 @@ Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma
         for (int b = 0; b < 256 && absorbing; ++b) absorbing = A.dfa[static_cast<size_t>(i) * 256 + b] == i;
         if (absorbing) A.dead = static_cast<int32_t>(i);
     }
+}
+
+}  // namespace
+
+Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa) {
+    auto t0 = std::chrono::steady_clock::now();
+    Automata A;
+    Front F = make_front(A, regex, sigma, sigma_len);
+    const ByteSet& sig = F.sig;
+    build_min_dfa(A, F);
+    const uint32_t nb = A.nD;
     A.dfa_seconds = seconds_since(t0);
     auto t1 = std::chrono::steady_clock::now();
 
@@ -727,6 +757,180 @@ Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma
         uint32_t p = parent[s];
         std::copy(A.rep.begin() + A.rep_off[p], A.rep.begin() + A.rep_off[p + 1], A.rep.begin() + A.rep_off[s]);
         A.rep[A.rep_off[s + 1] - 1] = A.rep_byte[pclass[s]];
+    }
+    A.sfa_seconds = seconds_since(t1);
+    return A;
+}
+
+// ------------------------------------------------------------------------------------------
+// N-SFA: Alg. 4 over the Glushkov NFA N = (Q, Sigma,
+// delta, I = {0}, F): a state is a mapping f: Q -> 2^Q stored as |Q| bitset
+// rows; f_I(q) = {q}; line 6: f_next(q) = U_{q' in f(q)} delta(q', sigma),
+// delta(q', k) = follow(q') & positions of class k; line 11: f in F_s iff
+// f(0) meets F.  Canonical numbering as the D-SFA (C3).  The composition
+// f . g is the logical matrix product
+// (f . g)(q) = U_{p in f(q)} g(p).
+// ------------------------------------------------------------------------------------------
+Automata compile_nsfa(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa) {
+    auto t0 = std::chrono::steady_clock::now();
+    Automata A;
+    Front F = make_front(A, regex, sigma, sigma_len);
+    const Glushkov& g = F.g;
+    try {  // the minimal DFA, for canonical final states (C3); optional
+        build_min_dfa(A, F);
+    } catch (const CompileError& e) {
+        if (e.code != kCapacity) throw;
+        A.has_dfa = false;
+        A.nD = 0;
+        A.dfa.clear();
+        A.dfa_final.clear();
+        A.dead = -1;
+    }
+    A.dfa_seconds = seconds_since(t0);
+    auto t1 = std::chrono::steady_clock::now();
+    A.nsfa = true;
+    const uint32_t Q = g.m + 1, W = g.W, MW = Q * W, K = F.K;
+    A.nfa_states = Q;
+    // table columns: the NFA byte classes; representative bytes prefer Sigma
+    A.C = K;
+    for (int b = 0; b < 256; ++b) A.cls[b] = static_cast<uint8_t>(F.ncls[b]);
+    {
+        std::vector<int> rep(K, -1);
+        for (int b = 0; b < 256; ++b)
+            if (bs_has(F.sig, b) && rep[F.ncls[b]] < 0) rep[F.ncls[b]] = b;
+        for (uint32_t k = 0; k < K; ++k) A.rep_byte[k] = static_cast<uint8_t>(rep[k] >= 0 ? rep[k] : F.krep[k]);
+    }
+    // delta(q, k) as W-word bitsets
+    std::vector<uint64_t> dq(static_cast<size_t>(Q) * K * W);
+    for (uint32_t q = 0; q < Q; ++q)
+        for (uint32_t k = 0; k < K; ++k)
+            for (uint32_t w = 0; w < W; ++w) dq[(static_cast<size_t>(q) * K + k) * W + w] = g.follow[q][w] & F.posmask[k][w];
+    std::vector<uint32_t> sig_order;
+    std::vector<uint8_t> has_sigma(K, 0);
+    for (int b = 0; b < 256; ++b)
+        if (bs_has(F.sig, b) && !has_sigma[F.ncls[b]]) {
+            has_sigma[F.ncls[b]] = 1;
+            sig_order.push_back(F.ncls[b]);
+        }
+    const uint32_t cap = max_sfa ? std::min<uint32_t>(max_sfa, 65535u) : 65535u;
+    std::vector<uint64_t> mp;  // nS * MW
+    std::vector<uint32_t> slots(1024, UINT32_MAX), parent, pclass;
+    auto hash_m = [&](const uint64_t* f) {
+        uint64_t h = 0x9E3779B97F4A7C15ull;
+        for (uint32_t i = 0; i < MW; ++i) h = (h ^ f[i]) * 0xBF58476D1CE4E5B9ull, h ^= h >> 29;
+        return h;
+    };
+    auto find = [&](const uint64_t* f) -> uint32_t {
+        size_t k = hash_m(f) & (slots.size() - 1);
+        while (slots[k] != UINT32_MAX) {
+            if (std::memcmp(&mp[static_cast<size_t>(slots[k]) * MW], f, MW * sizeof(uint64_t)) == 0) return slots[k];
+            k = (k + 1) & (slots.size() - 1);
+        }
+        return UINT32_MAX;
+    };
+    auto intern = [&](const uint64_t* f, uint32_t from, uint32_t via) -> uint32_t {
+        if ((A.nS + 1) * 2 > slots.size()) {
+            std::vector<uint32_t> ns(slots.size() * 2, UINT32_MAX);
+            for (uint32_t s = 0; s < A.nS; ++s) {
+                size_t k = hash_m(&mp[static_cast<size_t>(s) * MW]) & (ns.size() - 1);
+                while (ns[k] != UINT32_MAX) k = (k + 1) & (ns.size() - 1);
+                ns[k] = s;
+            }
+            slots.swap(ns);
+        }
+        size_t k = hash_m(f) & (slots.size() - 1);
+        while (slots[k] != UINT32_MAX) {
+            if (std::memcmp(&mp[static_cast<size_t>(slots[k]) * MW], f, MW * sizeof(uint64_t)) == 0) return slots[k];
+            k = (k + 1) & (slots.size() - 1);
+        }
+        if (A.nS >= cap) throw CompileError(kCapacity, "N-SFA has more than " + std::to_string(cap) + " states");
+        slots[k] = A.nS;
+        mp.insert(mp.end(), f, f + MW);
+        A.T.resize(A.T.size() + K, UINT32_MAX);
+        parent.push_back(from);
+        pclass.push_back(via);
+        return A.nS++;
+    };
+    {
+        std::vector<uint64_t> f(MW, 0), gn(MW);
+        for (uint32_t q = 0; q < Q; ++q) f[static_cast<size_t>(q) * W + (q >> 6)] = 1ull << (q & 63);  // f_I(q) = {q}
+        intern(f.data(), UINT32_MAX, UINT32_MAX);
+        for (int pass = 0; pass < 2; ++pass) {
+            const uint32_t n0 = A.nS;
+            for (uint32_t i = 0; i < A.nS; ++i) {
+                auto visit = [&](uint32_t c) {
+                    const uint64_t* fm = &mp[static_cast<size_t>(i) * MW];
+                    std::fill(gn.begin(), gn.end(), 0);
+                    for (uint32_t q = 0; q < Q; ++q)  // line 6: f_next(q) = U_{q' in f(q)} delta(q', sigma)
+                        for (uint32_t w = 0; w < W; ++w)
+                            for (uint64_t bits = fm[static_cast<size_t>(q) * W + w]; bits; bits &= bits - 1) {
+                                const uint32_t p = w * 64 + __builtin_ctzll(bits);
+                                const uint64_t* d = &dq[(static_cast<size_t>(p) * K + c) * W];
+                                for (uint32_t v = 0; v < W; ++v) gn[static_cast<size_t>(q) * W + v] |= d[v];
+                            }
+                    const uint32_t id = intern(gn.data(), i, c);
+                    A.T[static_cast<size_t>(i) * K + c] = id;  // line 7
+                };
+                if (pass == 0) {
+                    for (uint32_t c : sig_order) visit(c);
+                } else {
+                    for (uint32_t c = 0; c < K; ++c)
+                        if (!(has_sigma[c] && i < n0)) visit(c);
+                }
+            }
+        }
+    }
+    // rep words (Lemma 1 replay), F_s (line 11), the final-state map
+    A.rep_off.assign(A.nS + 1, 0);
+    std::vector<uint32_t> len(A.nS, 0);
+    for (uint32_t s = 1; s < A.nS; ++s) len[s] = len[parent[s]] + 1;
+    for (uint32_t s = 0; s < A.nS; ++s) {
+        A.rep_off[s + 1] = A.rep_off[s] + len[s];
+        A.depth = std::max(A.depth, len[s]);
+    }
+    A.rep.resize(A.rep_off[A.nS]);
+    for (uint32_t s = 1; s < A.nS; ++s) {
+        const uint32_t p = parent[s];
+        std::copy(A.rep.begin() + A.rep_off[p], A.rep.begin() + A.rep_off[p + 1], A.rep.begin() + A.rep_off[s]);
+        A.rep[A.rep_off[s + 1] - 1] = A.rep_byte[pclass[s]];
+    }
+    A.acc.resize(A.nS);
+    A.img0.resize(A.nS);
+    for (uint32_t s = 0; s < A.nS; ++s) {
+        bool fin = false;
+        for (uint32_t w = 0; w < W; ++w) fin = fin || (mp[static_cast<size_t>(s) * MW + w] & g.finals[w]);  // f(0) cap F
+        A.acc[s] = fin ? 1 : 0;
+        if (A.has_dfa) {  // the minimal DFA's state after rep(s): f_s(I) is that state's subset
+            uint32_t q = 0;
+            for (uint32_t k = A.rep_off[s]; k < A.rep_off[s + 1]; ++k) q = A.dfa[static_cast<size_t>(q) * 256 + A.rep[k]];
+            A.img0[s] = q;
+        } else {
+            A.img0[s] = s;
+        }
+    }
+    if (!A.has_dfa) {  // results are (N-SFA id, [id in F_s])
+        A.nD = A.nS;
+        A.dfa_final = A.acc;
+    }
+    // composition table by logical matrix products (|S| <= 4096)
+    if (A.nS <= 4096) {
+        A.comp.assign(static_cast<size_t>(A.nS) * A.nS, 0);
+        std::vector<uint64_t> h(MW);
+        for (uint32_t a = 0; a < A.nS; ++a)
+            for (uint32_t b = 0; b < A.nS; ++b) {
+                const uint64_t* fa = &mp[static_cast<size_t>(a) * MW];
+                const uint64_t* fb = &mp[static_cast<size_t>(b) * MW];
+                std::fill(h.begin(), h.end(), 0);
+                for (uint32_t q = 0; q < Q; ++q)
+                    for (uint32_t w = 0; w < W; ++w)
+                        for (uint64_t bits = fa[static_cast<size_t>(q) * W + w]; bits; bits &= bits - 1) {
+                            const uint32_t p = w * 64 + __builtin_ctzll(bits);
+                            for (uint32_t v = 0; v < W; ++v) h[static_cast<size_t>(q) * W + v] |= fb[static_cast<size_t>(p) * W + v];
+                        }
+                const uint32_t id = find(h.data());  // the transition monoid is closed (Lemma 1)
+                if (id == UINT32_MAX) throw CompileError(kCapacity, "N-SFA composition not closed");
+                A.comp[static_cast<size_t>(a) * A.nS + b] = id;
+            }
     }
     A.sfa_seconds = seconds_since(t1);
     return A;

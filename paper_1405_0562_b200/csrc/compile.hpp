@@ -46,9 +46,21 @@ struct Automata {
     uint32_t depth = 0;              // max |rep(s)|
 
     double dfa_seconds = 0, sfa_seconds = 0;
+
+    // ---- N-SFA (compile_nsfa): T/rep/acc as above, but a state is a mapping
+    // Q_N -> 2^Q_N of the Glushkov NFA (no `maps`); img0[s] = the minimal DFA's
+    // state after rep(s) when the DFA was built (has_dfa), else s (and then
+    // nD = nS, dfa_final = acc).  comp: the composition table by logical
+    // matrix products (|S| <= 4096), else empty.
+    bool nsfa = false, has_dfa = true;
+    uint32_t nfa_states = 0;        // |Q_N| (Glushkov positions + the initial state)
+    std::vector<uint32_t> comp;     // nS * nS
 };
 
 // Throws CompileError.  sigma == nullptr means all 256 bytes.
 Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa);
+// The N-SFA of the regex's Glushkov NFA by Alg. 4 in its general form
+// (PAPER.md:481-521); the minimal DFA too when it has <= 2^20 states.
+Automata compile_nsfa(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa);
 
 }  // namespace sfa

@@ -263,3 +263,15 @@ def ra_regex(n: int) -> str:
 
 def ra_text(nbytes: int = RN_BYTES) -> np.ndarray:
     return np.full(nbytes, 97, np.uint8)
+
+
+# --------------------------------------------------------------------------- Ex. 3
+# [ap]*[al][alp]{n-2} over {a, l, p}; the minimal DFA has 2^n
+# states.  Text: i.i.d. uniform over {a, l, p}, SeedSequence(3000 + n).
+def ex3_regex(n: int) -> str:
+    return "[ap]*[al][alp]{%d}" % (n - 2)
+
+
+def ex3_text(n: int, nbytes: int) -> np.ndarray:
+    rng = np.random.default_rng(np.random.SeedSequence(3000 + n))
+    return np.frombuffer(b"alp", np.uint8)[rng.integers(0, 3, size=nbytes)]
