@@ -105,9 +105,11 @@ typedef struct {
     uint32_t range_lo, range_width; /* byte window of the PRIVATE layout (0 if n/a) */
     uint64_t device_table_bytes;    /* bytes of SFA tables held on the device    */
     double   dfa_seconds, sfa_seconds; /* host construction times (not the target) */
-    uint32_t kind;             /* 0: D-SFA (sfa_compile), 1: N-SFA (sfa_compile_nsfa) */
+    uint32_t kind;             /* 0: D-SFA (sfa_compile), 1: N-SFA (sfa_compile_nsfa), 2: on the fly (sfa_compile_lazy) */
     uint32_t nfa_states;       /* N-SFA: |Q_N| of the Glushkov NFA (positions + initial) */
     uint32_t has_dfa;          /* 1: results carry the minimal DFA's canonical state */
+    uint64_t lazy_transitions; /* on the fly: SFA transitions built so far (sfa_states: states built) */
+    double   lazy_seconds;     /* on the fly: host time spent building them inside sfa_match_lazy */
 } sfa_info_t;
 
 /*
@@ -142,6 +144,33 @@ SFA_API int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet
  */
 SFA_API int sfa_compile_nsfa(const char* regex, const uint8_t* alphabet, int alphabet_len,
                              uint32_t max_sfa, sfa_handle** out);
+
+/*
+ * On-the-fly construction.
+ *
+ * sfa_compile_lazy -- builds only the minimal DFA (Alg. 1 + minimisation);
+ * the D-SFA is built while matching, one state and one transition at a time
+ * (Alg. 4 lines 6-8 for the (f, sigma) a chunk of text meets), with 32-bit ids
+ * in discovery order, so SFAs far beyond the eager tables' 65,535 states
+ * (r_500: 1,000,999) match with only their visited part
+ * built.  max_states: cap on states built (0 = 2^24; CAPACITY when reached
+ * during a match).  Needs |D| <= 65535.  Such a handle only matches with
+ * sfa_match_lazy (the other calls return INVALID_ARG); sfa_info reports kind
+ * 2, the states and transitions built, and the host time spent building.
+ *
+ * sfa_match_lazy -- one text in device memory (d_text, n bytes, caller-owned),
+ * blocking: rounds of a device scan of every unfinished chunk (SPEC's rule,
+ * <= 1024 chunks per SM) that stops at the first transition not built yet,
+ * and host construction of the transitions the stalled chunks need (the next
+ * 4 KiB of text of each); then the chunk states are folded as mapping vectors
+ * (a pairwise tree of (f . g)(q) = g(f(q))) and applied to q0.
+ * Results are the canonical (q_final, accept) of Alg. 2 (Theorem 2).  Built
+ * states persist in the handle.
+ */
+SFA_API int sfa_compile_lazy(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_states,
+                             sfa_handle** out);
+SFA_API int sfa_match_lazy(const sfa_handle* h, const uint8_t* d_text, size_t n, sfa_stream_t stream,
+                           uint32_t* final_state, int* accept);
 
 /* Releases the handle and its device memory (synchronises the device work
  * that used it).  NULL is a no-op. */
@@ -328,7 +357,9 @@ SFA_API int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* t);
 SFA_API int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals);
 
 /* D-SFA: table |S|*256 canonical SFA ids, maps |S|*|D| (row s = f_s),
- * finals |S| (s in F_s).  Any pointer may be NULL. */
+ * finals |S| (s in F_s).  Any pointer may be NULL.  On-the-fly handles: the
+ * states built so far (sfa_info().sfa_states, discovery order), transitions
+ * not built yet as UINT32_MAX. */
 SFA_API int sfa_export_sfa(const sfa_handle* h, uint32_t* table, uint32_t* maps, uint8_t* finals);
 
 #ifdef __cplusplus

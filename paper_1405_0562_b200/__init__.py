@@ -53,6 +53,7 @@ class sfa_info_t(C.Structure):
         ("compose_mode", C.c_uint32), ("range_lo", C.c_uint32), ("range_width", C.c_uint32),
         ("device_table_bytes", C.c_uint64), ("dfa_seconds", C.c_double), ("sfa_seconds", C.c_double),
         ("kind", C.c_uint32), ("nfa_states", C.c_uint32), ("has_dfa", C.c_uint32),
+        ("lazy_transitions", C.c_uint64), ("lazy_seconds", C.c_double),
     ]
 
 
@@ -73,7 +74,8 @@ INVALID_STATE = 0xFFFFFFFF
 EXPORTS = ("sfa_compile", "sfa_free", "sfa_last_error", "sfa_info", "sfa_match", "sfa_match_async",
            "sfa_match_batch", "sfa_match_host", "sfa_match_chunked", "sfa_set_residency", "sfa_set_compose",
            "sfa_tune_residency", "sfa_match_map", "sfa_combine_maps", "sfa_match_batch_uniform", "sfa_match_speculative",
-           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows", "sfa_match_batch_host", "sfa_compile_nsfa")
+           "sfa_export_dfa", "sfa_export_sfa", "sfa_set_tuning", "sfa_match_rows", "sfa_match_batch_host", "sfa_compile_nsfa", "sfa_compile_lazy",
+           "sfa_match_lazy")
 
 _lib = None
 
@@ -88,6 +90,8 @@ def lib() -> C.CDLL:
         vp, u8p, u32p, u64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
         L.sfa_compile.argtypes = [C.c_char_p, u8p, C.c_int, C.c_uint32, C.POINTER(vp)]
         L.sfa_compile_nsfa.argtypes = [C.c_char_p, u8p, C.c_int, C.c_uint32, C.POINTER(vp)]
+        L.sfa_compile_lazy.argtypes = [C.c_char_p, u8p, C.c_int, C.c_uint32, C.POINTER(vp)]
+        L.sfa_match_lazy.argtypes = [vp, vp, C.c_size_t, vp, u32p, C.POINTER(C.c_int)]
         L.sfa_free.argtypes = [vp]
         L.sfa_free.restype = None
         L.sfa_last_error.restype = C.c_char_p
@@ -146,14 +150,15 @@ def _nbytes(x) -> int:
 
 
 # --------------------------------------------------------------------------- C names
-def sfa_compile(regex, alphabet=None, max_sfa: int = 0, nsfa: bool = False) -> int:
+def sfa_compile(regex, alphabet=None, max_sfa: int = 0, nsfa: bool = False, lazy: bool = False) -> int:
     """regex (str/bytes), alphabet (bytes or None = all 256 bytes) -> handle (int).
-    nsfa: the N-SFA of the Glushkov NFA (sfa_compile_nsfa) instead of the D-SFA."""
+    nsfa: the N-SFA of the Glushkov NFA (sfa_compile_nsfa) instead of the D-SFA;
+    lazy: the DFA only, the D-SFA built on the fly while matching (sfa_compile_lazy)."""
     rx = regex.encode("latin-1") if isinstance(regex, str) else bytes(regex)
     if b"\0" in rx:
         raise SFAError(SFA_ERR_INVALID_ARG, "regex contains NUL")
     h = C.c_void_p()
-    fn = lib().sfa_compile_nsfa if nsfa else lib().sfa_compile
+    fn = lib().sfa_compile_lazy if lazy else (lib().sfa_compile_nsfa if nsfa else lib().sfa_compile)
     if alphabet is None:
         rc = fn(rx, None, 0, max_sfa, C.byref(h))
     else:
@@ -178,6 +183,14 @@ def sfa_match(h: int, d_text, n: int | None = None, stream=None):
     n = _nbytes(d_text) if n is None else n
     q, a = C.c_uint32(), C.c_int()
     _check(lib().sfa_match(h, _dptr(d_text) if n else None, n, _stream(stream), C.byref(q), C.byref(a)))
+    return q.value, bool(a.value)
+
+
+def sfa_match_lazy(h: int, d_text, n: int | None = None, stream=None):
+    """On-the-fly handle (sfa_compile_lazy), blocking: -> (final_state, accept)."""
+    n = _nbytes(d_text) if n is None else n
+    q, a = C.c_uint32(), C.c_int()
+    _check(lib().sfa_match_lazy(h, _dptr(d_text) if n else None, n, _stream(stream), C.byref(q), C.byref(a)))
     return q.value, bool(a.value)
 
 
@@ -351,8 +364,8 @@ def sfa_export_sfa(h: int):
 class SFA:
     """Owns one compiled handle: ``SFA(regex, alphabet)``."""
 
-    def __init__(self, regex, alphabet=None, max_sfa: int = 0, nsfa: bool = False):
-        self.h = sfa_compile(regex, alphabet, max_sfa, nsfa)
+    def __init__(self, regex, alphabet=None, max_sfa: int = 0, nsfa: bool = False, lazy: bool = False):
+        self.h = sfa_compile(regex, alphabet, max_sfa, nsfa, lazy)
         self._match_async = lib().sfa_match_async
 
     def close(self):
@@ -399,6 +412,9 @@ class SFA:
 
     def match_batch_host(self, h_texts, h_offsets, count=None, h_results=None, stream=None):
         return sfa_match_batch_host(self.h, h_texts, h_offsets, count, h_results, stream)
+
+    def match_lazy(self, d_text, stream=None):
+        return sfa_match_lazy(self.h, d_text, None, stream)
 
     def match_host(self, h_text, stream=None):
         return sfa_match_host(self.h, h_text, stream)

@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cpp", "compile.cpp", "kernels.cu", "kernels_private.cu", "kernels_shared.cu", "kernels_global.cu",
            "kernels_hot.cu", "kernels_private_seg.cu", "kernels_shared_seg.cu", "kernels_global_seg.cu",
-           "kernels_hot_seg.cu", "kernels_spec.cu"]
+           "kernels_hot_seg.cu", "kernels_spec.cu", "kernels_lazy.cu", "lazy.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr"]
 

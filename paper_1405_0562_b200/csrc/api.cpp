@@ -4,10 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -16,6 +18,7 @@
 #include "../../include/sfa.h"
 #include "compile.hpp"
 #include "kernels.hpp"
+#include "lazy.hpp"
 
 namespace {
 
@@ -55,8 +58,32 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
 
 }  // namespace
 
+// Device state of the on-the-fly construction (sfa_compile_lazy / sfa_match_lazy).
+struct LazyDev {
+    uint32_t* T = nullptr;   // transition table copy (u32, cap_rows * C)
+    uint16_t* maps = nullptr;  // mapping vectors (cap_rows * nD)
+    uint8_t* cls = nullptr;
+    size_t cap_rows = 0, maps_rows = 0;
+    uint32_t* state = nullptr;
+    uint64_t* pos = nullptr;
+    uint32_t* idx = nullptr;
+    uint8_t* win = nullptr;
+    uint16_t* fold = nullptr;
+    uint16_t* fin = nullptr;
+    size_t cap_p = 0, cap_win = 0;
+    void release() {
+        for (void* q : {(void*)T, (void*)maps, (void*)cls, (void*)state, (void*)pos, (void*)idx, (void*)win, (void*)fold,
+                        (void*)fin})
+            if (q) cudaFree(q);
+        *this = LazyDev{};
+    }
+};
+
 struct sfa_handle {
     sfa::Automata A;
+    std::unique_ptr<sfa::LazySFA> lazy;  // sfa_compile_lazy handles
+    LazyDev ld;
+    double lazy_build_s = 0;             // host time spent building states while matching
     // byte window of the range tables (DevTables::lo / W)
     uint32_t lo = 0, W = 1, other = 0;
     int forced = SFA_RES_AUTO;
@@ -148,6 +175,7 @@ struct sfa_handle {
         }
         if (hres) cudaFreeHost(hres);
         hres = nullptr;
+        ld.release();
         for (int i = 0; i < 2; ++i) {
             if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
             if (ev_used[i]) cudaEventDestroy(ev_used[i]);
@@ -789,6 +817,7 @@ struct sfa_handle {
     }
 
     int begin(cudaStream_t stream) {
+        if (lazy) return fail(SFA_ERR_INVALID_ARG, "an on-the-fly handle (sfa_compile_lazy) matches with sfa_match_lazy");
         int rc = ensure_uploaded();
         if (rc) return rc;
         if (has_last && stream != last_stream) {
@@ -855,6 +884,28 @@ int sfa_compile(const char* regex, const uint8_t* alphabet, int alphabet_len, ui
     return compile_any(false, regex, alphabet, alphabet_len, max_sfa, out);
 }
 
+int sfa_compile_lazy(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_states,
+                     sfa_handle** out) {
+    if (!out) return fail(SFA_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!regex) return fail(SFA_ERR_INVALID_ARG, "regex is NULL");
+    if (alphabet && alphabet_len < 0) return fail(SFA_ERR_INVALID_ARG, "alphabet_len < 0");
+    sfa_handle* h = new (std::nothrow) sfa_handle;
+    if (!h) return fail(SFA_ERR_OOM, "host allocation failed");
+    try {
+        h->A = sfa::compile_regex(regex, alphabet, alphabet ? alphabet_len : -1, 0, false);
+        h->lazy.reset(new sfa::LazySFA(h->A, max_states ? max_states : (1u << 24)));
+    } catch (const sfa::CompileError& e) {
+        delete h;
+        return fail(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        delete h;
+        return fail(SFA_ERR_OOM, "host allocation failed during compile");
+    }
+    *out = h;
+    return SFA_OK;
+}
+
 int sfa_compile_nsfa(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa,
                      sfa_handle** out) {
     return compile_any(true, regex, alphabet, alphabet_len, max_sfa, out);
@@ -885,7 +936,14 @@ int sfa_info(const sfa_handle* h, sfa_info_t* info) {
     info->device_table_bytes = h->dev_bytes;
     info->dfa_seconds = A.dfa_seconds;
     info->sfa_seconds = A.sfa_seconds;
-    info->kind = A.nsfa ? 1u : 0u;
+    info->kind = h->lazy ? 2u : (A.nsfa ? 1u : 0u);
+    if (h->lazy) {
+        info->compose_mode = 0;
+        info->residency = SFA_RES_L2;
+        info->sfa_states = h->lazy->nS;
+        info->lazy_transitions = h->lazy->transitions;
+        info->lazy_seconds = h->lazy_build_s;
+    }
     info->nfa_states = A.nfa_states;
     info->has_dfa = A.has_dfa ? 1u : 0u;
     return SFA_OK;
@@ -962,6 +1020,17 @@ int sfa_export_dfa(const sfa_handle* h, uint32_t* table, uint8_t* finals) {
 
 int sfa_export_sfa(const sfa_handle* h, uint32_t* table, uint32_t* maps, uint8_t* finals) {
     if (!h) return fail(SFA_ERR_INVALID_ARG, "NULL handle");
+    if (h->lazy) {  // the states built so far; transitions not built yet are UINT32_MAX
+        const sfa::LazySFA& Z = *h->lazy;
+        if (table)
+            for (uint32_t st = 0; st < Z.nS; ++st)
+                for (int b = 0; b < 256; ++b) table[static_cast<size_t>(st) * 256 + b] = Z.T[static_cast<size_t>(st) * Z.C + Z.cls[b]];
+        if (maps)
+            for (size_t i = 0; i < Z.maps.size(); ++i) maps[i] = Z.maps[i];
+        if (finals)
+            for (uint32_t st = 0; st < Z.nS; ++st) finals[st] = Z.dfinal[Z.img0(st)];
+        return SFA_OK;
+    }
     const auto& A = h->A;
     if (table)
         for (uint32_t s = 0; s < A.nS; ++s)
@@ -1303,6 +1372,139 @@ int sfa_match_batch_host(const sfa_handle* hc, const uint8_t* h_texts, const uin
     rc = h->end(s);
     if (rc) return rc;
     CU(cudaStreamSynchronize(s));
+    return SFA_OK;
+}
+
+// sfa_match_lazy: Alg. 5 with the SFA built on the fly.
+// Rounds of: the device runs every unfinished chunk until it meets a
+// transition not built yet; the host builds the transitions the stalled
+// chunks need by running its construction over the next K bytes of each
+// (Alg. 4 lines 6-8 per (f, sigma) met); the table copy is refreshed.  Then
+// the chunk states are folded as mapping vectors (pairwise tree on the
+// device) and applied to q0.  States persist in the handle: a later match
+// of similar text builds little or nothing.
+int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_stream_t stream, uint32_t* final_state,
+                   int* accept) {
+    sfa_handle* h = const_cast<sfa_handle*>(hc);
+    if (!h || !final_state || !accept) return fail(SFA_ERR_INVALID_ARG, "NULL argument");
+    if (!h->lazy) return fail(SFA_ERR_INVALID_ARG, "not an on-the-fly handle (sfa_compile_lazy)");
+    if (!d_text && n > 0) return fail(SFA_ERR_INVALID_ARG, "d_text is NULL with n > 0");
+    sfa::LazySFA& Z = *h->lazy;
+    if (n == 0) {
+        *final_state = 0;
+        *accept = Z.dfinal[0];
+        return SFA_OK;
+    }
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!h->uploaded) {
+        CU(cudaGetDevice(&h->device));
+        int v = 0;
+        CU(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, h->device));
+        h->sm_count = v;
+        h->uploaded = true;
+    }
+    LazyDev& D = h->ld;
+    const uint32_t nD = Z.nD, C = Z.C;
+    // chunks: SPEC's rule (C6); at most 1024 per SM and 256 MiB of fold vectors
+    uint64_t p = std::min<uint64_t>(n, 1024ull * static_cast<uint64_t>(h->sm_count));
+    p = std::max<uint64_t>(1, std::min<uint64_t>(p, (128ull << 20) / nD));
+    if (!D.cls) {
+        CU(cudaMalloc(&D.cls, 256));
+        CU(cudaMemcpy(D.cls, Z.cls, 256, cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&D.fin, nD * sizeof(uint16_t)));
+    }
+    if (D.cap_p < p) {
+        for (void* q : {(void*)D.state, (void*)D.pos, (void*)D.idx, (void*)D.fold})
+            if (q) CU(cudaFree(q));
+        D.state = nullptr, D.pos = nullptr, D.idx = nullptr, D.fold = nullptr;
+        D.cap_p = 0;
+        CU(cudaMalloc(&D.state, p * sizeof(uint32_t)));
+        CU(cudaMalloc(&D.pos, p * sizeof(uint64_t)));
+        CU(cudaMalloc(&D.idx, p * sizeof(uint32_t)));
+        CU(cudaMalloc(&D.fold, 2 * p * nD * sizeof(uint16_t)));
+        D.cap_p = p;
+    }
+    auto sync_tables = [&]() -> int {  // the device copies of T (all rows) and maps (new rows)
+        if (D.cap_rows < Z.nS) {
+            size_t cap = std::max<size_t>(1024, D.cap_rows);
+            while (cap < Z.nS) cap *= 2;
+            uint32_t* nT = nullptr;
+            uint16_t* nM = nullptr;
+            CU(cudaMalloc(&nT, cap * C * sizeof(uint32_t)));
+            CU(cudaMalloc(&nM, cap * nD * sizeof(uint16_t)));
+            if (D.maps_rows) CU(cudaMemcpyAsync(nM, D.maps, D.maps_rows * nD * sizeof(uint16_t), cudaMemcpyDeviceToDevice, s));
+            CU(cudaStreamSynchronize(s));
+            if (D.T) CU(cudaFree(D.T));
+            if (D.maps) CU(cudaFree(D.maps));
+            D.T = nT;
+            D.maps = nM;
+            D.cap_rows = cap;
+        }
+        CU(cudaMemcpyAsync(D.T, Z.T.data(), static_cast<size_t>(Z.nS) * C * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        if (D.maps_rows < Z.nS) {
+            CU(cudaMemcpyAsync(D.maps + D.maps_rows * nD, Z.maps.data() + D.maps_rows * nD,
+                               (Z.nS - D.maps_rows) * nD * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+            D.maps_rows = Z.nS;
+        }
+        return SFA_OK;
+    };
+    cudaError_t e = sfa::lazy_init(n, p, D.state, D.pos, h->sm_count, s);
+    if (e != cudaSuccess) return cuda_fail(e, "lazy init");
+    std::vector<uint64_t> hpos(p), hend(p);
+    std::vector<uint32_t> hstate(p), stalled;
+    for (uint64_t g = 0; g < p; ++g) hend[g] = (g + 1) * (n / p) + std::min<uint64_t>(g + 1, n % p);
+    const uint32_t K = 4096;  // bytes of text the host builds ahead per stalled chunk and round
+    std::vector<uint8_t> hwin;
+    for (int round = 0;; ++round) {
+        int rc = sync_tables();
+        if (rc) return rc;
+        e = sfa::lazy_scan(D.T, D.cls, C, d_text, n, p, D.state, D.pos, s);
+        if (e != cudaSuccess) return cuda_fail(e, "lazy scan");
+        CU(cudaMemcpyAsync(hpos.data(), D.pos, p * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hstate.data(), D.state, p * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        stalled.clear();
+        for (uint64_t g = 0; g < p; ++g)
+            if (hpos[g] < hend[g]) stalled.push_back(static_cast<uint32_t>(g));
+        if (stalled.empty()) break;
+        // the windows the host builds from
+        const size_t need = stalled.size() * static_cast<size_t>(K);
+        if (D.cap_win < need) {
+            if (D.win) CU(cudaFree(D.win));
+            D.win = nullptr;
+            D.cap_win = 0;
+            CU(cudaMalloc(&D.win, need));
+            D.cap_win = need;
+        }
+        hwin.resize(need);
+        CU(cudaMemcpyAsync(D.idx, stalled.data(), stalled.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        e = sfa::lazy_gather(d_text, n, p, D.pos, D.idx, static_cast<uint32_t>(stalled.size()), K, D.win, s);
+        if (e != cudaSuccess) return cuda_fail(e, "lazy gather");
+        CU(cudaMemcpyAsync(hwin.data(), D.win, need, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        const auto t0 = std::chrono::steady_clock::now();
+        try {
+            for (size_t j = 0; j < stalled.size(); ++j) {
+                const uint32_t g = stalled[j];
+                const uint64_t len = std::min<uint64_t>(K, hend[g] - hpos[g]);
+                Z.run(hstate[g], hwin.data() + j * static_cast<size_t>(K), len);
+            }
+        } catch (const sfa::CompileError& ce) {
+            return fail(ce.code, ce.what());
+        } catch (const std::bad_alloc&) {
+            return fail(SFA_ERR_OOM, "host allocation failed while building SFA states");
+        }
+        h->lazy_build_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    // f_fin = f_1 . ... . f_p on the device, q_final = f_fin(q0)
+    e = sfa::lazy_fold(D.maps, D.state, p, nD, D.fold, D.fin, h->sm_count, s);
+    if (e != cudaSuccess) return cuda_fail(e, "lazy fold");
+    uint16_t q16 = 0;
+    CU(cudaMemcpyAsync(&q16, D.fin, sizeof(uint16_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *final_state = q16;
+    *accept = Z.dfinal[q16];
     return SFA_OK;
 }
 

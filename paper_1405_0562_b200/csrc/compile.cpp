@@ -641,7 +641,7 @@ void build_min_dfa(Automata& A, const Front& F) {
 
 }  // namespace
 
-Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa) {
+Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa, bool build_sfa) {
     auto t0 = std::chrono::steady_clock::now();
     Automata A;
     Front F = make_front(A, regex, sigma, sigma_len);
@@ -669,6 +669,7 @@ Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma
         }
         for (uint32_t c = 0; c < A.C; ++c) A.rep_byte[c] = static_cast<uint8_t>(rep[c] >= 0 ? rep[c] : any[c]);
     }
+    if (!build_sfa) return A;  // the on-the-fly construction (lazy.cpp) builds the SFA while matching
 
     // ---- Alg. 4 (DFA form), canonical numbering ----
     const uint32_t D = nb, C = A.C;

@@ -58,7 +58,9 @@ struct Automata {
 };
 
 // Throws CompileError.  sigma == nullptr means all 256 bytes.
-Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa);
+// build_sfa = false: the minimal DFA and its byte classes only.
+Automata compile_regex(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa,
+                       bool build_sfa = true);
 // The N-SFA of the regex's Glushkov NFA by Alg. 4 in its general form
 // (PAPER.md:481-521); the minimal DFA too when it has <= 2^20 states.
 Automata compile_nsfa(const std::string& regex, const uint8_t* sigma, int sigma_len, uint32_t max_sfa);

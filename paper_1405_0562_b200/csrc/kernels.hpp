@@ -131,6 +131,16 @@ cudaError_t spec_plan(const SpecArgs& proto, int sm_count, size_t smem_optin, ui
                       SpecArgs* out, uint32_t* threads, size_t* smem);
 cudaError_t launch_spec(const SpecArgs& a, uint32_t threads, size_t smem, cudaStream_t stream);
 
+// On-the-fly construction (kernels_lazy.cu): chunk runs that stop at unbuilt transitions,
+// the gather of the text windows the host builds from, the mapping-vector fold.
+cudaError_t lazy_init(uint64_t n, uint64_t p, uint32_t* state, uint64_t* pos, int sm_count, cudaStream_t s);
+cudaError_t lazy_scan(const uint32_t* T, const uint8_t* cls, uint32_t C, const uint8_t* text, uint64_t n, uint64_t p,
+                      uint32_t* state, uint64_t* pos, cudaStream_t s);
+cudaError_t lazy_gather(const uint8_t* text, uint64_t n, uint64_t p, const uint64_t* pos, const uint32_t* idx,
+                        uint32_t count, uint32_t K, uint8_t* out, cudaStream_t s);
+cudaError_t lazy_fold(const uint16_t* maps, const uint32_t* state, uint64_t p, uint32_t nD, uint16_t* buf,
+                      uint16_t* out, int sm_count, cudaStream_t s);
+
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);
 cudaError_t launch_scan_seg(Res mode, const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t stream);

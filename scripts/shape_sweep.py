@@ -1,0 +1,49 @@
+"""Steady and single-launch GB/s of the TMA scan per launch shape (K, ROWB, ring).
+usage: python scripts/shape_sweep.py [configs]"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1405_0562_b200 as P  # noqa: E402
+
+cfgs = [int(c) for c in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["2", "4", "3"])]
+shapes = [dict(), dict(tma_k=1, tma_rowb=32), dict(tma_k=2, tma_rowb=16), dict(tma_k=1, tma_rowb=16),
+          dict(tma_k=2, tma_rowb=32), dict(tma_k=1, tma_rowb=64), dict(tma_k=2, tma_rowb=16, tma_ring=4),
+          dict(tma_k=2, tma_rowb=16, tma_ring=6)]
+s = torch.cuda.Stream()
+for cfg in cfgs:
+    rx, alpha, text = bench.workload(cfg)
+    if cfg == 5:
+        texts, off, _ = text
+        dt = torch.from_numpy(texts).cuda()
+        do = torch.from_numpy(off.astype(np.int64)).cuda()
+        res = torch.zeros(2 * (off.size - 1), dtype=torch.int32, device="cuda")
+        n = texts.size
+    else:
+        dt = torch.from_numpy(text).cuda()
+        res = torch.zeros(2, dtype=torch.int32, device="cuda")
+        n = text.size
+    ref = None
+    for sh in shapes:
+        sfa = P.SFA(rx, alpha)
+        try:
+            sfa.set_tuning(**sh)
+            fn = (lambda: sfa.match_batch(dt, do, off.size - 1, res, s)) if cfg == 5 else (lambda: sfa.match_async(dt, res, s))
+            ms, med = bench.steady(torch, fn, s, 30, 5)
+            one = bench.single(torch, fn, s, 10)
+            got = res.cpu().numpy().tobytes()
+            ok = ref is None or got == ref
+            ref = ref or got
+            print(json.dumps({"cfg": cfg, "shape": sh, "steady_gbs": round(n / ms / 1e6), "single_gbs": round(n / one / 1e6),
+                              "residency": P.RES_NAMES[sfa.info()["residency"]], "same_result": ok}), flush=True)
+        except P.SFAError as e:
+            print(json.dumps({"cfg": cfg, "shape": sh, "error": str(e)}), flush=True)
+        sfa.close()
+    del dt
