@@ -360,6 +360,44 @@ def nsfa_compare(torch, P, stream, steps, warmup, reps, peak, peak_kind, nsm, sm
     return out
 
 
+def lazy_family(torch, P, stream, warmup, peak, nbytes):
+    """the paper's r_500 (|S| = 1,000,999) and r_a
+     with the D-SFA built on the fly while matching
+    (PAPER.md:532-542): the first match (construction + scan), the steady match
+    of the same text (sfa_match_lazy, blocking), the states built, and Alg. 3
+    (the speculative DFA, 1001 lookups per byte) on the same text beside it."""
+    import workloads as W
+    out = {}
+    for name, rx, alpha, gen in (("r500", W.rn_regex(500), b"0123456789", lambda: W.rn_accepted(500, nbytes)),
+                                 ("ra500", W.ra_regex(500), b"0123456789a", lambda: W.ra_text(nbytes))):
+        text = gen()
+        sfa = P.SFA(rx, alpha, lazy=True)
+        dt = torch.from_numpy(text).cuda()
+        t0 = time.perf_counter()
+        q, acc = sfa.match_lazy(dt, stream)
+        first_s = time.perf_counter() - t0
+        if not acc:
+            raise SystemExit(f"{name}: the accepted text was rejected ({q})")
+        times = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            assert sfa.match_lazy(dt, stream) == (q, acc)
+            times.append(time.perf_counter() - t0)
+        ms = 1e3 * statistics.median(times)
+        info = sfa.info()
+        gbs = text.size / (ms * 1e-3) / 1e9
+        out[name] = {"regex": f"{rx[:24]}...", "bytes": int(text.size), "dfa_states": info["dfa_states"],
+                     "full_sfa_states": 1_000_999 if name == "r500" else 1_001_000,
+                     "states_built": info["sfa_states"], "transitions_built": info["lazy_transitions"],
+                     "first_match_s": first_s, "host_build_s": info["lazy_seconds"],
+                     "value": gbs, "unit": UNIT, "ms_per_step": ms, "roofline_frac": gbs / peak,
+                     "timer": "host wall clock around the blocking call (median of 5)",
+                     "alg3_speculative": spec_compare(torch, sfa, dt, text.size, ms, stream, warmup, (q, acc))}
+        del dt
+        sfa.close()
+    return out
+
+
 def rn_family(torch, P, stream, warmup, peak, nbytes):
     """SURVEY 8(f) NEXT-2, the paper's scalability study on the GPU:
     r_n on an accepted text and r_a on "a"^m, the SFA beside Alg. 3 (speculative DFA)."""
@@ -549,6 +587,8 @@ def main():
     ap.add_argument("--rn", action="store_true",
                     help="also run the r_n scalability family (r5..r127, r_a) with Alg. 3 beside it")
     ap.add_argument("--rn-bytes", type=int, default=1 << 30)
+    ap.add_argument("--lazy", action="store_true",
+                    help="also run r_500 and r_a with the D-SFA built on the fly (Alg. 3 beside)")
     ap.add_argument("--no-nsfa", dest="nsfa", action="store_false",
                     help="skip the N-SFA vs D-SFA line on the paper's Ex. 3")
     ap.add_argument("--spec", action="store_true",
@@ -642,6 +682,8 @@ def main():
         line["per_config"] = per
     if args.rn:
         line["rn_family"] = rn_family(torch, P, stream, args.warmup, peak, args.rn_bytes)
+    if args.lazy:
+        line["on_the_fly"] = lazy_family(torch, P, stream, args.warmup, peak, args.rn_bytes)
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_sample(cfg, rx, alpha, wl, args.cpu_seconds)
     print(json.dumps(line), flush=True)

@@ -455,6 +455,24 @@ struct sfa_handle {
         return upload_hot(sample.data(), ns);
     }
 
+    // Device state for the DFA-only calls of an on-the-fly handle (Alg. 3).
+    int ensure_dfa_only() {
+        if (!uploaded) {
+            CU(cudaGetDevice(&device));
+            int v = 0;
+            CU(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+            sm_count = v;
+            uploaded = true;
+        }
+        if (!smem_optin) {
+            int v = 0;
+            CU(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+            smem_optin = static_cast<size_t>(v);
+        }
+        if (!dfinal) CU(upload(&dfinal, A.dfa_final.data(), A.dfa_final.size()));
+        return SFA_OK;
+    }
+
     // Lazy upload: sfa_compile works without a GPU (host tests); the first
     // device call uploads to the then-current device.
     int ensure_uploaded() {
@@ -837,6 +855,29 @@ extern "C" {
 
 const char* sfa_last_error(void) { return g_err.c_str(); }
 
+// Byte window: the smallest [lo, hi] such that every byte outside it has one
+// class ("other"); table columns are lo..hi, then W-1 = other.  With cand = 0
+// the window never contains byte 0, with cand = 255 never byte 255, so W <= 256.
+static void set_window(sfa_handle* h) {
+    const uint8_t* cls = h->A.cls;
+    h->W = 257;
+    for (int cand : {0, 255}) {
+        const uint8_t o = cls[cand];
+        int lo = -1, hi = -1;
+        for (int b = 0; b < 256; ++b)
+            if (cls[b] != o) {
+                if (lo < 0) lo = b;
+                hi = b;
+            }
+        const uint32_t W = lo < 0 ? 1u : static_cast<uint32_t>(hi - lo + 2);
+        if (W < h->W) {
+            h->W = W;
+            h->lo = lo < 0 ? 0u : static_cast<uint32_t>(lo);
+            h->other = o;
+        }
+    }
+}
+
 static int compile_any(bool nsfa, const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_sfa,
                        sfa_handle** out) {
     if (!out) return fail(SFA_ERR_INVALID_ARG, "out is NULL");
@@ -855,27 +896,7 @@ static int compile_any(bool nsfa, const char* regex, const uint8_t* alphabet, in
         delete h;
         return fail(SFA_ERR_OOM, "host allocation failed during compile");
     }
-    // Byte window: the smallest [lo, hi] such that every byte outside it has
-    // one class ("other"); table columns are lo..hi, then W-1 = other.  With
-    // cand = 0 the window never contains byte 0, with cand = 255 never byte
-    // 255, so W <= 256.
-    const uint8_t* cls = h->A.cls;
-    h->W = 257;
-    for (int cand : {0, 255}) {
-        const uint8_t o = cls[cand];
-        int lo = -1, hi = -1;
-        for (int b = 0; b < 256; ++b)
-            if (cls[b] != o) {
-                if (lo < 0) lo = b;
-                hi = b;
-            }
-        const uint32_t W = lo < 0 ? 1u : static_cast<uint32_t>(hi - lo + 2);
-        if (W < h->W) {
-            h->W = W;
-            h->lo = lo < 0 ? 0u : static_cast<uint32_t>(lo);
-            h->other = o;
-        }
-    }
+    set_window(h);
     *out = h;
     return SFA_OK;
 }
@@ -895,6 +916,7 @@ int sfa_compile_lazy(const char* regex, const uint8_t* alphabet, int alphabet_le
     try {
         h->A = sfa::compile_regex(regex, alphabet, alphabet ? alphabet_len : -1, 0, false);
         h->lazy.reset(new sfa::LazySFA(h->A, max_states ? max_states : (1u << 24)));
+        set_window(h);  // for Alg. 3 (sfa_match_speculative) on the same DFA
     } catch (const sfa::CompileError& e) {
         delete h;
         return fail(e.code, e.what());
@@ -1224,7 +1246,7 @@ int sfa_match_speculative(const sfa_handle* hc, const uint8_t* d_text, size_t n,
         return fail(SFA_ERR_INVALID_ARG, "d_chunk_maps needs an explicit nchunks");
     std::lock_guard<std::mutex> lk(h->mu);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    int rc = h->begin(s);
+    int rc = h->lazy ? h->ensure_dfa_only() : h->begin(s);
     if (rc) return rc;
     if (n == 0) {  // no chunk: T = identity, q_final = q0
         cudaError_t e = sfa::launch_fill_result(d_result, 0, h->A.dfa_final[0], d_chunk_maps, h->A.nD, s);
@@ -1397,13 +1419,8 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
     }
     std::lock_guard<std::mutex> lk(h->mu);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (!h->uploaded) {
-        CU(cudaGetDevice(&h->device));
-        int v = 0;
-        CU(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, h->device));
-        h->sm_count = v;
-        h->uploaded = true;
-    }
+    int rc0 = h->ensure_dfa_only();
+    if (rc0) return rc0;
     LazyDev& D = h->ld;
     const uint32_t nD = Z.nD, C = Z.C;
     // chunks: SPEC's rule (C6); at most 1024 per SM and 256 MiB of fold vectors
