@@ -24,7 +24,11 @@ Beside it, on rank 0:
     same workload on one host core, with nproc and the CPU model;
   * ``e2e``: the same batch end to end from pinned host memory through
     ``sfa_match_batch_host`` (H2D of texts and offsets, D2H of the results in
-    the timed region).
+    the timed region);
+  * ``per_config.ex3_n11``: the paper's Ex. 3 matched with the N-SFA (built
+    from the NFA) beside the D-SFA;
+  * ``per_config.on_the_fly_r500_ra``: r_500 and r_a (1 GiB) with the D-SFA
+    built on the fly while matching, Alg. 3 beside.
 ``--spec`` adds the paper's baseline (Alg. 3) on cfg2-4; ``--rn`` the r_n
 family; ``--shard`` one text over the ranks.
 
@@ -587,8 +591,8 @@ def main():
     ap.add_argument("--rn", action="store_true",
                     help="also run the r_n scalability family (r5..r127, r_a) with Alg. 3 beside it")
     ap.add_argument("--rn-bytes", type=int, default=1 << 30)
-    ap.add_argument("--lazy", action="store_true",
-                    help="also run r_500 and r_a with the D-SFA built on the fly (Alg. 3 beside)")
+    ap.add_argument("--no-lazy", dest="lazy", action="store_false",
+                    help="skip r_500 and r_a with the D-SFA built on the fly (Alg. 3 beside)")
     ap.add_argument("--no-nsfa", dest="nsfa", action="store_false",
                     help="skip the N-SFA vs D-SFA line on the paper's Ex. 3")
     ap.add_argument("--spec", action="store_true",
@@ -683,7 +687,8 @@ def main():
     if args.rn:
         line["rn_family"] = rn_family(torch, P, stream, args.warmup, peak, args.rn_bytes)
     if args.lazy:
-        line["on_the_fly"] = lazy_family(torch, P, stream, args.warmup, peak, args.rn_bytes)
+        line["per_config"] = line.get("per_config", {})
+        line["per_config"]["on_the_fly_r500_ra"] = lazy_family(torch, P, stream, args.warmup, peak, args.rn_bytes)
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_sample(cfg, rx, alpha, wl, args.cpu_seconds)
     print(json.dumps(line), flush=True)
