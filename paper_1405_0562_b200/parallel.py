@@ -32,8 +32,15 @@ def gather_maps(local_map, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    out = torch.empty(world * local_map.numel(), dtype=local_map.dtype, device=local_map.device)
-    dist.all_gather_into_tensor(out, local_map.contiguous().view(-1), group=group)
+    src = local_map.contiguous().view(-1)
+    # gloo moves CPU tensors only: stage a device map through the host
+    staged = src.is_cuda and dist.get_backend(group) == "gloo"
+    if staged:
+        src = src.cpu()
+    out = torch.empty(world * src.numel(), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    if staged:
+        out = out.to(local_map.device)
     return out.view(world, -1)
 
 

@@ -102,3 +102,34 @@ def test_match_map_and_combine_on_gpu(cuda_ok):
         sfa.match_map(dt[:small.size], m)
         torch.cuda.synchronize()
         assert (m.cpu().numpy() == _oracle_map(d, small)).all(), rx
+
+
+def _sharded_worker(rank, world, port, text, rx, alpha, out):
+    """One rank of parallel.match_sharded: its shard on the GPU (sfa_match_map),
+    the maps all-gathered over gloo (staged through the host), the in-order
+    reduction on the device (sfa_combine_maps)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    sfa = P.SFA(rx, alpha)
+    a, b = PL.shard_bounds(text.size, world, rank)
+    out[rank] = PL.match_sharded(sfa, torch.from_numpy(text[a:b]).cuda())
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_match_sharded_end_to_end(cuda_ok, world):
+    """The product's parallel.match_sharded with world ranks (processes) on one
+    GPU over gloo: every rank returns the oracle's whole-text result; shards
+    are cut mid-block (cfg2) and mid-word (cfg3), and span both scan kernels."""
+    import torch.multiprocessing as mp
+    for rx, alpha, text in [(*CFG2, W.cfg2_accepted(1_300_011)), (*CFG2, W.cfg2_rejected(text=W.cfg2_accepted(700_000))),
+                            (W.cfg3_regex(), None, W.cfg3_text(9 << 20, plant=True))]:
+        d = O.OracleDFA(rx, alpha)
+        mgr = mp.Manager()
+        out = mgr.dict()
+        mp.spawn(_sharded_worker, args=(world, _free_port(), text, rx, alpha, out), nprocs=world, join=True)
+        assert [out[r] for r in range(world)] == [d.run(text)] * world
