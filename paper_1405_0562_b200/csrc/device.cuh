@@ -457,38 +457,47 @@ __device__ __forceinline__ uint32_t step16(const Step& S, uint32_t st, const uin
     return step4(S, st, v.w);
 }
 
-// A byte range [a, b) of `t`, from state st, with 16-byte loads where aligned.
+// Bytes [lo, hi) (offsets within the 16-byte block v) through S.
+template <class Step>
+__device__ __forceinline__ uint32_t step_part16(const Step& S, uint32_t st, const uint4& v, uint32_t lo, uint32_t hi) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j)
+        if (j >= lo && j < hi) st = S.step(st, (w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+    return st;
+}
+
+// A byte range [a, b) of `t`, from state st, with 16-byte loads only: the
+// ragged ends come from the aligned 16-byte blocks that hold them (a block
+// holding a byte of the text lies in the same page as that byte), so a short
+// unaligned piece costs one or two parallel loads, not one dependent load per
+// byte (head pieces, the tail).
 template <class Step>
 __device__ uint32_t run_range(const Step& S, uint32_t st, const uint8_t* __restrict__ t, uint64_t a, uint64_t b) {
-    while (a < b && (reinterpret_cast<uintptr_t>(t + a) & 15)) st = S.step(st, __ldg(t + a++));
-    if (a + 16 <= b) {
-        uint4 v = ldg_stream(t + a);
-        a += 16;
-        while (a + 16 <= b) {
-            uint4 nx = ldg_stream(t + a);  // next 16 bytes in flight while v is consumed
-            a += 16;
+    if (a >= b) return st;
+    const uintptr_t pa = reinterpret_cast<uintptr_t>(t + a), pb = reinterpret_cast<uintptr_t>(t + b);
+    uintptr_t blk = pa & ~uintptr_t(15);
+    const uintptr_t last = (pb - 1) & ~uintptr_t(15);
+    if (blk == last)  // one block
+        return step_part16(S, st, ldg_stream(reinterpret_cast<const void*>(blk)), static_cast<uint32_t>(pa - blk),
+                           static_cast<uint32_t>(pb - blk));
+    const uint4 vl = ldg_stream(reinterpret_cast<const void*>(last));  // in flight while the rest runs
+    if (pa != blk) {
+        st = step_part16(S, st, ldg_stream(reinterpret_cast<const void*>(blk)), static_cast<uint32_t>(pa - blk), 16u);
+        blk += 16;
+    }
+    if (blk < last) {
+        uint4 v = ldg_stream(reinterpret_cast<const void*>(blk));
+        blk += 16;
+        while (blk < last) {
+            const uint4 nx = ldg_stream(reinterpret_cast<const void*>(blk));  // next 16 bytes in flight while v is consumed
+            blk += 16;
             st = step16(S, st, v);
             v = nx;
         }
         st = step16(S, st, v);
     }
-    while (a < b) st = S.step(st, __ldg(t + a++));
-    return st;
-}
-
-// The same with 32-byte loads (one whole L2 sector per request: the batch
-// kernel's lanes read 32 scattered pieces, so 16-B loads fetch every sector
-// twice from L2).
-template <class Step>
-__device__ uint32_t run_range32(const Step& S, uint32_t st, const uint8_t* __restrict__ t, uint64_t a, uint64_t b) {
-    while (a < b && (reinterpret_cast<uintptr_t>(t + a) & 31)) st = S.step(st, __ldg(t + a++));
-    for (; a + 32 <= b; a += 32) {
-        const U8x32 v = ldg_stream32(t + a);
-        st = step16(S, st, v.lo);
-        st = step16(S, st, v.hi);
-    }
-    while (a < b) st = S.step(st, __ldg(t + a++));
-    return st;
+    return step_part16(S, st, vl, 0u, static_cast<uint32_t>(pb - last));
 }
 
 // ------------------------------------------------------------------------------------------

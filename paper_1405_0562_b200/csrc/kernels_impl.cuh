@@ -654,10 +654,14 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             pdl_wait();
             if (SEG && a.err && *a.err == a.epoch) return;  // bad offsets: the compute warps report
             const TmaPlan P = a.dplan ? *a.dplan : a.plan;
-            if (blockIdx.x == gridDim.x - 1) {  // the tail this CTA runs after its rows: into L2 now
-                const uint8_t* tp = a.text + (a.off ? __ldg(a.off) : 0ull) + P.tail_start;
+            if (blockIdx.x == gridDim.x - 1) {  // the tail this CTA runs after its rows, and the head: into L2 now
+                const uint8_t* base = a.text + (a.off ? __ldg(a.off) : 0ull);
                 const uint32_t tb = static_cast<uint32_t>((P.n - P.tail_start) & ~uint64_t(15));
-                if (tb) bulk_prefetch_l2(tp, tb);
+                if (tb) bulk_prefetch_l2(base + P.tail_start, tb);
+                // the 16-B blocks holding [0, head): the whole blocks lie in the text's pages
+                const uintptr_t h0 = reinterpret_cast<uintptr_t>(base) & ~uintptr_t(15);
+                const uintptr_t h1 = (reinterpret_cast<uintptr_t>(base) + P.head + 15) & ~uintptr_t(15);
+                if (P.head && h1 > h0) bulk_prefetch_l2(reinterpret_cast<const void*>(h0), static_cast<uint32_t>(h1 - h0));
             }
             const uint32_t rc = P.cta_rows(blockIdx.x);
             if (rc == 0) return;

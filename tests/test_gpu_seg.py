@@ -190,18 +190,6 @@ def test_batch_offsets_not_from_zero_and_gaps_in_buffer(torch_cuda):
         check_batch(torch, sfa, d, buf, off)
 
 
-def test_batch_cfg5_shape_through_offsets(torch_cuda):
-    """cfg5's 65,536 x 64 KiB through sfa_match_batch AND sfa_match_batch_uniform,
-    with the planted texts exactly the accepted ones."""
-    torch = torch_cuda
-    rx = W.cfg3_regex()
-    d = odfa(rx, None)
-    sfa = P.SFA(rx, None)
-    texts, off, idx = W.cfg5_batch()
-    q, acc = batch(torch, sfa, texts, off)
-    qo, ao = d.run_batch(texts, off)
-    assert (q == qo).all() and (acc == ao).all()
-    assert np.flatnonzero(acc).tolist() == idx.tolist()
 
 
 def test_batch_decreasing_offsets_invalidates_every_result(torch_cuda):
