@@ -165,15 +165,19 @@ def dist_setup():
     return world, rank, local
 
 
-def ncu_traffic(key: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+def ncu_entry(key: str) -> dict:
+    """The committed ncu --set full summary of the dominant kernel (profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(key, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(key, {})
     except Exception:
-        return None
+        return {}
+
+
+def ncu_traffic(key: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    return ncu_entry(key).get("dram_bytes_per_launch")
 
 
 # --------------------------------------------------------------------------- timing
@@ -215,9 +219,18 @@ def smem_peaks(nsm, sm_mhz):
     return nsm * 32 * hz / 1e9, nsm * (1.0 / (1 / 32 + 2 / 128)) * hz / 1e9
 
 
-def roofline(gbs, peak, peak_kind, nsm, sm_mhz, kernel, traffic, per_launch_bytes):
+def roofline(gbs, peak, peak_kind, nsm, sm_mhz, kernel, traffic, per_launch_bytes, key=None):
     lk, dp = smem_peaks(nsm, sm_mhz)
-    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+    extra = {}
+    e = ncu_entry(key) if key else {}
+    if e.get("smem_wavefronts_ld"):
+        # the shared-memory load data path at the measured wavefronts per byte (bank conflicts
+        # included): one wavefront per SM per clock -> bytes * nsm * f / wavefronts
+        ceil = per_launch_bytes * nsm * sm_mhz * 1e6 / e["smem_wavefronts_ld"] / 1e9
+        extra = {"smem_ld_ceiling_gbs": ceil, "frac_of_smem_ld_ceiling": gbs / ceil,
+                 "smem_conflicts_per_wavefront": e.get("smem_bank_conflicts_ld", 0) / e["smem_wavefronts_ld"],
+                 "smem_ld_ceiling_source": "profiles/ncu_summary.json wavefronts of the same kernel"}
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, **extra,
             "traffic": traffic, "traffic_source": "profiles/ncu_summary.json (ncu --set full of the same kernel)",
             "algorithmic_bytes_per_launch": per_launch_bytes,
             "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
@@ -335,7 +348,7 @@ def single_text_config(torch, P, cfg, stream, steps, warmup, reps, peak, peak_ki
            "single_launch": {"ms": one, "gbs": n / (one * 1e-3) / 1e9, "frac": n / (one * 1e-3) / 1e9 / peak,
                              "reps": reps, "how": "synchronised before each launch; launch-to-result events; median"},
            "roofline": roofline(gbs, peak, peak_kind, nsm, sm_mhz, "k_scan_tma (one launch per step)",
-                                ncu_traffic(f"cfg{cfg}") if cfg else None, int(n)),
+                                ncu_traffic(f"cfg{cfg}") if cfg else None, int(n), f"cfg{cfg}" if cfg else None),
            "residency": P.RES_NAMES.get(info["residency"], "?"), "sfa_states": info["sfa_states"],
            "dfa_states": info["dfa_states"], "api": "sfa_match_async", "gpu_launches_per_step": 1}
     if spec:
@@ -654,7 +667,7 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded, DESIGN.md input recipe)", "config": cfgd,
         "roofline": roofline(h["per_rank_gbs"], peak, peak_kind, nsm, sm_mhz, kernel,
-                             ncu_traffic(f"cfg{cfg}"), int(nbytes)),
+                             ncu_traffic(f"cfg{cfg}"), int(nbytes), f"cfg{cfg}"),
         "clocks": clocks, "gpu_launches": launches * args.steps,
     }
     for k in ("single_launch", "uniform_api"):

@@ -233,3 +233,37 @@ def test_rn_family_through_product():
     with pytest.raises(P.SFAError) as e:
         P.sfa_compile("([0-4]{500}[5-9]{500})*", b"0123456789")
     assert e.value.code == 3
+
+
+def test_argument_checks_before_any_device_work():
+    """Host-side argument checks of the async calls (no device call is made):
+    Alg. 3 chunk maps need an explicit chunk count (the automatic
+    count was not reported, the buffer could be overrun); NULL pointers and
+    out-of-range tuning values are INVALID_ARG; an on-the-fly handle refuses
+    the eager calls."""
+    import ctypes as C
+    L = P.lib()
+    h = P.sfa_compile("(ab|ba)*c", b"abc")
+    try:
+        fake = C.c_void_p(0x1000)
+        res = C.c_void_p(0x2000)
+        assert L.sfa_match_speculative(h, fake, 100, 0, None, fake, res) == P.SFA_ERR_INVALID_ARG
+        assert "explicit nchunks" in L.sfa_last_error().decode()
+        assert L.sfa_match_batch(h, None, fake, 3, None, res) == P.SFA_ERR_INVALID_ARG
+        assert L.sfa_match_async(h, None, 5, None, res) == P.SFA_ERR_INVALID_ARG
+        assert L.sfa_match_rows(h, fake, 1000, None, fake, 10, None, res) == P.SFA_ERR_INVALID_ARG
+        for bad in (dict(tma_k=3), dict(tma_rowb=32), dict(tma_k=1, tma_rowb=48), dict(row_align=96),
+                    dict(dfa_copies=3), dict(direct_piece=8), dict(tma_promo=100), dict(dfa_u8=2)):
+            with pytest.raises(P.SFAError) as e:
+                P.sfa_set_tuning(h, **bad)
+            assert e.value.code == P.SFA_ERR_INVALID_ARG, bad
+        P.sfa_set_tuning(h, tma_k=2, tma_rowb=16, hot_rows=7, no_factor=1)
+        P.sfa_set_tuning(h)
+    finally:
+        P.sfa_free(h)
+    lz = P.sfa_compile("(ab|ba)*c", b"abc", lazy=True)
+    try:
+        assert L.sfa_match_async(lz, C.c_void_p(0x1000), 5, None, C.c_void_p(0x2000)) == P.SFA_ERR_INVALID_ARG
+        assert "sfa_match_lazy" in L.sfa_last_error().decode()
+    finally:
+        P.sfa_free(lz)
