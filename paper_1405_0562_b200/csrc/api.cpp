@@ -1485,7 +1485,10 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
         for (uint64_t g = 0; g < p; ++g)
             if (hpos[g] < hend[g]) stalled.push_back(static_cast<uint32_t>(g));
         if (stalled.empty()) break;
-        // the windows the host builds from
+        // the windows the host builds from (at most 128 MiB of them per round:
+        // the other stalled chunks wait for the next round)
+        const size_t max_chunks = std::max<size_t>(1, (128u << 20) / K);
+        if (stalled.size() > max_chunks) stalled.resize(max_chunks);
         const size_t need = stalled.size() * static_cast<size_t>(K);
         if (D.cap_win < need) {
             if (D.win) CU(cudaFree(D.win));
