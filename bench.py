@@ -382,19 +382,17 @@ def lazy_family(torch, P, stream, warmup, peak, nbytes):
      with the D-SFA built on the fly while matching
     (PAPER.md:532-542): the first match (construction + scan), the steady match
     of the same text (sfa_match_lazy, blocking), the states built, and Alg. 3
-    (the speculative DFA, 1001 lookups per byte) on the same text beside it."""
+    (the speculative DFA, 1001 lookups per byte) on the same text beside it.
+    Default: factored chunk runs (C24); "full_construction" repeats
+    it with tuning no_factor, i.e. every visited state built (Table III's
+    construction, PAPER.md:816-820)."""
     import workloads as W
     out = {}
-    for name, rx, alpha, gen in (("r500", W.rn_regex(500), b"0123456789", lambda: W.rn_accepted(500, nbytes)),
-                                 ("ra500", W.ra_regex(500), b"0123456789a", lambda: W.ra_text(nbytes))):
-        text = gen()
-        sfa = P.SFA(rx, alpha, lazy=True)
-        dt = torch.from_numpy(text).cuda()
+
+    def one(sfa, dt, size):
         t0 = time.perf_counter()
         q, acc = sfa.match_lazy(dt, stream)
         first_s = time.perf_counter() - t0
-        if not acc:
-            raise SystemExit(f"{name}: the accepted text was rejected ({q})")
         times = []
         for _ in range(5):
             t0 = time.perf_counter()
@@ -402,14 +400,31 @@ def lazy_family(torch, P, stream, warmup, peak, nbytes):
             times.append(time.perf_counter() - t0)
         ms = 1e3 * statistics.median(times)
         info = sfa.info()
-        gbs = text.size / (ms * 1e-3) / 1e9
-        out[name] = {"regex": f"{rx[:24]}...", "bytes": int(text.size), "dfa_states": info["dfa_states"],
-                     "full_sfa_states": 1_000_999 if name == "r500" else 1_001_000,
-                     "states_built": info["sfa_states"], "transitions_built": info["lazy_transitions"],
-                     "first_match_s": first_s, "host_build_s": info["lazy_seconds"],
-                     "value": gbs, "unit": UNIT, "ms_per_step": ms, "roofline_frac": gbs / peak,
-                     "timer": "host wall clock around the blocking call (median of 5)",
-                     "alg3_speculative": spec_compare(torch, sfa, dt, text.size, ms, stream, warmup, (q, acc))}
+        return (q, acc), {"states_built": info["sfa_states"], "transitions_built": info["lazy_transitions"],
+                          "first_match_s": first_s, "host_build_s": info["lazy_seconds"],
+                          "value": size / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms}
+
+    for name, rx, alpha, gen in (("r500", W.rn_regex(500), b"0123456789", lambda: W.rn_accepted(500, nbytes)),
+                                 ("ra500", W.ra_regex(500), b"0123456789a", lambda: W.ra_text(nbytes))):
+        text = gen()
+        dt = torch.from_numpy(text).cuda()
+        sfa = P.SFA(rx, alpha, lazy=True)
+        res, r = one(sfa, dt, text.size)
+        if not res[1]:
+            raise SystemExit(f"{name}: the accepted text was rejected ({res})")
+        full = P.SFA(rx, alpha, lazy=True)
+        full.set_tuning(no_factor=1)
+        res_f, rf = one(full, dt, text.size)
+        assert res_f == res
+        full.close()
+        info = sfa.info()
+        r.update({"regex": f"{rx[:24]}...", "bytes": int(text.size), "dfa_states": info["dfa_states"],
+                  "full_sfa_states": 1_000_999 if name == "r500" else 1_001_000,
+                  "roofline_frac": r["value"] / peak, "mode": "factored chunk runs (C24)",
+                  "timer": "host wall clock around the blocking call (median of 5)",
+                  "full_construction": rf,
+                  "alg3_speculative": spec_compare(torch, sfa, dt, text.size, r["ms_per_step"], stream, warmup, res)})
+        out[name] = r
         del dt
         sfa.close()
     return out

@@ -164,8 +164,13 @@ SFA_API int sfa_compile_nsfa(const char* regex, const uint8_t* alphabet, int alp
  * and host construction of the transitions the stalled chunks need (the next
  * 4 KiB of text of each); then the chunk states are folded as mapping vectors
  * (a pairwise tree of (f . g)(q) = g(f(q))) and applied to q0.
- * Results are the canonical (q_final, accept) of Alg. 2 (Theorem 2).  Built
- * states persist in the handle.
+ * Factored chunk runs (C24; on unless tuning no_factor, and only
+ * when |D| x classes x 2 B <= 48 KiB): a chunk that reaches a factorable
+ * state s (every non-absorbing image equal to one g) runs the DFA alone from
+ * g to its end and no state past s is built; when every chunk ends factored
+ * the fold takes one lookup per composition.  Results are the canonical
+ * (q_final, accept) of Alg. 2 (Theorem 2) either way.  Built states persist
+ * in the handle.
  */
 SFA_API int sfa_compile_lazy(const char* regex, const uint8_t* alphabet, int alphabet_len, uint32_t max_states,
                              sfa_handle** out);
@@ -343,7 +348,7 @@ typedef struct {
     int32_t tma_ring;         /* cap on the stage-ring depth: 0 = as deep as fits, 2..8        */
     int32_t tma_promo;        /* L2 promotion of the TMA loads: 0 none (auto), 64, 128, 256    */
     uint32_t hot_rows;        /* HOT residency: cap on the rows kept in smem (0 = all that fit) */
-    uint32_t no_factor;       /* 1: never use the FACTORED step                                */
+    uint32_t no_factor;       /* 1: never use the FACTORED step (nor factored on-the-fly runs)  */
     uint32_t dfa_copies;      /* FACTORED: cap on lane-group copies of the DFA window (0 = 32)  */
     uint32_t private_copies;  /* PRIVATE: cap on lane-group copies of the SFA table (0 = 32)    */
     uint32_t row_align;       /* TMA row length alignment: 0 auto, 64, 128 or 256              */

@@ -62,17 +62,24 @@ cudaError_t upload(T** dst, const T* src, size_t count) {
 struct LazyDev {
     uint32_t* T = nullptr;   // transition table copy (u32, cap_rows * C)
     uint16_t* maps = nullptr;  // mapping vectors (cap_rows * nD)
+    uint32_t* fg = nullptr;    // factored images (cap_rows)
+    uint16_t* dfa = nullptr;   // nD * C DFA table (factored runs)
+    uint8_t* absorbing = nullptr;  // nD
     uint8_t* cls = nullptr;
     size_t cap_rows = 0, maps_rows = 0;
     uint32_t* state = nullptr;
     uint64_t* pos = nullptr;
     uint32_t* idx = nullptr;
+    uint32_t* fd = nullptr;    // p: DFA state of factored chunks
+    uint32_t* counts = nullptr;  // 2: chunks stalled / finished unfactored in the last scan
+    uint32_t* cbuf = nullptr;  // compact-fold scratch (4 * ceil(cap_p / 1024))
     uint8_t* win = nullptr;
     uint16_t* fold = nullptr;
     uint16_t* fin = nullptr;
     size_t cap_p = 0, cap_win = 0;
     void release() {
-        for (void* q : {(void*)T, (void*)maps, (void*)cls, (void*)state, (void*)pos, (void*)idx, (void*)win, (void*)fold,
+        for (void* q : {(void*)T, (void*)maps, (void*)fg, (void*)dfa, (void*)absorbing, (void*)cls, (void*)state,
+                        (void*)pos, (void*)idx, (void*)fd, (void*)counts, (void*)cbuf, (void*)win, (void*)fold,
                         (void*)fin})
             if (q) cudaFree(q);
         *this = LazyDev{};
@@ -1046,7 +1053,10 @@ int sfa_export_sfa(const sfa_handle* h, uint32_t* table, uint32_t* maps, uint8_t
         const sfa::LazySFA& Z = *h->lazy;
         if (table)
             for (uint32_t st = 0; st < Z.nS; ++st)
-                for (int b = 0; b < 256; ++b) table[static_cast<size_t>(st) * 256 + b] = Z.T[static_cast<size_t>(st) * Z.C + Z.cls[b]];
+                for (int b = 0; b < 256; ++b) {
+                    const uint32_t t = Z.next(st, Z.cls[b]);
+                    table[static_cast<size_t>(st) * 256 + b] = t == sfa::kUnknown ? t : t & ~sfa::kFactBit;
+                }
         if (maps)
             for (size_t i = 0; i < Z.maps.size(); ++i) maps[i] = Z.maps[i];
         if (finals)
@@ -1430,15 +1440,29 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
         CU(cudaMalloc(&D.cls, 256));
         CU(cudaMemcpy(D.cls, Z.cls, 256, cudaMemcpyHostToDevice));
         CU(cudaMalloc(&D.fin, nD * sizeof(uint16_t)));
+        // the factored runs' table: row offsets 2 C delta(q, class) (C24)
+        std::vector<uint16_t> dw(static_cast<size_t>(nD) * C);
+        if (dw.size() * 2 <= sfa::kLazyFactorSmem)
+            for (size_t i = 0; i < dw.size(); ++i) dw[i] = static_cast<uint16_t>(2u * C * Z.dcls[i]);
+        CU(cudaMalloc(&D.dfa, dw.size() * sizeof(uint16_t)));
+        CU(cudaMemcpy(D.dfa, dw.data(), dw.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&D.absorbing, nD));
+        CU(cudaMemcpy(D.absorbing, Z.absorbing.data(), nD, cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&D.counts, 2 * sizeof(uint32_t)));
     }
+    // factored runs (C24): the DFA table must fit the scan's shared memory; the
+    // host stops building at factorable states exactly when the device switches
+    const bool factor = !h->tuning.no_factor && static_cast<uint64_t>(nD) * C * 2 <= sfa::kLazyFactorSmem;
     if (D.cap_p < p) {
-        for (void* q : {(void*)D.state, (void*)D.pos, (void*)D.idx, (void*)D.fold})
+        for (void* q : {(void*)D.state, (void*)D.pos, (void*)D.idx, (void*)D.fd, (void*)D.cbuf, (void*)D.fold})
             if (q) CU(cudaFree(q));
-        D.state = nullptr, D.pos = nullptr, D.idx = nullptr, D.fold = nullptr;
+        D.state = nullptr, D.pos = nullptr, D.idx = nullptr, D.fd = nullptr, D.cbuf = nullptr, D.fold = nullptr;
         D.cap_p = 0;
         CU(cudaMalloc(&D.state, p * sizeof(uint32_t)));
         CU(cudaMalloc(&D.pos, p * sizeof(uint64_t)));
         CU(cudaMalloc(&D.idx, p * sizeof(uint32_t)));
+        CU(cudaMalloc(&D.fd, p * sizeof(uint32_t)));
+        CU(cudaMalloc(&D.cbuf, 4 * ((p + 1023) / 1024) * sizeof(uint32_t)));
         CU(cudaMalloc(&D.fold, 2 * p * nD * sizeof(uint16_t)));
         D.cap_p = p;
     }
@@ -1448,36 +1472,53 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
             while (cap < Z.nS) cap *= 2;
             uint32_t* nT = nullptr;
             uint16_t* nM = nullptr;
+            uint32_t* nF = nullptr;
             CU(cudaMalloc(&nT, cap * C * sizeof(uint32_t)));
             CU(cudaMalloc(&nM, cap * nD * sizeof(uint16_t)));
-            if (D.maps_rows) CU(cudaMemcpyAsync(nM, D.maps, D.maps_rows * nD * sizeof(uint16_t), cudaMemcpyDeviceToDevice, s));
+            CU(cudaMalloc(&nF, cap * sizeof(uint32_t)));
+            if (D.maps_rows) {
+                CU(cudaMemcpyAsync(nM, D.maps, D.maps_rows * nD * sizeof(uint16_t), cudaMemcpyDeviceToDevice, s));
+                CU(cudaMemcpyAsync(nF, D.fg, D.maps_rows * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+            }
             CU(cudaStreamSynchronize(s));
             if (D.T) CU(cudaFree(D.T));
             if (D.maps) CU(cudaFree(D.maps));
+            if (D.fg) CU(cudaFree(D.fg));
             D.T = nT;
             D.maps = nM;
+            D.fg = nF;
             D.cap_rows = cap;
         }
         CU(cudaMemcpyAsync(D.T, Z.T.data(), static_cast<size_t>(Z.nS) * C * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
         if (D.maps_rows < Z.nS) {
             CU(cudaMemcpyAsync(D.maps + D.maps_rows * nD, Z.maps.data() + D.maps_rows * nD,
                                (Z.nS - D.maps_rows) * nD * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+            CU(cudaMemcpyAsync(D.fg + D.maps_rows, Z.fg.data() + D.maps_rows, (Z.nS - D.maps_rows) * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, s));
             D.maps_rows = Z.nS;
         }
         return SFA_OK;
     };
-    cudaError_t e = sfa::lazy_init(n, p, D.state, D.pos, h->sm_count, s);
+    cudaError_t e = sfa::lazy_init(n, p, D.state, D.pos, D.fd, h->sm_count, s);
     if (e != cudaSuccess) return cuda_fail(e, "lazy init");
     std::vector<uint64_t> hpos(p), hend(p);
     std::vector<uint32_t> hstate(p), stalled;
     for (uint64_t g = 0; g < p; ++g) hend[g] = (g + 1) * (n / p) + std::min<uint64_t>(g + 1, n % p);
     const uint32_t K = 4096;  // bytes of text the host builds ahead per stalled chunk and round
     std::vector<uint8_t> hwin;
+    uint32_t counts[2] = {0, 0};
     for (int round = 0;; ++round) {
         int rc = sync_tables();
         if (rc) return rc;
-        e = sfa::lazy_scan(D.T, D.cls, C, d_text, n, p, D.state, D.pos, s);
+        sfa::LazyScanArgs la;
+        la.T = D.T, la.fg = D.fg, la.drow = D.dfa, la.cls = D.cls, la.C = C, la.nD = nD, la.factor = factor;
+        la.text = d_text, la.n = n, la.p = p, la.state = D.state, la.pos = D.pos, la.fd = D.fd, la.counts = D.counts;
+        CU(cudaMemsetAsync(D.counts, 0, 2 * sizeof(uint32_t), s));
+        e = sfa::lazy_scan(la, s);
         if (e != cudaSuccess) return cuda_fail(e, "lazy scan");
+        CU(cudaMemcpyAsync(counts, D.counts, sizeof(counts), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (counts[0] == 0) break;  // nothing stalled
         CU(cudaMemcpyAsync(hpos.data(), D.pos, p * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CU(cudaMemcpyAsync(hstate.data(), D.state, p * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
@@ -1508,7 +1549,7 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
             for (size_t j = 0; j < stalled.size(); ++j) {
                 const uint32_t g = stalled[j];
                 const uint64_t len = std::min<uint64_t>(K, hend[g] - hpos[g]);
-                Z.run(hstate[g], hwin.data() + j * static_cast<size_t>(K), len);
+                Z.run(hstate[g], hwin.data() + j * static_cast<size_t>(K), len, factor);
             }
         } catch (const sfa::CompileError& ce) {
             return fail(ce.code, ce.what());
@@ -1517,8 +1558,10 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
         }
         h->lazy_build_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
-    // f_fin = f_1 . ... . f_p on the device, q_final = f_fin(q0)
-    e = sfa::lazy_fold(D.maps, D.state, p, nD, D.fold, D.fin, h->sm_count, s);
+    // f_fin = f_1 . ... . f_p on the device, q_final = f_fin(q0): by single
+    // lookups when every chunk ended factored, else as mapping vectors
+    e = counts[1] == 0 ? sfa::lazy_cfold(D.maps, D.absorbing, nD, D.state, D.fd, p, D.cbuf, D.fin, s)
+                       : sfa::lazy_fold(D.maps, D.state, D.fd, D.absorbing, p, nD, D.fold, D.fin, h->sm_count, s);
     if (e != cudaSuccess) return cuda_fail(e, "lazy fold");
     uint16_t q16 = 0;
     CU(cudaMemcpyAsync(&q16, D.fin, sizeof(uint16_t), cudaMemcpyDeviceToHost, s));

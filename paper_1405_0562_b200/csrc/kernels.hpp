@@ -133,13 +133,32 @@ cudaError_t launch_spec(const SpecArgs& a, uint32_t threads, size_t smem, cudaSt
 
 // On-the-fly construction (kernels_lazy.cu): chunk runs that stop at unbuilt transitions,
 // the gather of the text windows the host builds from, the mapping-vector fold.
-cudaError_t lazy_init(uint64_t n, uint64_t p, uint32_t* state, uint64_t* pos, int sm_count, cudaStream_t s);
-cudaError_t lazy_scan(const uint32_t* T, const uint8_t* cls, uint32_t C, const uint8_t* text, uint64_t n, uint64_t p,
-                      uint32_t* state, uint64_t* pos, cudaStream_t s);
+struct LazyScanArgs {
+    const uint32_t* T = nullptr;      // nS * C: next id | kFactBit, 0xFFFFFFFF = not built
+    const uint32_t* fg = nullptr;     // nS: the factored image g_s, 0xFFFFFFFF = not factorable
+    const uint16_t* drow = nullptr;   // nD * C: byte offset 2 C delta(q, class) of the next row (factored runs)
+    const uint8_t* cls = nullptr;     // 256
+    uint32_t C = 0, nD = 0;
+    int factor = 0;                   // switch to the DFA at the first factorable state
+    const uint8_t* text = nullptr;
+    uint64_t n = 0, p = 0;
+    uint32_t* state = nullptr;        // p: SFA state (the factorable one once switched)
+    uint64_t* pos = nullptr;          // p: next byte
+    uint32_t* fd = nullptr;           // p: the DFA state of a factored chunk, 0xFFFFFFFF = not factored
+    uint32_t* counts = nullptr;       // 2, zeroed by the caller: chunks stalled, chunks finished unfactored
+};
+constexpr uint32_t kLazyFactorSmem = 48u << 10;  // the factored run's DFA table lives in smem
+cudaError_t lazy_init(uint64_t n, uint64_t p, uint32_t* state, uint64_t* pos, uint32_t* fd, int sm_count,
+                      cudaStream_t s);
+cudaError_t lazy_scan(const LazyScanArgs& a, cudaStream_t s);
 cudaError_t lazy_gather(const uint8_t* text, uint64_t n, uint64_t p, const uint64_t* pos, const uint32_t* idx,
                         uint32_t count, uint32_t K, uint8_t* out, cudaStream_t s);
-cudaError_t lazy_fold(const uint16_t* maps, const uint32_t* state, uint64_t p, uint32_t nD, uint16_t* buf,
-                      uint16_t* out, int sm_count, cudaStream_t s);
+// f_fin = f_{c_0} . ... . f_{c_{p-1}}, c_g the chunk states (state, fd); absorbing: nD flags
+cudaError_t lazy_fold(const uint16_t* maps, const uint32_t* state, const uint32_t* fd, const uint8_t* absorbing,
+                      uint64_t p, uint32_t nD, uint16_t* buf, uint16_t* out, int sm_count, cudaStream_t s);
+// the same when every chunk is factored, by one lookup per composition (buf: 4 * ceil(p / 1024) u32)
+cudaError_t lazy_cfold(const uint16_t* maps, const uint8_t* absorbing, uint32_t nD, const uint32_t* state,
+                       const uint32_t* fd, uint64_t p, uint32_t* buf, uint16_t* out, cudaStream_t s);
 
 cudaError_t launch_scan_tma(Res mode, bool vec, const ScanArgs& a, const TmaConfig& cfg, cudaStream_t stream);
 cudaError_t launch_scan_direct(Res mode, bool vec, const DirectArgs& a, cudaStream_t stream);

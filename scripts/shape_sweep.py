@@ -17,6 +17,13 @@ cfgs = [int(c) for c in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["2", 
 shapes = [dict(), dict(tma_k=1, tma_rowb=32), dict(tma_k=2, tma_rowb=16), dict(tma_k=1, tma_rowb=16),
           dict(tma_k=2, tma_rowb=32), dict(tma_k=1, tma_rowb=64), dict(tma_k=2, tma_rowb=16, tma_ring=4),
           dict(tma_k=2, tma_rowb=16, tma_ring=6)]
+if os.environ.get("SWEEP") == "ring":
+    shapes = [dict(), dict(tma_k=1, tma_rowb=32, tma_ring=2), dict(tma_k=1, tma_rowb=32, tma_ring=3),
+              dict(tma_k=1, tma_rowb=32, tma_ring=5), dict(tma_k=1, tma_rowb=64, tma_ring=2),
+              dict(tma_k=1, tma_rowb=16, tma_ring=4), dict(tma_k=1, tma_rowb=16, tma_ring=8)]
+if os.environ.get("SWEEP") == "promo":
+    shapes = [dict(), dict(tma_promo=64), dict(tma_promo=128), dict(tma_promo=256),
+              dict(tma_k=1, tma_rowb=16, tma_promo=128), dict(tma_k=1, tma_rowb=16, tma_promo=256)]
 if os.environ.get("SWEEP") == "factored":   # the FACTORED layouts (cfg3/5): u16 R=16 vs u8 R=32, K = 1 / 2
     shapes = [dict(), dict(hot_rows=400), dict(tma_k=2, tma_rowb=16, hot_rows=400),
               dict(tma_k=2, tma_rowb=16, hot_rows=200), dict(dfa_u8=1), dict(dfa_u8=1, hot_rows=400),

@@ -8,7 +8,9 @@ Checked against the oracle: results equal Alg. 2 of the oracle DFA (Theorem
 that is small enough to build) and every transition built is coherent with
 Lemma 1 (f_{T[s][b]} = f_s . delta(., b)); a second match of the same text
 builds nothing; only the visited part of an exploding SFA (Ex. 4, |S| = n^n,
-PAPER.md:893-906) is built.
+PAPER.md:893-906) is built.  Both with the factored chunk runs (C24:
+a chunk that reaches a factorable state runs the DFA alone; no state past it
+is built) and without them (tuning no_factor: every visited state is built).
 """
 import numpy as np
 import pytest
@@ -42,15 +44,17 @@ def _lazy_coherent(sfa, d):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("no_factor", [0, 1])
 @pytest.mark.parametrize("rx,alpha,gen", [("(ab|ba)*c", b"abc", lambda n: W.cfg1_accepted(n // 2)),
                                            (*CFG2, lambda n: W.cfg2_accepted(n // 10)),
                                            (".*a[ab]{8}", b"ab", W.cfg4_text),
                                            (W.rn_regex(20), b"0123456789", lambda n: W.rn_accepted(20, n))])
-def test_lazy_parity_small(cuda_ok, rx, alpha, gen):
+def test_lazy_parity_small(cuda_ok, rx, alpha, gen, no_factor):
     import torch
     d = O.OracleDFA(rx, alpha)
     full = O.OracleSFA(d)
     sfa = P.SFA(rx, alpha, lazy=True)
+    sfa.set_tuning(no_factor=no_factor)
     text = gen(20 << 20)
     rng = np.random.default_rng(4)
     for n in (1, 100, 70_001, 5 << 20, text.size):
@@ -68,26 +72,30 @@ def test_lazy_parity_small(cuda_ok, rx, alpha, gen):
 
 
 @pytest.mark.gpu
-def test_lazy_r500_and_ra(cuda_ok):
+@pytest.mark.parametrize("no_factor", [0, 1])
+def test_lazy_r500_and_ra(cuda_ok, no_factor):
     """r_500 (|D| = 1001 with the dead state, |S| = 1,000,999) and r_a = r_500|a*
     on accepted / rejected texts: the oracle's Alg. 2, with only the visited
-    states built."""
+    states built (factored: only the states before each chunk's first
+    factorable one -- a few per 1000-byte phase, far fewer)."""
     import torch
     rx, alpha = W.rn_regex(500), b"0123456789"
     d = O.OracleDFA(rx, alpha)
     assert d.n == 1001
     sfa = P.SFA(rx, alpha, lazy=True)
+    sfa.set_tuning(no_factor=no_factor)
     t = W.rn_accepted(500, 64 << 20)
     r = t.copy()
     r[len(r) // 3] = ord("9") if r[len(r) // 3] < ord("5") else ord("0")
     for x in (t, r, t[:12_345_678], t[1:]):
         assert sfa.match_lazy(torch.from_numpy(x).cuda()) == d.run(x)
     info = sfa.info()
-    assert 1 < info["sfa_states"] < 1_000_999
+    assert 1 < info["sfa_states"] < (1_000_999 if no_factor else 300_000)
     _lazy_coherent(sfa, d)
     rxa = W.ra_regex(500)
     da = O.OracleDFA(rxa, b"0123456789a")
     sa = P.SFA(rxa, b"0123456789a", lazy=True)
+    sa.set_tuning(no_factor=no_factor)
     for x in (W.ra_text(32 << 20), t[:5 << 20]):
         assert sa.match_lazy(torch.from_numpy(x).cuda()) == da.run(x)
 
