@@ -354,7 +354,7 @@ typedef struct {
     uint32_t row_align;       /* TMA row length alignment: 0 auto, 64, 128 or 256              */
     uint32_t direct_piece;    /* bytes per thread of the short-text kernel: 0 auto, 16..4096   */
     uint32_t dfa_u8;          /* FACTORED: 1 = 32 bank-private u8 copies of the DFA window when
-                                 32 u16 copies do not fit (|D| <= 256); 0 = u16 copies      */
+                                 32 u16 copies do not fit (|D| <= 256, state-major); 0 = u16 */
 } sfa_tuning_t;
 SFA_API int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* t);
 

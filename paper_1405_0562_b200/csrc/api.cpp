@@ -407,15 +407,15 @@ struct sfa_handle {
         // Layout: the largest R of 32, 16, ... lane-group u16 copies that fits
         // (cfg4: R = 32, conflict-free, 4 instr/byte; cfg3/5: R = 16, 2-way
         // conflicts).  Tuning dfa_u8 = 1 takes 32 bank-private u8 copies instead
-        // when |D| <= 256 and 32 u16 copies do not fit: conflict-free but 3 more
-        // ALU ops per byte -- measured 17% slower than R = 16 on cfg5.
+        // when |D| <= 256 and 32 u16 copies do not fit (plan.hpp col8):
+        // conflict-free, 2 more ALU ops per byte off the dependency chain.
         uint32_t R = 32, X = 0;
         const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R
         const bool u16_32 = Rmax >= 32 && static_cast<uint64_t>(sfa::dfa_X(nD, 32)) * W <= kDfaMax;
         const bool u8_32 = tuning.dfa_u8 && !u16_32 && Rmax >= 32 && nD <= 256 &&
-                           static_cast<uint64_t>(sfa::dfa8_X(nD)) * W <= kDfaMax;
+                           static_cast<uint64_t>(nD) * sfa::dfa8_RB(W) <= kDfaMax;
         if (u8_32) {
-            X = sfa::dfa8_X(nD);
+            X = sfa::dfa8_RB(W);  // bytes per state row
         } else {
             for (; R >= 1; R /= 2) {
                 X = sfa::dfa_X(nD, R);
@@ -429,14 +429,14 @@ struct sfa_handle {
         CU(upload(&dfam, fam.data(), fam.size()));
         CU(upload(&dfg, g.data(), g.size()));
         CU(upload(&dftab, tab.data(), tab.size()));
-        dwin_bytes = (X * W + 15) & ~15u;
+        dwin_bytes = ((u8_32 ? X * nD : X * W) + 15) & ~15u;
         std::vector<uint8_t> img(dwin_bytes, 0);
         for (uint32_t j = 0; j < W; ++j)
             for (uint32_t q = 0; q < nD; ++q) {
                 const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
                 for (uint32_t c = 0; c < R; ++c) {
                     if (u8_32) {
-                        img[j * X + sfa::enc8(q, c)] = static_cast<uint8_t>(nq);
+                        img[q * X + sfa::col8(j) + 4 * c] = static_cast<uint8_t>(nq);
                     } else {
                         const uint16_t v = static_cast<uint16_t>(sfa::dfa_enc(nq, c, R));
                         std::memcpy(&img[j * X + sfa::dfa_enc(q, c, R)], &v, 2);

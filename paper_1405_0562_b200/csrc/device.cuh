@@ -412,21 +412,27 @@ struct StepDfa {
     }
 };
 
-// The same with the u8 layout (plan.hpp enc8): 32 bank-private byte copies,
-// state = enc8(g, lane); one step = PRMT + VIADDMNMX + IMAD + LDS.U8 + the
-// re-encoding of the loaded id (3 ALU ops), conflict-free where the u16
-// layout only fits 16 copies (2-way conflicts).
+// The same with the u8 layout (plan.hpp col8): 32 bank-private byte copies,
+// state = the DFA id; one step = PRMT + VIADDMNMX + 2 ALU ops for the column
+// term (off the chain) + IMAD + LDS.U8 (the chain), conflict-free where the
+// u16 layout only fits 16 copies (2-way conflicts).
 struct StepDfa8 {
-    uint32_t neg_lo, wmax, X, lane4;
+    uint32_t neg_lo, wmax, RB, lanebase;
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
-        X = t.dwin_X;
-        lane4 = lane_id() << 2;
+        RB = t.dwin_X;
+        lanebase = smem_u32(dsmem) + (lane_id() << 2);  // the table sits at dsmem offset 0
     }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
-        const uint32_t v = ld_tbl_u8(window_col(byte, neg_lo, wmax) * X + st);
-        return ((v >> 2) << 7) + (v & 3u) + lane4;
+        const uint32_t x = window_col(byte, neg_lo, wmax);
+        // the column term (x >> 2) * 128 + (x & 3) = 31 (x & ~3) + x, plus
+        // the lane and base bits -- all off the chain
+        const uint32_t c = (x & ~3u) * 31u + x + lanebase;
+        uint32_t a, v;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(st), "r"(RB), "r"(c));  // the chain: one IMAD
+        asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));                        // non-volatile: freely scheduled
+        return v;
     }
 };
 

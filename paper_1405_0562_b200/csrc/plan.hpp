@@ -44,7 +44,7 @@ struct DevTables {
     const uint16_t* dwin = nullptr;     // smem image of the DFA window table: dwin_R lane-group copies
     uint32_t dwin_bytes = 0;            // (StepDfa, dfa_enc), copied to smem offset 0
     uint32_t dwin_R = 0, dwin_X = 0;
-    uint32_t dwin_u8 = 0;               // 1: 32 bank-private u8 copies (StepDfa8, enc8), |D| <= 256
+    uint32_t dwin_u8 = 0;               // 1: 32 bank-private u8 copies (StepDfa8, col8), |D| <= 256
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;
@@ -70,13 +70,17 @@ __host__ __device__ __forceinline__ uint32_t dfa_X(uint32_t nD, uint32_t R) {
     return 128u * ((nD + 64u / R - 1) / (64u / R)) + (R < 32 ? 4u * R : 0u);  // R = 32: one lane per copy, no skew needed
 }
 
-// The u8 DFA window layout (|D| <= 256): 32 bank-private byte copies; cell
-// (q, j) of lane L is the byte at j*X + enc8(q, L), X = 128 * ceil(|D| / 4):
-// four states share lane L's word in bank L, so every lookup is conflict-free
-// at half the bytes of 32 u16 copies.  The cell holds the next DFA id.
-__host__ __device__ __forceinline__ uint32_t enc8(uint32_t q, uint32_t L) { return ((q >> 2) << 7) | (q & 3u) | (L << 2); }
-__host__ __device__ __forceinline__ uint32_t dec8(uint32_t e) { return ((e >> 7) << 2) | (e & 3u); }
-__host__ __device__ __forceinline__ uint32_t dfa8_X(uint32_t nD) { return 128u * ((nD + 3) / 4); }
+// The u8 DFA window layout (|D| <= 256): 32 bank-private byte copies,
+// state-major: cell (q, j) of lane L is the byte at q*RB + col8(j) + 4L with
+// col8(j) = ((j >> 2) << 7) | (j & 3) and RB = 128 * ceil(W / 4) -- four
+// columns share lane L's word in bank L, so every lookup is conflict-free at
+// half the bytes of 32 u16 copies.  The cell holds the next DFA id, which is
+// also the carried state: one IMAD and one LDS.U8 on the dependency chain,
+// the column term computed off it.
+__host__ __device__ __forceinline__ uint32_t enc8(uint32_t q, uint32_t) { return q; }
+__host__ __device__ __forceinline__ uint32_t dec8(uint32_t e) { return e; }
+__host__ __device__ __forceinline__ uint32_t col8(uint32_t j) { return ((j >> 2) << 7) | (j & 3u); }
+__host__ __device__ __forceinline__ uint32_t dfa8_RB(uint32_t W) { return 128u * ((W + 3) / 4); }
 // a DFA state in the factored step's encoding (either layout) and back
 __host__ __device__ __forceinline__ uint32_t dw_enc(const DevTables& t, uint32_t q, uint32_t lane) {
     return t.dwin_u8 ? enc8(q, lane) : dfa_enc(q, lane % t.dwin_R, t.dwin_R);
