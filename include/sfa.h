@@ -110,6 +110,9 @@ typedef struct {
     uint32_t has_dfa;          /* 1: results carry the minimal DFA's canonical state */
     uint64_t lazy_transitions; /* on the fly: SFA transitions built so far (sfa_states: states built) */
     double   lazy_seconds;     /* on the fly: host time spent building them inside sfa_match_lazy */
+    uint32_t dfa_window_copies;/* FACTORED step: lane-group copies of the DFA window (32: bank-private
+                                  or MIXED; 0 before the first device call or without it)       */
+    uint32_t dfa_window_hot;   /* MIXED layout: DFA states in 32 bank-private copies (0: not MIXED) */
 } sfa_info_t;
 
 /*
@@ -355,6 +358,10 @@ typedef struct {
     uint32_t direct_piece;    /* bytes per thread of the short-text kernel: 0 auto, 16..4096   */
     uint32_t dfa_u8;          /* FACTORED: 1 = 32 bank-private u8 copies of the DFA window when
                                  32 u16 copies do not fit (|D| <= 256, state-major); 0 = u16 */
+    uint32_t dfa_layout;      /* FACTORED u16 layout when 32 copies do not fit: 0 auto, 1 = R
+                                 lane-group copies, 2 = MIXED (the most visited DFA states in 32
+                                 bank-private copies, every state in one shared copy)          */
+    uint32_t dfa_hot;         /* MIXED: cap on the bank-private DFA states (0 = all that fit)   */
 } sfa_tuning_t;
 SFA_API int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* t);
 

@@ -54,6 +54,7 @@ class sfa_info_t(C.Structure):
         ("device_table_bytes", C.c_uint64), ("dfa_seconds", C.c_double), ("sfa_seconds", C.c_double),
         ("kind", C.c_uint32), ("nfa_states", C.c_uint32), ("has_dfa", C.c_uint32),
         ("lazy_transitions", C.c_uint64), ("lazy_seconds", C.c_double),
+        ("dfa_window_copies", C.c_uint32), ("dfa_window_hot", C.c_uint32),
     ]
 
 
@@ -61,7 +62,7 @@ class sfa_tuning_t(C.Structure):
     _fields_ = [("tma_k", C.c_int32), ("tma_rowb", C.c_int32), ("tma_ring", C.c_int32), ("tma_promo", C.c_int32),
                 ("hot_rows", C.c_uint32), ("no_factor", C.c_uint32), ("dfa_copies", C.c_uint32),
                 ("private_copies", C.c_uint32), ("row_align", C.c_uint32), ("direct_piece", C.c_uint32),
-                ("dfa_u8", C.c_uint32)]
+                ("dfa_u8", C.c_uint32), ("dfa_layout", C.c_uint32), ("dfa_hot", C.c_uint32)]
 
 
 class sfa_rows_plan(C.Structure):

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -117,6 +118,8 @@ struct sfa_handle {
     uint16_t* diperm = nullptr;               // HOT: device -> canonical id
     uint16_t *dfam = nullptr, *dfg = nullptr, *dftab = nullptr, *ddwin = nullptr;  // FACTORED step tables
     uint32_t dwin_bytes = 0, nfam = 0, dwin_R = 0, dwin_X = 0, dwin_u8 = 0;
+    uint32_t dwin_H = 0, dwin_hotb = 0;                     // MIXED layout (plan.hpp mix_*)
+    uint16_t *ddrank = nullptr, *ddunrank = nullptr;        // MIXED: DFA id <-> rank
     sfa_tuning_t tuning{};                    // shape knobs (sfa_set_tuning); zero = automatic
     bool factor_on() const { return tuning.no_factor == 0; }
     sfa::Tuning ktune() const {
@@ -175,7 +178,7 @@ struct sfa_handle {
                           (void**)&dfinal, (void**)&drep_off, (void**)&drep, (void**)&partials, (void**)&ticket, (void**)&dres,
                           (void**)&dplan, (void**)&gmaps, (void**)&berr, (void**)&stage[0], (void**)&stage[1], (void**)&soff[0], (void**)&soff[1], (void**)&bres,
                           (void**)&dcomp, (void**)&dpairs, (void**)&dTdev, (void**)&dfam, (void**)&dfg, (void**)&dftab,
-                          (void**)&ddwin, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
+                          (void**)&ddwin, (void**)&ddrank, (void**)&ddunrank, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
                           (void**)&spec_maps, (void**)&spec_ticket, (void**)&daux[0], (void**)&daux[1]}) {
             if (*pp) cudaFree(*pp);
             *pp = nullptr;
@@ -192,7 +195,7 @@ struct sfa_handle {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         ev_done = nullptr;
         copy_stream = nullptr;
-        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = 0;
+        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = dwin_H = dwin_hotb = 0;
         aux_bytes[0] = aux_bytes[1] = 0;
         spec_cap = 0;
         stage_cap = soff_cap = bres_cap = 0;
@@ -260,6 +263,10 @@ struct sfa_handle {
             t.dwin_R = dwin_R;
             t.dwin_X = dwin_X;
             t.dwin_u8 = dwin_u8;
+            t.dwin_H = dwin_H;
+            t.dwin_hotb = dwin_hotb;
+            t.dwin_rank = ddrank;
+            t.dwin_unrank = ddunrank;
         }
         t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin, tuning.hot_rows) : 0;
         return t;
@@ -301,6 +308,31 @@ struct sfa_handle {
         std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
         perm.assign(nS, 0);
         for (uint32_t r = 0; r < nS; ++r) perm[order[r]] = r;
+    }
+
+    // DFA states by visit frequency (the MIXED DFA window layout): the same
+    // static walk over the window columns as hot_ranking, on the minimal DFA
+    // from q0 (a factored warp runs the DFA once its chunks have synchronised).
+    // order[r] = the DFA id of rank r; cnt = visits per DFA id.
+    void dfa_ranking(std::vector<uint32_t>& order, std::vector<uint64_t>& cnt) const {
+        const uint32_t nD = A.nD;
+        cnt.assign(nD, 0);
+        const uint32_t ob = lo + W - 1 < 256 ? lo + W - 1 : lo - 1;  // a byte of column W-1
+        uint64_t x = 0x2545f4914f6cdd1dull;
+        for (int walk = 0; walk < 1024; ++walk) {
+            uint32_t q = 0;
+            for (int k = 0; k < 2048; ++k) {
+                x ^= x << 13;
+                x ^= x >> 7;
+                x ^= x << 17;
+                const uint32_t j = static_cast<uint32_t>((x >> 11) % W);
+                q = A.dfa[static_cast<size_t>(q) * 256 + (j + 1 < W ? lo + j : ob)];
+                ++cnt[q];
+            }
+        }
+        order.resize(nD);
+        for (uint32_t i = 0; i < nD; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
     }
 
     // (Re)builds the HOT tables from a ranking and writes them to the device
@@ -409,11 +441,34 @@ struct sfa_handle {
         // conflicts).  Tuning dfa_u8 = 1 takes 32 bank-private u8 copies instead
         // when |D| <= 256 and 32 u16 copies do not fit (plan.hpp col8):
         // conflict-free, 2 more ALU ops per byte off the dependency chain.
-        uint32_t R = 32, X = 0;
+        uint32_t R = 32, X = 0, H = 0;
         const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R
         const bool u16_32 = Rmax >= 32 && static_cast<uint64_t>(sfa::dfa_X(nD, 32)) * W <= kDfaMax;
         const bool u8_32 = tuning.dfa_u8 && !u16_32 && Rmax >= 32 && nD <= 256 &&
                            static_cast<uint64_t>(nD) * sfa::dfa8_RB(W) <= kDfaMax;
+        // MIXED candidate (plan.hpp mix_*): DFA states ranked by visit frequency,
+        // the largest even H whose 32 private copies + the shared copy fit
+        std::vector<uint32_t> order, rank;
+        uint32_t Hm = 0;
+        double cold = 1.0;  // walk visits outside the H hot states
+        if (!u16_32 && !u8_32 && tuning.dfa_layout != 1 && !tuning.dfa_copies) {
+            std::vector<uint64_t> cnt;
+            dfa_ranking(order, cnt);
+            const uint32_t hcap = tuning.dfa_hot ? std::max(2u, tuning.dfa_hot & ~1u) : nD;
+            for (uint32_t h = 2; h < nD && h <= hcap; h += 2) {
+                const uint64_t xm = sfa::mix_X(nD, h);
+                if (xm * W > kDfaMax || xm > 65535u) break;
+                Hm = h;
+            }
+            if (Hm) {
+                uint64_t tot = 0, hot = 0;
+                for (uint32_t r = 0; r < nD; ++r) {
+                    tot += cnt[order[r]];
+                    if (r < Hm) hot += cnt[order[r]];
+                }
+                cold = tot ? 1.0 - static_cast<double>(hot) / static_cast<double>(tot) : 1.0;
+            }
+        }
         if (u8_32) {
             X = sfa::dfa8_RB(W);  // bytes per state row
         } else {
@@ -421,28 +476,65 @@ struct sfa_handle {
                 X = sfa::dfa_X(nD, R);
                 if (R <= Rmax && static_cast<uint64_t>(X) * W <= (kDfaMax) && X <= 65535u) break;
             }
+            // smem wavefronts per warp lookup: R lane-group copies ~ 1 + log2(32/R)
+            // (two lanes per copy at R = 16: nearly always a 2-way conflict); MIXED
+            // ~ 1 + P(some lane of the warp runs in the shared copy), a lane staying
+            // there ~8.5 bytes (to the next 16-byte fix) per entry
+            if (Hm) {
+                const double est_u = R >= 1 ? 1.0 + std::log2(32.0 / R) : 1e9;
+                const double est_m = 1.0 + std::min(1.0, 1.0 - std::pow(1.0 - std::min(1.0, 8.5 * cold), 32.0));
+                if (tuning.dfa_layout == 2 || est_m < est_u) {
+                    H = Hm;
+                    R = 32;
+                    X = sfa::mix_X(nD, H);
+                }
+            }
             if (R == 0) return SFA_OK;
         }
         dwin_R = R;
         dwin_X = X;
         dwin_u8 = u8_32 ? 1u : 0u;
+        dwin_H = H;
+        dwin_hotb = 64u * H;
         CU(upload(&dfam, fam.data(), fam.size()));
         CU(upload(&dfg, g.data(), g.size()));
         CU(upload(&dftab, tab.data(), tab.size()));
         dwin_bytes = ((u8_32 ? X * nD : X * W) + 15) & ~15u;
         std::vector<uint8_t> img(dwin_bytes, 0);
-        for (uint32_t j = 0; j < W; ++j)
+        auto put16 = [&](size_t at, uint32_t v) {
+            const uint16_t v16 = static_cast<uint16_t>(v);
+            std::memcpy(&img[at], &v16, 2);
+        };
+        if (H) {  // MIXED: ranks; hot cells per lane, twin cells shared (plan.hpp)
+            rank.assign(nD, 0);
+            for (uint32_t r = 0; r < nD; ++r) rank[order[r]] = r;
+            const uint32_t hotb = dwin_hotb;
+            for (uint32_t j = 0; j < W; ++j)
+                for (uint32_t r = 0; r < nD; ++r) {
+                    const uint32_t nr = rank[dw[static_cast<size_t>(order[r]) * W + j]];
+                    put16(static_cast<size_t>(j) * X + sfa::mix_twin(r, hotb), sfa::mix_twin(nr, hotb));
+                    if (r < H)
+                        for (uint32_t L = 0; L < 32; ++L)
+                            put16(static_cast<size_t>(j) * X + sfa::mix_hot(r, L),
+                                  nr < H ? sfa::mix_hot(nr, L) : sfa::mix_twin(nr, hotb));
+                }
+            std::vector<uint16_t> rk(nD), ur(nD);
             for (uint32_t q = 0; q < nD; ++q) {
-                const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
-                for (uint32_t c = 0; c < R; ++c) {
-                    if (u8_32) {
-                        img[q * X + sfa::col8(j) + 4 * c] = static_cast<uint8_t>(nq);
-                    } else {
-                        const uint16_t v = static_cast<uint16_t>(sfa::dfa_enc(nq, c, R));
-                        std::memcpy(&img[j * X + sfa::dfa_enc(q, c, R)], &v, 2);
+                rk[q] = static_cast<uint16_t>(rank[q]);
+                ur[rank[q]] = static_cast<uint16_t>(q);
+            }
+            CU(upload(&ddrank, rk.data(), rk.size()));
+            CU(upload(&ddunrank, ur.data(), ur.size()));
+        } else {
+            for (uint32_t j = 0; j < W; ++j)
+                for (uint32_t q = 0; q < nD; ++q) {
+                    const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
+                    for (uint32_t c = 0; c < R; ++c) {
+                        if (u8_32) img[q * X + sfa::col8(j) + 4 * c] = static_cast<uint8_t>(nq);
+                        else put16(j * X + sfa::dfa_enc(q, c, R), sfa::dfa_enc(nq, c, R));
                     }
                 }
-            }
+        }
         CU(upload(reinterpret_cast<uint8_t**>(&ddwin), img.data(), img.size()));
         nfam = static_cast<uint32_t>(fams.size());
         dev_bytes += fam.size() * 4 + tab.size() * 2 + dw.size() * 2;
@@ -975,6 +1067,8 @@ int sfa_info(const sfa_handle* h, sfa_info_t* info) {
     }
     info->nfa_states = A.nfa_states;
     info->has_dfa = A.has_dfa ? 1u : 0u;
+    info->dfa_window_copies = h->dfam ? h->dwin_R : 0u;
+    info->dfa_window_hot = h->dfam ? h->dwin_H : 0u;
     return SFA_OK;
 }
 
@@ -1029,7 +1123,7 @@ int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* tu) {
         (t.row_align && t.row_align != 64 && t.row_align != 128 && t.row_align != 256) ||
         (t.dfa_copies & (t.dfa_copies - 1)) || t.dfa_copies > 32 ||
         (t.private_copies & (t.private_copies - 1)) || t.private_copies > 32 ||
-        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)) || t.dfa_u8 > 1)
+        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)) || t.dfa_u8 > 1 || t.dfa_layout > 2)
         return fail(SFA_ERR_INVALID_ARG, "bad tuning value");
     if (!tu) t.tma_promo = -1;
     std::lock_guard<std::mutex> lk(h->mu);

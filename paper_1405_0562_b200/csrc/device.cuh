@@ -23,6 +23,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "plan.hpp"
@@ -412,6 +413,42 @@ struct StepDfa {
     }
 };
 
+// The MIXED layout (plan.hpp mix_hot / mix_twin): the same one-IMAD step --
+// a hot state's cells are lane L's bank-private copy, a twin's the shared
+// copy -- plus fix(), run every 16 bytes off the byte loop: a lane whose
+// state is the twin of a hot state moves back to its own copy (arithmetic
+// only; the twin of a cold state stays).
+struct StepDfaMix {
+    uint32_t neg_lo, wmax, X, hotb, twoH, lane4;
+    __device__ void params(const DevTables& t) {
+        neg_lo = 0u - t.lo;
+        wmax = t.W - 1;
+        X = t.dwin_X;
+        hotb = t.dwin_hotb;
+        twoH = 2u * t.dwin_H;
+        lane4 = 4u * lane_id();
+    }
+    __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
+        return ld_tbl_u16(window_col(byte, neg_lo, wmax) * X + st);
+    }
+    __device__ __forceinline__ uint32_t fix(uint32_t st) const {
+        const uint32_t d = st - hotb;  // 2r for a twin (wraps for a hot state)
+        const uint32_t h = ((d & ~3u) << 5) + (d & 2u) + lane4;  // mix_hot(d / 2, lane)
+        return d < twoH ? h : st;
+    }
+};
+
+// Steps that re-normalise their state between 16-byte pieces (StepDfaMix)
+template <class T, class = void>
+struct HasFix : std::false_type {};
+template <class T>
+struct HasFix<T, std::void_t<decltype(&T::fix)>> : std::true_type {};
+template <class Step>
+__device__ __forceinline__ uint32_t maybe_fix(const Step& S, uint32_t st) {
+    if constexpr (HasFix<Step>::value) return S.fix(st);
+    else return st;
+}
+
 // The same with the u8 layout (plan.hpp col8): 32 bank-private byte copies,
 // state = the DFA id; one step = PRMT + VIADDMNMX + 2 ALU ops for the column
 // term (off the chain) + IMAD + LDS.U8 (the chain), conflict-free where the
@@ -460,7 +497,7 @@ __device__ __forceinline__ uint32_t step16(const Step& S, uint32_t st, const uin
     st = step4(S, st, v.x);
     st = step4(S, st, v.y);
     st = step4(S, st, v.z);
-    return step4(S, st, v.w);
+    return maybe_fix(S, step4(S, st, v.w));
 }
 
 // Bytes [lo, hi) (offsets within the 16-byte block v) through S.

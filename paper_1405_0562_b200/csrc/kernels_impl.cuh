@@ -341,6 +341,10 @@ struct Seg {
             StepDfa8 D;
             D.params(t);
             for (uint32_t k = __ldg(t.rep_off + s); k < e; ++k) st = D.step(st, __ldg(t.rep + k));
+        } else if (t.dwin_H) {
+            StepDfaMix D;
+            D.params(t);
+            for (uint32_t k = __ldg(t.rep_off + s); k < e; ++k) st = D.step(st, __ldg(t.rep + k));
         } else {
             StepDfa D;
             D.params(t);
@@ -534,6 +538,8 @@ __device__ __forceinline__ void scan_stages(const StepT& S, uint32_t (&st)[K], c
 #pragma unroll
                 for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
             }
+#pragma unroll
+            for (int k = 0; k < K; ++k) st[k] = maybe_fix(S, st[k]);
         }
         ring.release(lane);
     }
@@ -579,6 +585,8 @@ __device__ __forceinline__ void scan_stages_seg(const StepT& S, uint32_t (&st)[K
 #pragma unroll
                     for (int k = 0; k < K; ++k) st[k] = S.step(st[k], byte_of<3>(w[k][q]));
                 }
+#pragma unroll
+                for (int k = 0; k < K; ++k) st[k] = maybe_fix(S, st[k]);
             }
         } else {
             mbar_wait(ring.full0 + 8 * ring.slot, ring.phase);
@@ -592,6 +600,8 @@ __device__ __forceinline__ void scan_stages_seg(const StepT& S, uint32_t (&st)[K
                     if (pos == nb[k]) close(k);
                 }
             }
+#pragma unroll
+            for (int k = 0; k < K; ++k) st[k] = maybe_fix(S, st[k]);
         }
         ring.release(lane);
     }
@@ -864,6 +874,10 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 };
                 if (t.dwin_u8) {
                     StepDfa8 D;
+                    D.params(t);
+                    run_dfa(D);
+                } else if (t.dwin_H) {
+                    StepDfaMix D;
                     D.params(t);
                     run_dfa(D);
                 } else {

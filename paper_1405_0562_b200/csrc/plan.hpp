@@ -45,6 +45,11 @@ struct DevTables {
     uint32_t dwin_bytes = 0;            // (StepDfa, dfa_enc), copied to smem offset 0
     uint32_t dwin_R = 0, dwin_X = 0;
     uint32_t dwin_u8 = 0;               // 1: 32 bank-private u8 copies (StepDfa8, col8), |D| <= 256
+    // MIXED u16 layout (dwin_H > 0, StepDfaMix, mix_enc): the dwin_H most visited DFA states in
+    // 32 bank-private copies, every state once more in one shared copy; ranks by visit frequency
+    uint32_t dwin_H = 0, dwin_hotb = 0;
+    const uint16_t* dwin_rank = nullptr;    // DFA id -> rank
+    const uint16_t* dwin_unrank = nullptr;  // rank -> DFA id
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;
@@ -81,12 +86,38 @@ __host__ __device__ __forceinline__ uint32_t enc8(uint32_t q, uint32_t) { return
 __host__ __device__ __forceinline__ uint32_t dec8(uint32_t e) { return e; }
 __host__ __device__ __forceinline__ uint32_t col8(uint32_t j) { return ((j >> 2) << 7) | (j & 3u); }
 __host__ __device__ __forceinline__ uint32_t dfa8_RB(uint32_t W) { return 128u * ((W + 3) / 4); }
-// a DFA state in the factored step's encoding (either layout) and back
-__host__ __device__ __forceinline__ uint32_t dw_enc(const DevTables& t, uint32_t q, uint32_t lane) {
-    return t.dwin_u8 ? enc8(q, lane) : dfa_enc(q, lane % t.dwin_R, t.dwin_R);
+// The MIXED u16 layout (|D| too large for 32 u16 copies): DFA states ranked by
+// visit frequency; ranks r < H (even) are "hot" and every rank has a "twin".
+// Column j occupies [j*X, (j+1)*X), X = hotb + 128 * ceil(nD / 64):
+//   hot  (r, lane L): j*X + mix_hot(r, L),  mix_hot(r, L) = (r >> 1) * 128 + 4L + 2 (r & 1)
+//                     (32 bank-private copies: lane L only touches bank L; hotb = 64 H)
+//   twin (r):         j*X + mix_twin(r),    mix_twin(r) = hotb + 2r  (one copy shared by all lanes)
+// A hot cell holds the next state as mix_hot (lane L's own copy) if it is hot,
+// else as mix_twin; a twin cell always holds mix_twin (lane-independent).  Both
+// encodings are complete tables, so any mix of them runs the DFA exactly; a
+// lane in the twin copy is moved back to its private copy every 16 bytes
+// (StepDfaMix::fix) -- only the bank conflicts depend on where it runs.
+__host__ __device__ __forceinline__ uint32_t mix_hot(uint32_t r, uint32_t lane) {
+    return (r >> 1) * 128u + 4u * lane + 2u * (r & 1u);
 }
-__host__ __device__ __forceinline__ uint32_t dw_dec(const DevTables& t, uint32_t e, uint32_t lane) {
-    return t.dwin_u8 ? dec8(e) : dfa_dec(e, lane % t.dwin_R, t.dwin_R);
+__host__ __device__ __forceinline__ uint32_t mix_twin(uint32_t r, uint32_t hotb) { return hotb + 2u * r; }
+__host__ __device__ __forceinline__ uint32_t mix_X(uint32_t nD, uint32_t H) { return 64u * H + 128u * ((nD + 63) / 64); }
+__host__ __device__ __forceinline__ uint32_t mix_rank_of(uint32_t e, uint32_t hotb) {
+    return e < hotb ? 2u * (e >> 7) + ((e >> 1) & 1u) : (e - hotb) >> 1;
+}
+// a DFA state in the factored step's encoding (any layout) and back
+__device__ __forceinline__ uint32_t dw_enc(const DevTables& t, uint32_t q, uint32_t lane) {
+    if (t.dwin_u8) return enc8(q, lane);
+    if (t.dwin_H) {
+        const uint32_t r = t.dwin_rank[q];
+        return r < t.dwin_H ? mix_hot(r, lane) : mix_twin(r, t.dwin_hotb);
+    }
+    return dfa_enc(q, lane % t.dwin_R, t.dwin_R);
+}
+__device__ __forceinline__ uint32_t dw_dec(const DevTables& t, uint32_t e, uint32_t lane) {
+    if (t.dwin_u8) return dec8(e);
+    if (t.dwin_H) return t.dwin_unrank[mix_rank_of(e, t.dwin_hotb)];
+    return dfa_dec(e, lane % t.dwin_R, t.dwin_R);
 }
 
 // Residency modes that have a kernel (sfa_residency without AUTO).

@@ -29,6 +29,10 @@ if os.environ.get("SWEEP") == "factored":   # the FACTORED layouts (cfg3/5): u16
               dict(tma_k=2, tma_rowb=16, hot_rows=200), dict(dfa_u8=1), dict(dfa_u8=1, hot_rows=400),
               dict(dfa_u8=1, tma_k=2, tma_rowb=16, hot_rows=400), dict(dfa_u8=1, tma_k=2, tma_rowb=16, hot_rows=100),
               dict(tma_k=1, tma_rowb=32, hot_rows=200), dict(dfa_u8=1, tma_k=1, tma_rowb=32, hot_rows=200)]
+if os.environ.get("SWEEP") == "mixed":   # DFA window layouts of the FACTORED step (cfg3/5)
+    shapes = [dict(), dict(dfa_layout=1), dict(dfa_layout=2, dfa_hot=64), dict(dfa_layout=2, dfa_hot=40),
+              dict(dfa_layout=2, dfa_hot=16), dict(tma_k=1, tma_rowb=32), dict(tma_k=1, tma_rowb=32, hot_rows=200),
+              dict(tma_k=2, tma_rowb=16, hot_rows=200), dict(dfa_u8=1)]
 s = torch.cuda.Stream()
 for cfg in cfgs:
     rx, alpha, text = bench.workload(cfg)
@@ -54,7 +58,9 @@ for cfg in cfgs:
             ok = ref is None or got == ref
             ref = ref or got
             print(json.dumps({"cfg": cfg, "shape": sh, "steady_gbs": round(n / ms / 1e6), "single_gbs": round(n / one / 1e6),
-                              "residency": P.RES_NAMES[sfa.info()["residency"]], "same_result": ok}), flush=True)
+                              "residency": P.RES_NAMES[sfa.info()["residency"]], "same_result": ok,
+                              "dfa_hot": sfa.info()["dfa_window_hot"], "dfa_copies": sfa.info()["dfa_window_copies"]}),
+                  flush=True)
         except P.SFAError as e:
             print(json.dumps({"cfg": cfg, "shape": sh, "error": str(e)}), flush=True)
         sfa.close()

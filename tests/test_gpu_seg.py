@@ -95,11 +95,15 @@ def test_rows_private_cfg4_r16(torch_cuda):
     rows_vs_oracle(torch, sfa, *CFG4, W.cfg4_text(64 << 20), 3)
 
 
-@pytest.mark.parametrize("which", ["cfg3", "cfg4", "cfg3-u8"])
+@pytest.mark.parametrize("which", ["cfg3", "cfg4", "cfg3-u8", "cfg3-lanes", "cfg3-hot8", "cfg3-hot2"])
 def test_rows_hot_factored(torch_cuda, which):
     """HOT + FACTORED: rows switch to the DFA step after their first stages;
-    their canonical ids come back through fact_tab (u16 lane-group copies of
-    the DFA window, or the u8 bank-private layout)."""
+    their canonical ids come back through fact_tab.  DFA window layouts: AUTO
+    (cfg3: MIXED -- hot states in 32 bank-private copies, every state in one
+    shared copy; cfg4: 32 u16 copies), R = 16 lane-group copies ("lanes"), the
+    u8 bank-private layout, and MIXED with only 8 / 2 hot states (most bytes
+    run in the shared copy and move back to the private copies at every
+    16-byte fix)."""
     torch = torch_cuda
     if which.startswith("cfg3"):
         rx, alpha = W.cfg3_regex(), None
@@ -114,11 +118,20 @@ def test_rows_hot_factored(torch_cuda, which):
         rx, alpha = CFG4
         t = W.cfg4_text(64 << 20)
     sfa = P.SFA(rx, alpha)
-    if which.endswith("u8"):
-        sfa.set_tuning(dfa_u8=1)
+    knobs = {"cfg3-u8": dict(dfa_u8=1), "cfg3-lanes": dict(dfa_layout=1), "cfg3-hot8": dict(dfa_layout=2, dfa_hot=8),
+             "cfg3-hot2": dict(dfa_layout=2, dfa_hot=2)}.get(which)
+    if knobs:
+        sfa.set_tuning(**knobs)
     rows_vs_oracle(torch, sfa, rx, alpha, t, 0)
-    assert P.sfa_info(sfa.h)["residency"] == P.RES_HOT_L2
-    if which.endswith("u8"):   # and a batch through the u8 layout
+    info = P.sfa_info(sfa.h)
+    assert info["residency"] == P.RES_HOT_L2
+    hot = {"cfg3": None, "cfg4": 0, "cfg3-u8": 0, "cfg3-lanes": 0, "cfg3-hot8": 8, "cfg3-hot2": 2}[which]
+    if hot is None:
+        assert 0 < info["dfa_window_hot"] < info["dfa_states"]      # AUTO picks MIXED for cfg3
+    else:
+        assert info["dfa_window_hot"] == hot
+    assert info["dfa_window_copies"] == (16 if which == "cfg3-lanes" else 32)
+    if which != "cfg4":   # and a batch through the same layout
         texts, off = W.ragged_batch(19, 2000, 40_000, b"abcdefghijklmnopqrstuvwxyz")
         check_batch(torch, sfa, odfa(rx, alpha), texts, off)
 
