@@ -455,9 +455,10 @@ struct sfa_handle {
             std::vector<uint64_t> cnt;
             dfa_ranking(order, cnt);
             const uint32_t hcap = tuning.dfa_hot ? std::max(2u, tuning.dfa_hot & ~1u) : nD;
+            const uint64_t budget = sfa::factored_mixed_budget(smem_optin, W);
             for (uint32_t h = 2; h < nD && h <= hcap; h += 2) {
                 const uint64_t xm = sfa::mix_X(nD, h);
-                if (xm * W > kDfaMax || xm > 65535u) break;
+                if (xm * W > budget || xm > 65535u) break;
                 Hm = h;
             }
             if (Hm) {

@@ -35,7 +35,9 @@ uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin, uint32_t 
     size_t other = t.aux_bytes + t.dwin_bytes + 32;
     if (kind == 0) {
         using Sh = TmaShape<1, 32>;
-        other += Sh::kFixed + 2 * Sh::kStageBytes;
+        // FACTORED (a DFA window in smem): the SFA rows only serve the first
+        // stages of a row, the ring of 32-byte stages comes first (3 deep)
+        other += Sh::kFixed + (t.dwin_bytes ? 3 : 2) * Sh::kStageBytes;
     } else if (kind == 1) {
         other += kDirectRed + 16;
     }
@@ -43,6 +45,12 @@ uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin, uint32_t 
     size_t rows = (smem_optin - other) / (2 * static_cast<size_t>(t.W));
     if (cap) rows = std::min<size_t>(rows, cap);
     return static_cast<uint32_t>(std::min<size_t>(rows, t.nS));
+}
+
+size_t factored_mixed_budget(size_t smem_optin, uint32_t W) {
+    using Sh = TmaShape<1, 32>;
+    const size_t keep = Sh::kFixed + 3 * Sh::kStageBytes + 64u * 2u * W + 64;
+    return smem_optin > keep ? smem_optin - keep : 0;
 }
 
 size_t direct_smem_bytes(Res mode, const DevTables& t) { return kDirectRed + 16 + table_smem_bytes(mode, t); }

@@ -85,6 +85,9 @@ struct Tuning {
 };
 
 uint32_t hot_rows_for(int kind, const DevTables& t, size_t smem_optin, uint32_t cap);
+// smem the MIXED DFA window may take: what is left after a 3-deep ring of
+// 32-byte stages, the fixed part and 64 SFA hot rows (kernels.cu)
+size_t factored_mixed_budget(size_t smem_optin, uint32_t W);
 // Host: the PRIVATE layout's lane-independent pair words for R copies (StepPrivate::npairs u32).
 void build_private_pairs(const uint16_t* Trange, uint32_t nS, uint32_t W, uint32_t R, uint32_t* pairs);
 size_t direct_smem_bytes(Res mode, const DevTables& t);

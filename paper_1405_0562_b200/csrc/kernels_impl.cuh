@@ -545,6 +545,15 @@ __device__ __forceinline__ void scan_stages(const StepT& S, uint32_t (&st)[K], c
     }
 }
 
+// A warp without rows: keeps the ring's empty-barrier count (kNW arrivals per
+// stage) without reading the stages.
+__device__ __forceinline__ void follow_stages(Ring& ring, uint32_t nstages, uint32_t lane) {
+    for (uint32_t i = 0; i < nstages; ++i) {
+        mbar_wait(ring.full0 + 8 * ring.slot, ring.phase);
+        ring.release(lane);
+    }
+}
+
 // Per-row segment state of a SEG scan (row-relative positions).
 template <int K>
 struct RowSegs {
@@ -562,6 +571,18 @@ __device__ __forceinline__ void scan_stages_seg(const StepT& S, uint32_t (&st)[K
                                                 const uint32_t (&rrow)[K], Ring& ring, uint32_t i0, uint32_t i1,
                                                 uint32_t lane, const uint32_t (&nb)[K], Close&& close) {
     for (uint32_t i = i0; i < i1; ++i) {
+        // the stages before the warp's next text boundary run as a plain scan
+        // (no per-stage test); a boundary at row position nb lies in stage (nb - 1) / ROWB
+        uint32_t m = nb[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) m = min(m, nb[k]);
+        m = __reduce_min_sync(kFull, m);
+        const uint32_t j = m == 0xffffffffu ? i1 : min(i1, (m - 1) / ROWB);
+        if (j > i) {
+            scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, i, j, lane);
+            i = j - 1;
+            continue;
+        }
         const uint32_t pend = (i + 1) * ROWB;
         bool need = false;
 #pragma unroll
@@ -831,7 +852,14 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
         seg_close(k, S.id(st[k], lane));
         st[k] = S.init(lane);
     };
-    if constexpr (Step::kFactor) {
+    // A warp none of whose rows exists (the CTA has fewer rows than threads)
+    // only follows the ring: wait for each stage, release it.
+    bool any_valid = false;
+#pragma unroll
+    for (int k = 0; k < K; ++k) any_valid |= valid[k];
+    if (!__any_sync(kFull, any_valid)) {
+        follow_stages(ring, nstages, lane);
+    } else if constexpr (Step::kFactor) {
         // Stages through the SFA table until every lane's state is factorable
         // (<= 1 non-absorbing image; the image count never grows along a
         // walk), checked after stages 1, 2, 4, 8, ...; the rest with the

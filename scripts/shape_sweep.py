@@ -33,6 +33,12 @@ if os.environ.get("SWEEP") == "mixed":   # DFA window layouts of the FACTORED st
     shapes = [dict(), dict(dfa_layout=1), dict(dfa_layout=2, dfa_hot=64), dict(dfa_layout=2, dfa_hot=40),
               dict(dfa_layout=2, dfa_hot=16), dict(tma_k=1, tma_rowb=32), dict(tma_k=1, tma_rowb=32, hot_rows=200),
               dict(tma_k=2, tma_rowb=16, hot_rows=200), dict(dfa_u8=1)]
+if os.environ.get("SWEEP") == "ring2":   # FACTORED: smem for the ring instead of SFA hot rows
+    shapes = [dict(), dict(hot_rows=256), dict(hot_rows=64), dict(hot_rows=16), dict(tma_k=1, tma_rowb=16, hot_rows=64, tma_ring=4),
+              dict(tma_k=1, tma_rowb=32, hot_rows=16), dict(tma_k=1, tma_rowb=32, hot_rows=64),
+              dict(tma_k=1, tma_rowb=32, hot_rows=16, dfa_hot=56), dict(tma_k=1, tma_rowb=32, hot_rows=16, dfa_hot=48)]
+if os.environ.get("SWEEP") == "base":    # the automatic shape against the two 1-row alternatives
+    shapes = [dict(), dict(tma_k=1, tma_rowb=16), dict(tma_k=1, tma_rowb=32)]
 s = torch.cuda.Stream()
 for cfg in cfgs:
     rx, alpha, text = bench.workload(cfg)
