@@ -120,6 +120,8 @@ struct sfa_handle {
     uint32_t dwin_bytes = 0, nfam = 0, dwin_R = 0, dwin_X = 0, dwin_u8 = 0;
     uint32_t dwin_H = 0, dwin_hotb = 0;                     // MIXED layout (plan.hpp mix_*)
     uint16_t *ddrank = nullptr, *ddunrank = nullptr;        // MIXED: DFA id <-> rank
+    uint32_t *ddcpt = nullptr, *ddtwin = nullptr;           // compact source of a bank-private window
+    uint32_t dwin_hl = 0, dwin_tw = 0;
     sfa_tuning_t tuning{};                    // shape knobs (sfa_set_tuning); zero = automatic
     bool factor_on() const { return tuning.no_factor == 0; }
     sfa::Tuning ktune() const {
@@ -148,7 +150,7 @@ struct sfa_handle {
     sfa_result* dres = nullptr;       // 2 results (single-text matches and the slice ring)
     sfa_result* hres = nullptr;       // pinned
 #ifdef SFA_STAMPS
-    uint64_t* dstamps = nullptr;      // diagnostic builds: 8 stamps per CTA of the last TMA scan
+    uint64_t* dstamps = nullptr;      // diagnostic builds: 16 stamps per CTA of the last TMA scan
 #endif
     sfa::TmaPlan* dplan = nullptr;    // batch: the plan k_batch_plan writes
     void* gmaps = nullptr;            // batch: 3 tensor maps rewritten on the device
@@ -178,7 +180,7 @@ struct sfa_handle {
                           (void**)&dfinal, (void**)&drep_off, (void**)&drep, (void**)&partials, (void**)&ticket, (void**)&dres,
                           (void**)&dplan, (void**)&gmaps, (void**)&berr, (void**)&stage[0], (void**)&stage[1], (void**)&soff[0], (void**)&soff[1], (void**)&bres,
                           (void**)&dcomp, (void**)&dpairs, (void**)&dTdev, (void**)&dfam, (void**)&dfg, (void**)&dftab,
-                          (void**)&ddwin, (void**)&ddrank, (void**)&ddunrank, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
+                          (void**)&ddwin, (void**)&ddrank, (void**)&ddunrank, (void**)&ddcpt, (void**)&ddtwin, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
                           (void**)&spec_maps, (void**)&spec_ticket, (void**)&daux[0], (void**)&daux[1]}) {
             if (*pp) cudaFree(*pp);
             *pp = nullptr;
@@ -195,7 +197,7 @@ struct sfa_handle {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         ev_done = nullptr;
         copy_stream = nullptr;
-        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = dwin_H = dwin_hotb = 0;
+        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = dwin_H = dwin_hotb = dwin_hl = dwin_tw = 0;
         aux_bytes[0] = aux_bytes[1] = 0;
         spec_cap = 0;
         stage_cap = soff_cap = bres_cap = 0;
@@ -267,6 +269,10 @@ struct sfa_handle {
             t.dwin_hotb = dwin_hotb;
             t.dwin_rank = ddrank;
             t.dwin_unrank = ddunrank;
+            t.dwin_cpt = ddcpt;
+            t.dwin_hl = dwin_hl;
+            t.dwin_twin = ddtwin;
+            t.dwin_tw = dwin_tw;
         }
         t.hotH = (mode == sfa::Res::Hot && dTdev) ? sfa::hot_rows_for(kind, t, smem_optin, tuning.hot_rows) : 0;
         return t;
@@ -537,6 +543,32 @@ struct sfa_handle {
                 }
         }
         CU(upload(reinterpret_cast<uint8_t**>(&ddwin), img.data(), img.size()));
+        // compact source of a bank-private window (32 u16 copies or MIXED; the
+        // kernels expand it in smem): per (column, 128-B line) the pair word of
+        // lane 0 with bit 15 set on private targets (values < 32768), then the twin words
+        if (!u8_32 && R == 32 && X <= 32768u) {
+            const uint32_t hl = H ? H / 2 : X / 128u, hotb = dwin_hotb;
+            std::vector<uint32_t> cpt(static_cast<size_t>(W) * hl, 0);
+            auto cell = [&](uint32_t j, uint32_t r) -> uint32_t {  // lane-0 value of rank/state r, flagged
+                if (r >= (H ? H : nD)) return 0u;
+                const uint32_t q = H ? order[r] : r;
+                const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
+                const uint32_t nr = H ? rank[nq] : nq;
+                if (H && nr >= H) return sfa::mix_twin(nr, hotb);
+                return ((nr >> 1) * 128u + 2u * (nr & 1u)) | 0x8000u;
+            };
+            for (uint32_t j = 0; j < W; ++j)
+                for (uint32_t k = 0; k < hl; ++k) cpt[static_cast<size_t>(j) * hl + k] = cell(j, 2 * k) | (cell(j, 2 * k + 1) << 16);
+            CU(upload(&ddcpt, cpt.data(), cpt.size()));
+            dwin_hl = hl;
+            if (H) {
+                const uint32_t tw = (X - hotb) / 4;
+                std::vector<uint32_t> twin(static_cast<size_t>(W) * tw);
+                for (uint32_t j = 0; j < W; ++j) std::memcpy(&twin[static_cast<size_t>(j) * tw], &img[static_cast<size_t>(j) * X + hotb], tw * 4);
+                CU(upload(&ddtwin, twin.data(), twin.size()));
+                dwin_tw = tw;
+            }
+        }
         nfam = static_cast<uint32_t>(fams.size());
         dev_bytes += fam.size() * 4 + tab.size() * 2 + dw.size() * 2;
         return SFA_OK;
@@ -688,7 +720,11 @@ struct sfa_handle {
             if (rc) return rc;
             dev_bytes += static_cast<uint64_t>(nS) * W * 2 + 4ull * nS;
         }
-        CU(upload(&dimg0, A.img0.data(), A.img0.size()));
+        {  // f_s(q0) with its accept bit (bit 31): the epilogue's last lookup is one load
+            std::vector<uint32_t> ia(A.img0.size());
+            for (size_t i = 0; i < ia.size(); ++i) ia[i] = A.img0[i] | (A.dfa_final[A.img0[i]] ? 0x80000000u : 0u);
+            CU(upload(&dimg0, ia.data(), ia.size()));
+        }
         CU(upload(&dfinal, A.dfa_final.data(), A.dfa_final.size()));
         CU(upload(&drep_off, A.rep_off.data(), A.rep_off.size()));
         if (!A.rep.empty()) CU(upload(&drep, A.rep.data(), A.rep.size()));
@@ -700,7 +736,7 @@ struct sfa_handle {
         CU(cudaMemset(ticket, 0, sizeof(uint32_t)));
         CU(cudaMalloc(&dres, 2 * sizeof(sfa_result)));
 #ifdef SFA_STAMPS
-        CU(cudaMalloc(&dstamps, kMaxSlots * 8 * sizeof(uint64_t)));
+        CU(cudaMalloc(&dstamps, kMaxSlots * 16 * sizeof(uint64_t)));
 #endif
         CU(cudaMalloc(&dplan, sizeof(sfa::TmaPlan)));
         CU(cudaMalloc(&gmaps, 512));
@@ -808,7 +844,7 @@ struct sfa_handle {
             a.row_ids = row_ids;
 #ifdef SFA_STAMPS
             a.stamps = dstamps;
-            CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 8 * sizeof(uint64_t), stream));
+            CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 16 * sizeof(uint64_t), stream));
 #endif
             sfa::TmaConfig cfg;
             rc = tma_plan(mode, a.t, d_text, n, &cfg, &a.plan);
@@ -864,7 +900,7 @@ struct sfa_handle {
         a.results = d_results;
 #ifdef SFA_STAMPS
         a.stamps = dstamps;
-        CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 8 * sizeof(uint64_t), stream));
+        CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 16 * sizeof(uint64_t), stream));
 #endif
         sfa::TmaConfig cfg;
         if (!sfa::tma_choose(mode, a.t, smem_optin, ktune(), &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
@@ -1671,7 +1707,7 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
 SFA_API int sfa_diag_stamps(const sfa_handle* h, uint64_t* host, size_t n) {
     if (!h || !h->dstamps) return fail(SFA_ERR_INVALID_ARG, "no stamps");
     CU(cudaDeviceSynchronize());
-    CU(cudaMemcpy(host, h->dstamps, std::min<size_t>(n, kMaxSlots * 8) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(host, h->dstamps, std::min<size_t>(n, kMaxSlots * 16) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return SFA_OK;
 }
 #endif

@@ -360,8 +360,25 @@ struct StepHot {
     __device__ static void fill(const DevTables& t, int tid, int nthreads, uint32_t) {  // hot rows = Tdev's prefix
         copy16(reinterpret_cast<uint4*>(dsmem + t.dwin_bytes), reinterpret_cast<const uint4*>(t.Tdev), hot_bytes(t) / 16,
                tid, nthreads);
-        if (t.dwin_bytes)  // the DFA window table's smem image (dwin_R lane-group copies, built on the host)
+        if (t.dwin_cpt) {  // bank-private rows expanded from the compact source (plan.hpp DevTables::dwin_cpt)
+            uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
+            const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5, X4 = t.dwin_X >> 2, hl = t.dwin_hl;
+            const uint32_t units = t.W * hl, l4 = 4u * L;
+#pragma unroll 4
+            for (uint32_t u = w; u < units; u += nw) {
+                const uint32_t c = __ldg(t.dwin_cpt + u), j = u / hl, k = u - j * hl;
+                tbl[j * X4 + k * 32 + L] = (c & 0x7fff7fffu) + ((c >> 15) & 0x00010001u) * l4;
+            }
+            if (t.dwin_tw) {  // the shared twin copy, as is
+                const uint32_t tw = t.dwin_tw, hb4 = t.dwin_hotb >> 2, total = t.W * tw;
+                for (uint32_t i = tid; i < total; i += nthreads) {
+                    const uint32_t j = i / tw;
+                    tbl[j * X4 + hb4 + (i - j * tw)] = __ldg(t.dwin_twin + i);
+                }
+            }
+        } else if (t.dwin_bytes) {  // the DFA window table's smem image (lane-group copies, built on the host)
             copy16(reinterpret_cast<uint4*>(dsmem), reinterpret_cast<const uint4*>(t.dwin), t.dwin_bytes / 16, tid, nthreads);
+        }
     }
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;

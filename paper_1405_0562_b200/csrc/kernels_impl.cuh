@@ -49,11 +49,11 @@ namespace sfa {
 #ifdef SFA_STAMPS
 #define SFA_STAMP(i)                                                                 \
     do {                                                                             \
-        if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 8 + (i)] = globaltimer(); \
+        if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 16 + (i)] = globaltimer(); \
     } while (0)
 #define SFA_STAMP_P(i)                                                               \
     do {                                                                             \
-        if (a.stamps) a.stamps[blockIdx.x * 8 + (i)] = globaltimer();                \
+        if (a.stamps) a.stamps[blockIdx.x * 16 + (i)] = globaltimer();                \
     } while (0)
 #else
 #define SFA_STAMP(i) \
@@ -172,7 +172,7 @@ struct Comp<Step, false> {
         return acc;
     }
     __device__ static uint32_t q_final(const DevTables& t, uint32_t v, uint32_t q) {
-        return q == 0 ? t.img0[v] : t.maps16[static_cast<uint64_t>(v) * t.nD + q];
+        return q == 0 ? (t.img0[v] & 0x7fffffffu) : t.maps16[static_cast<uint64_t>(v) * t.nD + q];
     }
 };
 
@@ -193,8 +193,8 @@ __device__ __forceinline__ void load_tables(const DevTables& t, int tid, int nth
 
 template <class Step, bool VEC>
 __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& sc, sfa_result* result,
-                              const uint8_t* text, uint64_t head, uint32_t nslots, const uint32_t* q_in,
-                              int nwarps, uint8_t* red, uint32_t* flag, uint32_t* map_out) {
+                              const uint8_t* text, uint64_t head, uint32_t nslots, uint64_t tail0, uint64_t tail1,
+                              const uint32_t* q_in, int nwarps, uint8_t* red, uint32_t* flag, uint32_t* map_out) {
     using CP = Comp<Step, VEC>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nthreads = nwarps * 32;
@@ -205,37 +205,55 @@ __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& 
     bar_compute(nthreads);
     if (*flag == 0) return;
     __threadfence();  // acquire the other CTAs' partials
-    const int nfold = nwarps - 1;
-    const uint32_t per = (nslots + nfold - 1) / nfold;
-    uint8_t* slot_head = red + nfold * CP::kSlot;
-    if (warp < nfold) {
-        uint32_t b0 = min(nslots, warp * per), b1 = min(nslots, b0 + per);
-        uint32_t acc = CP::fold_slots(S, t, sc.partials + b0 * CP::kSlot, b1 - b0, CP::identity(), true);
-        CP::store(red + warp * CP::kSlot, acc);
-    } else {  // head [0, head), split over the 32 lanes
-        const uint64_t per = (head + 31) / 32;
-        const uint64_t h0 = min(head, lane * per), h1 = min(head, h0 + per);
+    // The last CTA, all warps at once: warps [0, np) fold the CTA partials,
+    // warp np runs the head [0, head), the other warps the tail [tail0,
+    // tail1) in 16-byte pieces (its bytes were prefetched into L2 at entry);
+    // slots in text order: head | partials | tail pieces.
+    const int np = min(nwarps - 2, max(1, static_cast<int>((nslots + 31) / 32)));
+    const uint32_t per = (nslots + np - 1) / np;
+    const int tw = nwarps - 1 - np;  // tail warps
+    uint32_t acc;
+    if (warp < np) {
+        const uint32_t b0 = min(nslots, warp * per), b1 = min(nslots, b0 + per);
+        acc = CP::fold_slots(S, t, sc.partials + b0 * CP::kSlot, b1 - b0, CP::identity(), true);
+        CP::store(red + (1 + warp) * CP::kSlot, acc);
+    } else if (warp == np) {  // head, split over the 32 lanes
+        const uint64_t hp = (head + 31) / 32;
+        const uint64_t h0 = min(head, lane * hp), h1 = min(head, h0 + hp);
         const uint32_t s = S.id(run_range(S, S.init(lane), text, h0, h1), lane);
-        CP::store(slot_head, CP::fold_states(S, t, s));
+        CP::store(red, CP::fold_states(S, t, s));
+    } else {
+        const uint64_t len = tail1 - tail0, ti = static_cast<uint64_t>(threadIdx.x - (np + 1) * 32);
+        const uint64_t pp = 16 * ((len + 16 * 32 * tw - 1) / (16 * 32 * tw));
+        const uint64_t p0 = min(tail1, tail0 + ti * pp), p1 = min(tail1, p0 + pp);
+        const uint32_t s = S.id(run_range(S, S.init(lane), text, p0, p1), lane);
+        CP::store(red + warp * CP::kSlot, CP::fold_states(S, t, s));
     }
     bar_compute(nthreads);
     if (warp == 0) {
-        uint32_t acc = CP::load(slot_head);
-        acc = CP::fold_slots(S, t, red, nfold, acc, false);
+        acc = CP::fold_slots(S, t, red, nwarps, CP::identity(), false);
         const uint32_t q0 = q_in ? *q_in : 0u;
-        const uint32_t q = CP::q_final(t, acc, q0);
         if (map_out)  // the whole mapping f_fin (sfa_match_map: shards of a text compose by Lemma 1)
             for (uint32_t b = 0; b < t.nD; b += 32) {
                 const uint32_t qq = b + lane;
                 const uint32_t v = CP::q_final(t, acc, qq < t.nD ? qq : 0u);
                 if (qq < t.nD) map_out[qq] = v;
             }
-        if (lane == 0) {
-            if (result) {
-                result->final_state = q;
-                result->accept = t.dfinal[q];
+        if (!VEC && q0 == 0) {  // f_fin(q0) and its accept bit in one load (DevTables::img0)
+            if (lane == 0) {
+                const uint32_t x = t.img0[acc];
+                if (result) *result = sfa_result{x & 0x7fffffffu, x >> 31};
+                *sc.ticket = 0;  // ready for the next launch (stream-ordered)
             }
-            *sc.ticket = 0;  // ready for the next launch (stream-ordered)
+        } else {
+            const uint32_t q = CP::q_final(t, acc, q0);
+            if (lane == 0) {
+                if (result) {
+                    result->final_state = q;
+                    result->accept = t.dfinal[q];
+                }
+                *sc.ticket = 0;
+            }
         }
     }
 }
@@ -358,8 +376,13 @@ struct Seg {
         return Comp<Step, false>::combine(S, t, a, b);
     }
     __device__ __noinline__ static void emit(const DevTables& t, sfa_result* res, uint32_t ti, uint32_t v) {
-        const uint32_t q = (v & kTag) ? (v & ~kTag) : t.img0[v];
-        res[ti] = sfa_result{q, t.dfinal[q]};
+        if (v & kTag) {
+            const uint32_t q = v & ~kTag;
+            res[ti] = sfa_result{q, t.dfinal[q]};
+        } else {
+            const uint32_t x = t.img0[v];
+            res[ti] = sfa_result{x & 0x7fffffffu, x >> 31};
+        }
     }
     __device__ __noinline__ static SegEl comb(const Step& S, const DevTables& t, sfa_result* res, const SegEl x,
                                               const SegEl y) {
@@ -654,7 +677,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     if (a.stamps && threadIdx.x == 0) {
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        a.stamps[blockIdx.x * 8 + 6] = smid;
+        a.stamps[blockIdx.x * 16 + 6] = smid;
     }
 #endif
     if (threadIdx.x == 0) {
@@ -878,7 +901,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 const uint32_t sid = S.id(st[k], lane);
                 if (SEG && rs.ts[k]) {
                     fam[k] = kTagFam;
-                    g[k] = dw_enc(t, t.img0[sid], lane);
+                    g[k] = dw_enc(t, t.img0[sid] & 0x7fffffffu, lane);
                 } else {
                     ok &= fact_from_id(t, sid, fam[k], g[k]);
                 }
@@ -923,7 +946,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     }
     SFA_STAMP(3);  // thread 0's rows scanned
     if (t.aux_bytes) mbar_wait(abar, 0);  // the composition image (bulk copy issued at entry)
-    if (blockIdx.x == gridDim.x - 1) run_tail();
+    if (SEG && blockIdx.x == gridDim.x - 1) run_tail();  // single texts: the tail is the epilogue's
+    SFA_STAMP(8);  // thread 0: composition image and tail done
     // canonical value of each row's running piece
     uint32_t val[K];
 #pragma unroll
@@ -934,6 +958,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             val[k] = S.id(st[k], lane);
         }
     }
+    SFA_STAMP(9);  // thread 0: canonical values
 
     if constexpr (SEG) {
         // ---- segmented composition: warp -> block -> grid ----
@@ -946,6 +971,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             if (lane == 0) slots[k * kNW + warp] = make_uint4(e.h, e.t, e.tl, e.b);
         }
         bar_compute(kNW * 32);
+        SFA_STAMP(10);  // every warp folded
         uint4* parts = reinterpret_cast<uint4*>(a.sc.partials);
         if (warp == 0) {
             const SegEl e = SG::fold_slots(S, t, a.results, slots, K * kNW, seg_identity(), false);
@@ -1003,14 +1029,14 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
             CP::store(red + (k * kNW + warp) * CP::kSlot, CP::fold_states(S, t, s));
         }
         bar_compute(kNW * 32);
+        SFA_STAMP(10);  // every warp folded
         if (warp == 0) {
             uint32_t acc = CP::fold_slots(S, t, red, K * kNW, CP::identity(), false);
             store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
-            if (blockIdx.x == gridDim.x - 1) store_partial<VEC>(a.sc.partials, gridDim.x, tail_acc);
         }
         bar_compute(kNW * 32);
         SFA_STAMP(4);  // CTA folded
-        grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, P.head, gridDim.x + 1, a.q_in, kNW, red, flag,
+        grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, P.head, gridDim.x, P.tail_start, P.n, a.q_in, kNW, red, flag,
                                  a.map_out);
         SFA_STAMP(5);
     }
@@ -1050,7 +1076,7 @@ k_scan_direct(const __grid_constant__ DirectArgs a) {
     const uint32_t acc = block_fold<Step, VEC>(S, t, s, kDirectWarps, red);
     if ((threadIdx.x >> 5) == 0) store_partial<VEC>(a.sc.partials, blockIdx.x, acc);
     bar_compute(kDirectWarps * 32);
-    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, 0, gridDim.x, a.q_in, kDirectWarps, red, flag, a.map_out);
+    grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, 0, gridDim.x, 0, 0, a.q_in, kDirectWarps, red, flag, a.map_out);
 }
 
 // ------------------------------------------------------------------------------------------

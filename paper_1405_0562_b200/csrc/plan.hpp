@@ -18,7 +18,7 @@ struct DevTables {
     uint32_t priv_R = 0;                // PRIVATE: lane-group copies (32 = bank-private), 0 = unavailable
     const uint8_t* maps32 = nullptr;    // nS * 32  f_s(q) for |D| <= 32 (identity-padded)
     const uint16_t* maps16 = nullptr;   // nS * nD  f_s(q) (any |D|; used to apply f_fin to q_in != q0)
-    const uint32_t* img0 = nullptr;     // nS       f_s(q0)
+    const uint32_t* img0 = nullptr;     // nS       f_s(q0) | [f_s(q0) in F_d] << 31 (the accept bit: one load at the end)
     const uint8_t* dfinal = nullptr;    // nD       q in F_d
     const uint32_t* rep_off = nullptr;  // nS + 1
     const uint8_t* rep = nullptr;       // representative words (bytes)
@@ -50,6 +50,14 @@ struct DevTables {
     uint32_t dwin_H = 0, dwin_hotb = 0;
     const uint16_t* dwin_rank = nullptr;    // DFA id -> rank
     const uint16_t* dwin_unrank = nullptr;  // rank -> DFA id
+    // compact source of a bank-private u16 window (32 u16 copies, or MIXED): per column j and
+    // 128-byte line k (dwin_hl lines) one word = the pair of cells of lane 0 with bit 15 of each
+    // half set where lane L adds 4L (a private target); then the shared twin words (dwin_tw per
+    // column).  The kernels expand it in smem (StepHot::fill) instead of copying the image.
+    const uint32_t* dwin_cpt = nullptr;
+    uint32_t dwin_hl = 0;
+    const uint32_t* dwin_twin = nullptr;
+    uint32_t dwin_tw = 0;
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
     uint32_t nS = 0, C = 0, nD = 0;

@@ -39,6 +39,10 @@ if os.environ.get("SWEEP") == "ring2":   # FACTORED: smem for the ring instead o
               dict(tma_k=1, tma_rowb=32, hot_rows=16, dfa_hot=56), dict(tma_k=1, tma_rowb=32, hot_rows=16, dfa_hot=48)]
 if os.environ.get("SWEEP") == "base":    # the automatic shape against the two 1-row alternatives
     shapes = [dict(), dict(tma_k=1, tma_rowb=16), dict(tma_k=1, tma_rowb=32)]
+if os.environ.get("SWEEP") == "k2":      # two rows per thread (ILP 2) with 32-byte stages, 2-deep ring
+    shapes = [dict(), dict(tma_k=2, tma_rowb=32, hot_rows=16), dict(tma_k=2, tma_rowb=32, hot_rows=16, dfa_hot=40),
+              dict(tma_k=2, tma_rowb=32, hot_rows=16, dfa_hot=24), dict(tma_k=1, tma_rowb=64, hot_rows=16),
+              dict(tma_k=1, tma_rowb=64, hot_rows=16, dfa_hot=40)]
 s = torch.cuda.Stream()
 for cfg in cfgs:
     rx, alpha, text = bench.workload(cfg)

@@ -21,9 +21,9 @@ L.sfa_diag_stamps.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
 
 
 def report(name, h, G):
-    st = np.zeros(G * 8, np.uint64)
+    st = np.zeros(G * 16, np.uint64)
     assert L.sfa_diag_stamps(h, st.ctypes.data, st.size) == 0
-    st = st.reshape(G, 8).astype(np.int64)
+    st = st.reshape(G, 16).astype(np.int64)
     live = st[:, 0] > 0
     st = st[live]
     smid = st[:, 6].copy()
@@ -34,7 +34,8 @@ def report(name, h, G):
     q = lambda c: (np.nanmin(rel[:, c]), np.nanmedian(rel[:, c]), np.nanmax(rel[:, c]))  # noqa: E731
     print(f"{name}: ctas={st.shape[0]}")
     for c, what in [(0, "entry"), (7, "first TMA issued"), (1, "tables built"), (2, "after pdl wait"),
-                    (3, "rows scanned"), (4, "CTA folded"), (5, "epilogue end")]:
+                    (3, "rows scanned"), (8, "aux+tail done"), (9, "values"), (10, "warps folded"),
+                    (4, "CTA folded"), (5, "epilogue end")]:
         mn, md, mx = q(c)
         print(f"  {what:18s} min {mn:8.2f}  median {md:8.2f}  max {mx:8.2f} us")
     scan = rel[:, 3] - rel[:, 2]
