@@ -52,7 +52,8 @@ template <class T>
 cudaError_t upload(T** dst, const T* src, size_t count) {
     *dst = nullptr;
     if (count == 0) return cudaSuccess;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), count * sizeof(T));
+    // padded to 256 B: the kernels bulk-prefetch whole 16-B granules of the tables into L2
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), (count * sizeof(T) + 255) & ~size_t(255));
     if (e != cudaSuccess) return e;
     return cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
 }
@@ -121,6 +122,9 @@ struct sfa_handle {
     uint32_t dwin_H = 0, dwin_hotb = 0;                     // MIXED layout (plan.hpp mix_*)
     uint16_t *ddrank = nullptr, *ddunrank = nullptr;        // MIXED: DFA id <-> rank
     uint32_t *ddcpt = nullptr, *ddtwin = nullptr;           // compact source of a bank-private window
+    uint32_t* dfam_bits = nullptr;                          // factored values: marked sets (one absorbing state)
+    uint16_t* dfam_img = nullptr;                           //   or absorbing images per family
+    uint32_t fam_w = 0, fam_a0 = 0;
     uint32_t dwin_hl = 0, dwin_tw = 0;
     sfa_tuning_t tuning{};                    // shape knobs (sfa_set_tuning); zero = automatic
     bool factor_on() const { return tuning.no_factor == 0; }
@@ -180,7 +184,7 @@ struct sfa_handle {
                           (void**)&dfinal, (void**)&drep_off, (void**)&drep, (void**)&partials, (void**)&ticket, (void**)&dres,
                           (void**)&dplan, (void**)&gmaps, (void**)&berr, (void**)&stage[0], (void**)&stage[1], (void**)&soff[0], (void**)&soff[1], (void**)&bres,
                           (void**)&dcomp, (void**)&dpairs, (void**)&dTdev, (void**)&dfam, (void**)&dfg, (void**)&dftab,
-                          (void**)&ddwin, (void**)&ddrank, (void**)&ddunrank, (void**)&ddcpt, (void**)&ddtwin, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
+                          (void**)&ddwin, (void**)&ddrank, (void**)&ddunrank, (void**)&ddcpt, (void**)&ddtwin, (void**)&dfam_bits, (void**)&dfam_img, (void**)&dperm, (void**)&diperm, (void**)&drep16, (void**)&dspecT,
                           (void**)&spec_maps, (void**)&spec_ticket, (void**)&daux[0], (void**)&daux[1]}) {
             if (*pp) cudaFree(*pp);
             *pp = nullptr;
@@ -197,7 +201,7 @@ struct sfa_handle {
         if (copy_stream) cudaStreamDestroy(copy_stream);
         ev_done = nullptr;
         copy_stream = nullptr;
-        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = dwin_H = dwin_hotb = dwin_hl = dwin_tw = 0;
+        priv_R = dwin_bytes = nfam = dwin_R = dwin_X = dwin_u8 = dwin_H = dwin_hotb = dwin_hl = dwin_tw = fam_w = fam_a0 = 0;
         aux_bytes[0] = aux_bytes[1] = 0;
         spec_cap = 0;
         stage_cap = soff_cap = bres_cap = 0;
@@ -208,6 +212,11 @@ struct sfa_handle {
     }
 
     bool has_comp() const { return A.nS <= kCompMaxStates; }
+    // bytes of the families' marked sets as an smem aux image (0: too large, or none)
+    uint32_t fam_aux_bytes() const {
+        const uint64_t b = (static_cast<uint64_t>(nfam) * fam_w * 4 + 15) & ~uint64_t(15);
+        return b <= 8192 ? static_cast<uint32_t>(b) : 0u;
+    }
     // mapping vectors (VEC composition, sfa_match_map, q_in chaining): D-SFA only
     bool can_vec() const { return !A.nsfa && A.nD <= 32; }
     // effective composition mode
@@ -270,6 +279,16 @@ struct sfa_handle {
             t.dwin_rank = ddrank;
             t.dwin_unrank = ddunrank;
             t.dwin_cpt = ddcpt;
+            t.fam_bits = dfam_bits;
+            t.fam_img = dfam_img;
+            if (!t.aux && dfam_bits && fam_aux_bytes()) {  // the marked sets in smem for the folds
+                t.aux = dfam_bits;
+                t.aux_bytes = fam_aux_bytes();
+                t.aux_fam = 1;
+            }
+            t.fam_w = fam_w;
+            t.fam_n = nfam;
+            t.fam_a0 = fam_a0;
             t.dwin_hl = dwin_hl;
             t.dwin_twin = ddtwin;
             t.dwin_tw = dwin_tw;
@@ -433,6 +452,27 @@ struct sfa_handle {
                     tab[static_cast<size_t>(kv.second) * nD + a] = tab[static_cast<size_t>(f2->second) * nD + abs0];
             }
         }
+        // factored chunk values (DevTables::fam_bits / fam_img): a family's marked
+        // states and their absorbing images, read by the folds (F < 2^14)
+        if (fams.size() < (1u << 14)) {
+            uint32_t nabs = 0;
+            for (uint32_t q = 0; q < nD; ++q) nabs += absorbing[q];
+            if (nabs <= 1) {
+                const uint32_t w = (nD + 31) / 32;
+                std::vector<uint32_t> bits(fams.size() * static_cast<size_t>(w), 0);
+                for (const auto& kv : fams)
+                    for (uint32_t q = 0; q < nD; ++q)
+                        if (kv.first[q] != 0xffff) bits[static_cast<size_t>(kv.second) * w + q / 32] |= 1u << (q % 32);
+                CU(upload(&dfam_bits, bits.data(), bits.size()));
+                fam_w = w;
+                fam_a0 = nabs ? abs0 : 0u;
+            } else {
+                std::vector<uint16_t> img(fams.size() * static_cast<size_t>(nD));
+                for (const auto& kv : fams)
+                    std::memcpy(&img[static_cast<size_t>(kv.second) * nD], kv.first.data(), nD * 2);
+                CU(upload(&dfam_img, img.data(), img.size()));
+            }
+        }
         // compact DFA window table (next state ids); in smem as R lane-group copies,
         // R the largest of 32, 16, ..., 1 whose copies take <= 80 KB (StepDfa)
         const uint32_t ob = lo + W - 1 < 256 ? lo + W - 1 : lo - 1;  // a byte outside the window (class `other`)
@@ -461,7 +501,9 @@ struct sfa_handle {
             std::vector<uint64_t> cnt;
             dfa_ranking(order, cnt);
             const uint32_t hcap = tuning.dfa_hot ? std::max(2u, tuning.dfa_hot & ~1u) : nD;
-            const uint64_t budget = sfa::factored_mixed_budget(smem_optin, W);
+            // (less the families' marked sets, which sit in smem as the aux image)
+            const uint64_t fb = (static_cast<uint64_t>(fams.size()) * fam_w * 4 + 15) & ~uint64_t(15);
+            const uint64_t budget = sfa::factored_mixed_budget(smem_optin, W) - (dfam_bits && fb <= 8192 ? fb : 0);
             for (uint32_t h = 2; h < nD && h <= hcap; h += 2) {
                 const uint64_t xm = sfa::mix_X(nD, h);
                 if (xm * W > budget || xm > 65535u) break;
@@ -736,7 +778,7 @@ struct sfa_handle {
         CU(cudaMemset(ticket, 0, sizeof(uint32_t)));
         CU(cudaMalloc(&dres, 2 * sizeof(sfa_result)));
 #ifdef SFA_STAMPS
-        CU(cudaMalloc(&dstamps, kMaxSlots * 16 * sizeof(uint64_t)));
+        CU(cudaMalloc(&dstamps, (kMaxSlots + 1) * 16 * sizeof(uint64_t)));
 #endif
         CU(cudaMalloc(&dplan, sizeof(sfa::TmaPlan)));
         CU(cudaMalloc(&gmaps, 512));
@@ -844,7 +886,8 @@ struct sfa_handle {
             a.row_ids = row_ids;
 #ifdef SFA_STAMPS
             a.stamps = dstamps;
-            CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 16 * sizeof(uint64_t), stream));
+            a.t.diag = reinterpret_cast<unsigned long long*>(dstamps + kMaxSlots * 16);
+            CU(cudaMemsetAsync(dstamps, 0, (kMaxSlots + 1) * 16 * sizeof(uint64_t), stream));
 #endif
             sfa::TmaConfig cfg;
             rc = tma_plan(mode, a.t, d_text, n, &cfg, &a.plan);
@@ -900,7 +943,8 @@ struct sfa_handle {
         a.results = d_results;
 #ifdef SFA_STAMPS
         a.stamps = dstamps;
-        CU(cudaMemsetAsync(dstamps, 0, kMaxSlots * 16 * sizeof(uint64_t), stream));
+        a.t.diag = reinterpret_cast<unsigned long long*>(dstamps + kMaxSlots * 16);
+        CU(cudaMemsetAsync(dstamps, 0, (kMaxSlots + 1) * 16 * sizeof(uint64_t), stream));
 #endif
         sfa::TmaConfig cfg;
         if (!sfa::tma_choose(mode, a.t, smem_optin, ktune(), &cfg)) return fail(SFA_ERR_CAPACITY, "no TMA shape fits");
@@ -1704,6 +1748,12 @@ int sfa_match_lazy(const sfa_handle* hc, const uint8_t* d_text, size_t n, sfa_st
 
 #ifdef SFA_STAMPS
 // Diagnostic builds only (include/sfa_diag.h): the stamps of the last TMA scan.
+SFA_API int sfa_diag_counters(const sfa_handle* h, uint64_t* host, size_t n) {
+    if (!h || !h->dstamps) return fail(SFA_ERR_INVALID_ARG, "no stamps");
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(host, h->dstamps + kMaxSlots * 16, std::min<size_t>(n, 16) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return SFA_OK;
+}
 SFA_API int sfa_diag_stamps(const sfa_handle* h, uint64_t* host, size_t n) {
     if (!h || !h->dstamps) return fail(SFA_ERR_INVALID_ARG, "no stamps");
     CU(cudaDeviceSynchronize());

@@ -364,16 +364,38 @@ struct StepHot {
             uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
             const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5, X4 = t.dwin_X >> 2, hl = t.dwin_hl;
             const uint32_t units = t.W * hl, l4 = 4u * L;
-#pragma unroll 4
-            for (uint32_t u = w; u < units; u += nw) {
-                const uint32_t c = __ldg(t.dwin_cpt + u), j = u / hl, k = u - j * hl;
-                tbl[j * X4 + k * 32 + L] = (c & 0x7fff7fffu) + ((c >> 15) & 0x00010001u) * l4;
+            // warp w: units [32 b, 32 b + 32) for b = w, w + nw, ...: one load per lane
+            // (one L2 round trip per 32 units), each unit broadcast to the 32 lanes
+            for (uint32_t u0 = 32 * w; u0 < units; u0 += 32 * nw) {
+                const uint32_t mine = u0 + L < units ? __ldg(t.dwin_cpt + u0 + L) : 0u;
+                const uint32_t n = min(32u, units - u0);
+                uint32_t j = u0 / hl, k = u0 - j * hl;
+                for (uint32_t i = 0; i < n; ++i) {
+                    const uint32_t c = __shfl_sync(0xffffffffu, mine, i);
+                    tbl[j * X4 + k * 32 + L] = (c & 0x7fff7fffu) + ((c >> 15) & 0x00010001u) * l4;
+                    if (++k == hl) {
+                        k = 0;
+                        ++j;
+                    }
+                }
             }
-            if (t.dwin_tw) {  // the shared twin copy, as is
+            if (t.dwin_tw) {  // the shared twin copy, as is: 4 loads in flight per thread
                 const uint32_t tw = t.dwin_tw, hb4 = t.dwin_hotb >> 2, total = t.W * tw;
-                for (uint32_t i = tid; i < total; i += nthreads) {
-                    const uint32_t j = i / tw;
-                    tbl[j * X4 + hb4 + (i - j * tw)] = __ldg(t.dwin_twin + i);
+                for (uint32_t i0 = tid; i0 < total; i0 += 4 * nthreads) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t i = i0 + r * nthreads;
+                        v[r] = i < total ? __ldg(t.dwin_twin + i) : 0u;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t i = i0 + r * nthreads;
+                        if (i < total) {
+                            const uint32_t j = i / tw;
+                            tbl[j * X4 + hb4 + (i - j * tw)] = v[r];
+                        }
+                    }
                 }
             }
         } else if (t.dwin_bytes) {  // the DFA window table's smem image (lane-group copies, built on the host)
@@ -500,6 +522,42 @@ __device__ __forceinline__ uint32_t fact_to_id(const DevTables& t, uint32_t fam,
     return __ldg(t.fact_tab + fam * t.nD + dw_dec(t, st, lane_id()));
 }
 
+// Factored chunk values (DevTables::fam_bits / fam_img): bit 30 tags (F, g),
+// F in bits 16..29, g (a DFA id) in bits 0..15; untagged values are SFA ids.
+constexpr uint32_t kFact = 0x40000000u;
+__device__ __forceinline__ bool fact_values(const DevTables& t) { return t.fam_bits || t.fam_img; }
+__device__ __forceinline__ uint32_t fact_pack(uint32_t fam, uint32_t g) { return kFact | (fam << 16) | g; }
+// f_(F, g)(q): the absorbing image of a marked q, else g
+__device__ __forceinline__ uint32_t fam_apply(const DevTables& t, uint32_t F, uint32_t g, uint32_t q) {
+    if (t.aux_fam) return (lds_u32(smem_u32(dsmem) + t.aux_off + 4u * (F * t.fam_w + (q >> 5))) >> (q & 31)) & 1u ? t.fam_a0 : g;
+    if (t.fam_bits) return (__ldg(t.fam_bits + F * t.fam_w + (q >> 5)) >> (q & 31)) & 1u ? t.fam_a0 : g;
+    const uint32_t m = __ldg(t.fam_img + F * t.nD + q);
+    return m != 0xffffu ? m : g;
+}
+// Diagnostic builds with -DSFA_COUNTERS: count an event (sfa_diag_counters):
+// 0 combine_fact, 1 combine_ids, 2 combine_slow, 3 replay (per warp; the
+// atomics perturb the timings, so the stamp build leaves them out)
+#if defined(SFA_STAMPS) && defined(SFA_COUNTERS)
+#define SFA_CTR(t, i)                                 \
+    do {                                              \
+        if ((t).diag && (threadIdx.x & 31) == 0) atomicAdd((t).diag + (i), 1ull); \
+    } while (0)
+#else
+#define SFA_CTR(t, i) \
+    do {              \
+    } while (0)
+#endif
+
+// an SFA id as a factored value when it is factorable
+__device__ __forceinline__ uint32_t fact_of_id(const DevTables& t, uint32_t s) {
+    const uint32_t fa = __ldg(t.fact_fam + s);
+    return fa != 0xffffu ? fact_pack(fa, __ldg(t.fact_g + s)) : s;
+}
+// a factored value's canonical SFA id
+__device__ __forceinline__ uint32_t fact_value_id(const DevTables& t, uint32_t v) {
+    return __ldg(t.fact_tab + ((v >> 16) & 0x3fffu) * t.nD + (v & 0xffffu));
+}
+
 // 4 text bytes of one word, in text order (little-endian)
 template <class Step>
 __device__ __forceinline__ uint32_t step4(const Step& S, uint32_t st, uint32_t w) {
@@ -583,6 +641,7 @@ __device__ __forceinline__ uint32_t vec_fold_ids(const uint8_t* __restrict__ map
 // f_I -w-> s_b (Lemma 1), w = the representative word of s_b.
 template <class Step>
 __device__ __forceinline__ uint32_t replay(const Step& S, const DevTables& t, uint32_t sa, uint32_t sb, uint32_t lane) {
+    SFA_CTR(t, 3);
     uint32_t st = S.from_id(sa, lane);
     if (t.rep16) {  // depth <= 15: the word in one 16-byte slot, its length in byte 15
         const uint4 w = __ldg(t.rep16 + sb);

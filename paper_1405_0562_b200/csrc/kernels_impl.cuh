@@ -55,7 +55,14 @@ namespace sfa {
     do {                                                                             \
         if (a.stamps) a.stamps[blockIdx.x * 16 + (i)] = globaltimer();                \
     } while (0)
+#define SFA_STAMP_AT(ptr, i)                                                         \
+    do {                                                                             \
+        if ((ptr) && threadIdx.x == 0) (ptr)[blockIdx.x * 16 + (i)] = globaltimer(); \
+    } while (0)
 #else
+#define SFA_STAMP_AT(ptr, i) \
+    do {                     \
+    } while (0)
 #define SFA_STAMP(i) \
     do {             \
     } while (0)
@@ -95,7 +102,7 @@ struct Comp<Step, true> {
     __device__ static uint32_t identity() { return lane_id(); }
     // maps32: its smem copy when the aux image holds it
     __device__ static const uint8_t* maps(const DevTables& t) {
-        return t.aux_maps ? dsmem + table_bytes<Step>(t) + t.aux_maps_off : t.maps32;
+        return t.aux_maps ? dsmem + t.aux_off + t.aux_maps_off : t.maps32;
     }
     __device__ static uint32_t fold_states(const Step&, const DevTables& t, uint32_t s) { return vec_fold_ids(maps(t), s); }
     __device__ static uint32_t combine(const Step&, const DevTables&, uint32_t a, uint32_t b) { return vec_compose(a, b); }
@@ -122,15 +129,43 @@ struct Comp<Step, false> {
     __device__ __forceinline__ static uint32_t combine(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
         if (a == 0) return b;  // f_I . f = f
         if (b == 0) return a;
+        // factored values stay factored (and SFA ids become factored when they
+        // can) unless the composition table sits in smem
+        if (a & b & kFact)  // both factored: (F1, g1) . (F2, g2) = (F1, f_(F2, g2)(g1)), inline
+            return (a & 0xffff0000u) | fam_apply(t, (b >> 16) & 0x3fffu, b & 0xffffu, a & 0xffffu);
+        if (((a | b) & kFact) || (fact_values(t) && !t.aux_comp)) return combine_fact(S, t, a, b);
+        return combine_ids(S, t, a, b);
+    }
+    // two canonical SFA ids
+    __device__ __forceinline__ static uint32_t combine_ids(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
+        SFA_CTR(t, 1);
         if (t.comp) {  // its smem copy when the aux image holds it
-            const void* c = t.aux_comp ? static_cast<const void*>(dsmem + table_bytes<Step>(t)) : t.comp;
+            const void* c = t.aux_comp ? static_cast<const void*>(dsmem + t.aux_off) : t.comp;
             const uint32_t i = a * t.nS + b;
             return t.comp_u8 ? static_cast<const uint8_t*>(c)[i] : static_cast<const uint16_t*>(c)[i];
         }
         return combine_slow(S, t, a, b);
     }
+    // A factored value on either side (Step policies with FACTORED chunk values):
+    // (F1, g1) . b = (F1, f_b(g1)) -- f_b(g1) from b's family when b is factored
+    // (fam_apply, L1-resident), else from maps16; an SFA id a on the left is
+    // factored first when it can be, else b goes back to its canonical id.
+    __device__ __noinline__ static uint32_t combine_fact(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
+        SFA_CTR(t, 0);
+        if (!(a & kFact)) {
+            const uint32_t fa = __ldg(t.fact_fam + a);
+            if (fa == 0xffffu) return combine_ids(S, t, a, (b & kFact) ? fact_value_id(t, b) : b);
+            a = fact_pack(fa, __ldg(t.fact_g + a));
+        }
+        if (!(b & kFact) && !t.maps16) return combine_ids(S, t, fact_value_id(t, a), b);
+        const uint32_t g1 = a & 0xffffu;
+        const uint32_t g = (b & kFact) ? fam_apply(t, (b >> 16) & 0x3fffu, b & 0xffffu, g1)
+                                       : __ldg(t.maps16 + static_cast<uint64_t>(b) * t.nD + g1);
+        return (a & 0xffff0000u) | g;
+    }
     // no composition table (|S| > 4096): a call, so the folds stay small
     __device__ __noinline__ static uint32_t combine_slow(const Step& S, const DevTables& t, uint32_t a, uint32_t b) {
+        SFA_CTR(t, 2);
         if (t.fact_fam && t.maps16) {
             // a factorable: f_a = (family F, g) sends its unmarked q to g and the
             // marked ones to absorbing states, which f_b fixes; so f_a . f_b =
@@ -147,10 +182,43 @@ struct Comp<Step, false> {
     // the 32 lanes' ids, in lane order, folded by a shuffle tree; result in every lane
     __device__ static uint32_t fold_states(const Step& S, const DevTables& t, uint32_t s) {
         const uint32_t lane = lane_id();
+        if (t.aux_comp && !fact_values(t)) {  // ids through the smem composition table: a tight LDS tree
+            const uint32_t base = smem_u32(dsmem) + t.aux_off, nS = t.nS;
+            const bool u8 = t.comp_u8 != 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_down_sync(kFull, s, d);
-            if ((lane & (2 * d - 1)) == 0) s = combine(S, t, s, o);
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_down_sync(kFull, s, d);
+                const uint32_t i = s * nS + o;
+                const uint32_t v = u8 ? lds_u8(base + i) : lds_u16(base + 2 * i);
+                const uint32_t c = s == 0 ? o : (o == 0 ? s : v);
+                s = (lane & (2 * d - 1)) == 0 ? c : s;
+            }
+            return __shfl_sync(kFull, s, 0);
+        }
+        if (fact_values(t)) {  // factored values: the inline (F, g) rule, the rest by combine
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_down_sync(kFull, s, d);
+                if ((lane & (2 * d - 1)) == 0) {
+                    if (s & o & kFact) s = (s & 0xffff0000u) | fam_apply(t, (o >> 16) & 0x3fffu, o & 0xffffu, s & 0xffffu);
+                    else s = combine(S, t, s, o);
+                }
+            }
+            return __shfl_sync(kFull, s, 0);
+        }
+        if (t.comp) {  // a table lookup: every lane combines (no divergence), the tree keeps its lanes
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_down_sync(kFull, s, d);
+                const uint32_t c = combine(S, t, s, o);
+                s = (lane & (2 * d - 1)) == 0 ? c : s;
+            }
+        } else {
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_down_sync(kFull, s, d);
+                if ((lane & (2 * d - 1)) == 0) s = combine(S, t, s, o);
+            }
         }
         return __shfl_sync(kFull, s, 0);
     }
@@ -172,6 +240,7 @@ struct Comp<Step, false> {
         return acc;
     }
     __device__ static uint32_t q_final(const DevTables& t, uint32_t v, uint32_t q) {
+        if (v & kFact) return fam_apply(t, (v >> 16) & 0x3fffu, v & 0xffffu, q);
         return q == 0 ? (t.img0[v] & 0x7fffffffu) : t.maps16[static_cast<uint64_t>(v) * t.nD + q];
     }
 };
@@ -194,17 +263,21 @@ __device__ __forceinline__ void load_tables(const DevTables& t, int tid, int nth
 template <class Step, bool VEC>
 __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& sc, sfa_result* result,
                               const uint8_t* text, uint64_t head, uint32_t nslots, uint64_t tail0, uint64_t tail1,
-                              const uint32_t* q_in, int nwarps, uint8_t* red, uint32_t* flag, uint32_t* map_out) {
+                              const uint32_t* q_in, int nwarps, uint8_t* red, uint32_t* flag, uint32_t* map_out,
+                              uint64_t* stamps = nullptr) {
     using CP = Comp<Step, VEC>;
+    (void)stamps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nthreads = nwarps * 32;
-    if (warp == 0) {
-        __threadfence();
-        if (lane == 0) *flag = (atomicAdd(sc.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (warp == 0 && lane == 0) {  // the partial (stored by this thread) is released with the ticket
+        uint32_t old;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(sc.ticket) : "memory");
+        *flag = old == gridDim.x - 1 ? 1u : 0u;
     }
     bar_compute(nthreads);
     if (*flag == 0) return;
     __threadfence();  // acquire the other CTAs' partials
+    SFA_STAMP_AT(stamps, 11);  // last CTA: ticket taken
     // The last CTA, all warps at once: warps [0, np) fold the CTA partials,
     // warp np runs the head [0, head), the other warps the tail [tail0,
     // tail1) in 16-byte pieces (its bytes were prefetched into L2 at entry);
@@ -220,18 +293,29 @@ __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& 
     } else if (warp == np) {  // head, split over the 32 lanes
         const uint64_t hp = (head + 31) / 32;
         const uint64_t h0 = min(head, lane * hp), h1 = min(head, h0 + hp);
-        const uint32_t s = S.id(run_range(S, S.init(lane), text, h0, h1), lane);
+        uint32_t s = S.id(run_range(S, S.init(lane), text, h0, h1), lane);
+        if (!VEC && fact_values(t) && s) s = fact_of_id(t, s);
         CP::store(red, CP::fold_states(S, t, s));
     } else {
         const uint64_t len = tail1 - tail0, ti = static_cast<uint64_t>(threadIdx.x - (np + 1) * 32);
         const uint64_t pp = 16 * ((len + 16 * 32 * tw - 1) / (16 * 32 * tw));
         const uint64_t p0 = min(tail1, tail0 + ti * pp), p1 = min(tail1, p0 + pp);
-        const uint32_t s = S.id(run_range(S, S.init(lane), text, p0, p1), lane);
+        uint32_t s = S.id(run_range(S, S.init(lane), text, p0, p1), lane);
+        if (!VEC && fact_values(t) && s) s = fact_of_id(t, s);
         CP::store(red + warp * CP::kSlot, CP::fold_states(S, t, s));
     }
     bar_compute(nthreads);
+    SFA_STAMP_AT(stamps, 12);  // partials, head and tail folded
     if (warp == 0) {
         acc = CP::fold_slots(S, t, red, nwarps, CP::identity(), false);
+        SFA_STAMP_AT(stamps, 13);  // final fold
+#ifdef SFA_STAMPS
+        {  // diagnostic: the same fold again (warm caches)
+            const uint32_t again = CP::fold_slots(S, t, red, nwarps, CP::identity(), false);
+            SFA_STAMP_AT(stamps, 14);
+            if (again != acc) acc = 0xdeadbeefu;
+        }
+#endif
         const uint32_t q0 = q_in ? *q_in : 0u;
         if (map_out)  // the whole mapping f_fin (sfa_match_map: shards of a text compose by Lemma 1)
             for (uint32_t b = 0; b < t.nD; b += 32) {
@@ -239,7 +323,7 @@ __device__ void grid_epilogue(const Step& S, const DevTables& t, const Scratch& 
                 const uint32_t v = CP::q_final(t, acc, qq < t.nD ? qq : 0u);
                 if (qq < t.nD) map_out[qq] = v;
             }
-        if (!VEC && q0 == 0) {  // f_fin(q0) and its accept bit in one load (DevTables::img0)
+        if (!VEC && q0 == 0 && !(acc & kFact)) {  // f_fin(q0) and its accept bit in one load (DevTables::img0)
             if (lane == 0) {
                 const uint32_t x = t.img0[acc];
                 if (result) *result = sfa_result{x & 0x7fffffffu, x >> 31};
@@ -317,6 +401,39 @@ __device__ __forceinline__ SegEl shfl_down_el(const SegEl& e, int d) {
                  __shfl_down_sync(kFull, e.b, d)};
 }
 
+// The tables the folds and the epilogue read from global memory, bulk-
+// prefetched into L2 at kernel entry (the streamed text is evict-first, so
+// they stay): otherwise each dependent lookup of the last CTA's fold can be
+// a DRAM miss.  CTA 0 takes the small tables, CTAs 1.. the large ones in
+// 1 MiB pieces (<= 8 MiB each).
+__device__ __forceinline__ void prefetch_span(const void* p, uint64_t bytes, uint32_t piece, uint32_t npieces) {
+    if (!p || !bytes) return;
+    bytes = (bytes + 15) & ~uint64_t(15);
+    const uint64_t per = 1u << 20, n = (bytes + per - 1) / per;
+    for (uint64_t j = piece; j < n; j += npieces) {
+        const uint64_t o = j * per;
+        bulk_prefetch_l2(static_cast<const uint8_t*>(p) + o, static_cast<uint32_t>(min(per, bytes - o)));
+    }
+}
+__device__ inline void prefetch_fold_tables(const DevTables& t, uint32_t cta, uint32_t nctas) {
+    const uint64_t nS = t.nS, nD = t.nD;
+    if (cta == 0) {
+        prefetch_span(t.img0, nS * 4, 0, 1);
+        prefetch_span(t.dfinal, nD, 0, 1);
+        prefetch_span(t.fam_bits, static_cast<uint64_t>(t.fam_n) * t.fam_w * 4, 0, 1);
+        prefetch_span(t.fam_img, static_cast<uint64_t>(t.fam_n) * nD * 2, 0, 1);
+        prefetch_span(t.dwin_unrank, nD * 2, 0, 1);
+        prefetch_span(t.dwin_rank, nD * 2, 0, 1);
+        prefetch_span(t.fact_fam, nS * 2, 0, 1);
+        prefetch_span(t.fact_g, nS * 2, 0, 1);
+        prefetch_span(t.fact_tab, static_cast<uint64_t>(t.fam_n) * nD * 2, 0, 1);
+        return;
+    }
+    const uint64_t m16 = nS * nD * 2, cb = nS * nS * (t.comp_u8 ? 1 : 2);
+    if (m16 <= (8u << 20)) prefetch_span(t.maps16, m16, cta - 1, nctas - 1);
+    if (t.comp && !t.aux_comp && cb <= (8u << 20)) prefetch_span(t.comp, cb, cta - 1, nctas - 1);
+}
+
 // The boundaries of a batch range: text i = [start(i), start(i+1)).
 struct Bounds {
     const uint64_t* off;  // count + 1 absolute offsets; nullptr: equal texts of `len` bytes
@@ -351,6 +468,7 @@ struct Seg {
     // f_s(q): the mapping table, else Lemma-1 replay of rep(s) through the DFA
     // window table (smem; kTag values only come from FACTORED warps, which have it)
     __device__ __noinline__ static uint32_t apply(const DevTables& t, uint32_t s, uint32_t q) {
+        if (s & kFact) return fam_apply(t, (s >> 16) & 0x3fffu, s & 0xffffu, q);
         if (t.maps16) return __ldg(t.maps16 + static_cast<uint64_t>(s) * t.nD + q);
         const uint32_t lane = lane_id();
         uint32_t st = dw_enc(t, q, lane);
@@ -376,8 +494,8 @@ struct Seg {
         return Comp<Step, false>::combine(S, t, a, b);
     }
     __device__ __noinline__ static void emit(const DevTables& t, sfa_result* res, uint32_t ti, uint32_t v) {
-        if (v & kTag) {
-            const uint32_t q = v & ~kTag;
+        if (v & (kTag | kFact)) {
+            const uint32_t q = (v & kTag) ? v & ~kTag : fam_apply(t, (v >> 16) & 0x3fffu, v & 0xffffu, 0u);
             res[ti] = sfa_result{q, t.dfinal[q]};
         } else {
             const uint32_t x = t.img0[v];
@@ -698,6 +816,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 mbar_expect_tx(cbar, stage_bytes);
                 bulk_g2s(smem_u32(staging), Step::staged_src(a.t), stage_bytes, cbar);
             }
+            if (gridDim.x > 1) prefetch_fold_tables(a.t, blockIdx.x, gridDim.x);
             if (a.t.aux_bytes) {  // composition aux image: needed only at the fold
                 const uint32_t tb = static_cast<uint32_t>((Step::smem_bytes(a.t) + 15) & ~size_t(15));
                 mbar_expect_tx(abar, a.t.aux_bytes);
@@ -765,6 +884,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
     // hot loop ([R+UR]), one IADD per byte less.
     if (stage_bytes) mbar_wait(cbar, 0);
     load_tables<Step>(t, threadIdx.x, kNW * 32, true, stage_bytes ? smem_u32(staging) : 0u);
+    if (t.aux_fam) mbar_wait(abar, 0);  // the marked sets: a batch may finish texts (emit) mid-scan
     __syncwarp();
     if (lane == 0) mbar_arrive(rbar);
     bar_compute(kNW * 32);
@@ -913,7 +1033,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                         const uint32_t g0 = dw_enc(t, 0u, lane);
                         auto close_fact = [&](int k) {
                             const uint32_t v = fam[k] == kTagFam ? (kTag | dw_dec(t, g[k], lane))
-                                                                 : fact_to_id(t, fam[k], g[k]);
+                                               : fact_values(t) ? fact_pack(fam[k], dw_dec(t, g[k], lane))
+                                                                : fact_to_id(t, fam[k], g[k]);
                             seg_close(k, v);
                             fam[k] = kTagFam;
                             g[k] = g0;
@@ -953,7 +1074,9 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         if (factored) {
-            val[k] = (SEG && fam[k] == kTagFam) ? (kTag | dw_dec(t, g[k], lane)) : fact_to_id(t, fam[k], g[k]);
+            if (SEG && fam[k] == kTagFam) val[k] = kTag | dw_dec(t, g[k], lane);
+            else if (!VEC && fact_values(t) && !a.row_ids) val[k] = fact_pack(fam[k], dw_dec(t, g[k], lane));
+            else val[k] = fact_to_id(t, fam[k], g[k]);
         } else {
             val[k] = S.id(st[k], lane);
         }
@@ -1037,7 +1160,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
         bar_compute(kNW * 32);
         SFA_STAMP(4);  // CTA folded
         grid_epilogue<Step, VEC>(S, t, a.sc, a.result, a.text, P.head, gridDim.x, P.tail_start, P.n, a.q_in, kNW, red, flag,
-                                 a.map_out);
+                                 a.map_out, a.stamps);
         SFA_STAMP(5);
     }
 }
@@ -1201,6 +1324,8 @@ template <class Step, int K, int ROWB, bool VEC, bool SEG>
 cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, unsigned grid, cudaStream_t stream) {
     using Sh = TmaShape<K, ROWB>;
     auto kern = k_scan_tma<Step, K, ROWB, VEC, SEG>;
+    ScanArgs a2 = a;
+    a2.t.aux_off = static_cast<uint32_t>(table_bytes<Step>(a.t));
     const uint32_t tbytes = static_cast<uint32_t>(table_bytes<Step>(a.t) + a.t.aux_bytes);
     const uint32_t sbytes = cfg.staged ? Step::staged_bytes(a.t) : 0u;
     const size_t smem = tbytes + sbytes + Sh::kFixed + static_cast<size_t>(cfg.nring) * Sh::kStageBytes;
@@ -1215,7 +1340,7 @@ cudaError_t tma_launch_t(const ScanArgs& a, const TmaConfig& cfg, unsigned grid,
         e = host_maps(a, cfg, &maps);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(kern, grid, (kNW + 1) * 32, smem, stream, maps, a, tbytes, sbytes, cfg.nring);
+    return launch_pdl(kern, grid, (kNW + 1) * 32, smem, stream, maps, a2, tbytes, sbytes, cfg.nring);
 }
 
 template <class Step, bool VEC, bool SEG>
@@ -1238,7 +1363,9 @@ cudaError_t direct_launch(const DirectArgs& a, cudaStream_t stream) {
     cudaError_t e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
     const uint64_t ctas = (a.npieces + kDirectWarps * 32 - 1) / (kDirectWarps * 32);
-    return launch_pdl(kern, static_cast<unsigned>(ctas), kDirectWarps * 32, smem, stream, a);
+    DirectArgs a2 = a;
+    a2.t.aux_off = static_cast<uint32_t>(table_bytes<Step>(a.t));
+    return launch_pdl(kern, static_cast<unsigned>(ctas), kDirectWarps * 32, smem, stream, a2);
 }
 
 }  // namespace detail

@@ -54,14 +54,26 @@ struct DevTables {
     // 128-byte line k (dwin_hl lines) one word = the pair of cells of lane 0 with bit 15 of each
     // half set where lane L adds 4L (a private target); then the shared twin words (dwin_tw per
     // column).  The kernels expand it in smem (StepHot::fill) instead of copying the image.
+    // Factored composition (kernels_impl.cuh Comp): a chunk value (F, g) = fact_pack(F, g) keeps
+    // its form through the folds; (F1, g1) . (F2, g2) = (F1, marked_F2(g1) ? img_F2(g1) : g2).
+    // fam_bits[F * fam_w + q / 32] bit q % 32 = q marked in F (every marked q goes to the one
+    // absorbing state fam_a0), else fam_img[F * nD + q] = img_F(q) or 0xFFFF (unmarked).
+    const uint32_t* fam_bits = nullptr;
+    const uint16_t* fam_img = nullptr;
+    uint32_t fam_w = 0, fam_a0 = 0, fam_n = 0;  // fam_n: families
     const uint32_t* dwin_cpt = nullptr;
     uint32_t dwin_hl = 0;
     const uint32_t* dwin_twin = nullptr;
     uint32_t dwin_tw = 0;
     const uint32_t* aux = nullptr;
     uint32_t aux_bytes = 0, aux_comp = 0, aux_maps = 0, aux_maps_off = 0;
+    uint32_t aux_off = 0;               // dsmem offset of the aux image (= the step table's bytes; set per launch)
+    uint32_t aux_fam = 0;               // the aux image is fam_bits (factored handles without an smem table)
     uint32_t nS = 0, C = 0, nD = 0;
     uint32_t lo = 0, W = 0;             // byte window: columns lo..lo+W-2, column W-1 = every other byte
+#ifdef SFA_STAMPS
+    unsigned long long* diag = nullptr;  // diagnostic builds: event counters (sfa_diag_counters)
+#endif
 };
 
 // R lane-group copies of a u16 table (R | 32; lane L uses copy L % R, which

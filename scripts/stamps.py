@@ -18,6 +18,7 @@ import bench  # noqa: E402
 
 L = P.lib()
 L.sfa_diag_stamps.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+L.sfa_diag_counters.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
 
 
 def report(name, h, G):
@@ -35,9 +36,13 @@ def report(name, h, G):
     print(f"{name}: ctas={st.shape[0]}")
     for c, what in [(0, "entry"), (7, "first TMA issued"), (1, "tables built"), (2, "after pdl wait"),
                     (3, "rows scanned"), (8, "aux+tail done"), (9, "values"), (10, "warps folded"),
-                    (4, "CTA folded"), (5, "epilogue end")]:
+                    (4, "CTA folded"), (11, "last: ticket"), (12, "last: parts+tail"), (13, "last: final fold"), (14, "last: fold again"),
+                    (5, "epilogue end")]:
         mn, md, mx = q(c)
         print(f"  {what:18s} min {mn:8.2f}  median {md:8.2f}  max {mx:8.2f} us")
+    ctr = np.zeros(16, np.uint64)
+    if hasattr(L, "sfa_diag_counters") and L.sfa_diag_counters(h, ctr.ctypes.data, 16) == 0:
+        print("  counters: combine_fact %d  combine_ids %d  combine_slow %d  replay %d" % tuple(int(x) for x in ctr[:4]))
     scan = rel[:, 3] - rel[:, 2]
     print(f"  scan duration      min {np.nanmin(scan):.2f} median {np.nanmedian(scan):.2f} max {np.nanmax(scan):.2f}")
     order = np.argsort(scan)
