@@ -33,7 +33,7 @@ def _inputs():
 DIAG_LIB = os.path.join(LIBDIR, "libsfa_diag.so")
 
 
-def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, diag: bool = False, counters: bool = False) -> str:
     """diag: the diagnostic library (-DSFA_STAMPS: per-CTA phase stamps of the
     TMA scan, sfa_diag_stamps) -- never loaded by the product, tests or bench."""
     os.makedirs(LIBDIR, exist_ok=True)
@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str
     for src_name in SOURCES:
         src = os.path.join(CSRC, src_name)
         obj = os.path.join(LIBDIR, src_name + f".{os.getpid()}{'.diag' if diag else ''}.o")
-        cmd = [NVCC, *ARCH, *FLAGS, *(["-DSFA_STAMPS"] if diag else []), "-c", src, "-o", obj]
+        extra = (["-DSFA_STAMPS"] if diag else []) + (["-DSFA_COUNTERS"] if diag and counters else [])
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         if src_name.endswith(".cu") and verbose:
             cmd[1:1] = ["-Xptxas", "-v"]
         if verbose:
@@ -71,4 +72,5 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, diag="--diag" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, diag="--diag" in sys.argv,
+                counters="--counters" in sys.argv))

@@ -180,7 +180,9 @@ struct Comp<Step, false> {
         return replay(S, t, a, b, lane_id());
     }
     // the 32 lanes' ids, in lane order, folded by a shuffle tree; result in every lane
-    __device__ static uint32_t fold_states(const Step& S, const DevTables& t, uint32_t s) {
+    // __noinline__: one copy of the fold code, so the last CTA's final fold runs
+    // instructions its own CTA fold has just brought into the I-cache
+    __device__ __noinline__ static uint32_t fold_states(const Step& S, const DevTables& t, uint32_t s) {
         const uint32_t lane = lane_id();
         if (t.aux_comp && !fact_values(t)) {  // ids through the smem composition table: a tight LDS tree
             const uint32_t base = smem_u32(dsmem) + t.aux_off, nS = t.nS;
@@ -191,6 +193,20 @@ struct Comp<Step, false> {
                 const uint32_t i = s * nS + o;
                 const uint32_t v = u8 ? lds_u8(base + i) : lds_u16(base + 2 * i);
                 const uint32_t c = s == 0 ? o : (o == 0 ? s : v);
+                s = (lane & (2 * d - 1)) == 0 ? c : s;
+            }
+            return __shfl_sync(kFull, s, 0);
+        }
+        if (t.aux_fam && __all_sync(kFull, s == 0 || (s & kFact))) {
+            // every value factored (or f_I): branch-free tree over the smem marked sets
+            const uint32_t base = smem_u32(dsmem) + t.aux_off, fw = t.fam_w, a0 = t.fam_a0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_down_sync(kFull, s, d);
+                const uint32_t F = (o >> 16) & 0x3fffu, g = s & 0xffffu;
+                const uint32_t w = lds_u32(base + 4u * (F * fw + (g >> 5)));
+                uint32_t c = (s & 0xffff0000u) | (((w >> (g & 31)) & 1u) ? a0 : (o & 0xffffu));
+                c = s == 0 ? o : (o == 0 ? s : c);
                 s = (lane & (2 * d - 1)) == 0 ? c : s;
             }
             return __shfl_sync(kFull, s, 0);
@@ -226,8 +242,8 @@ struct Comp<Step, false> {
         if (lane_id() == 0) *reinterpret_cast<uint32_t*>(slot) = v;
     }
     __device__ static uint32_t load(const uint8_t* slot) { return *reinterpret_cast<const uint32_t*>(slot); }
-    __device__ static uint32_t fold_slots(const Step& S, const DevTables& t, const uint8_t* base, uint32_t count,
-                                          uint32_t acc, bool global) {
+    __device__ __noinline__ static uint32_t fold_slots(const Step& S, const DevTables& t, const uint8_t* base,
+                                                       uint32_t count, uint32_t acc, bool global) {
         for (uint32_t c0 = 0; c0 < count; c0 += 32) {
             uint32_t u = c0 + lane_id();
             uint32_t x = 0;
