@@ -596,8 +596,8 @@ struct sfa_handle {
                 const uint32_t q = H ? order[r] : r;
                 const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
                 const uint32_t nr = H ? rank[nq] : nq;
-                if (H && nr >= H) return sfa::mix_twin(nr, hotb);
-                return ((nr >> 1) * 128u + 2u * (nr & 1u)) | 0x8000u;
+                if (H && nr >= H) return sfa::cpt_cell(sfa::mix_twin(nr, hotb), false);
+                return sfa::cpt_cell(sfa::mix_hot(nr, 0), true);
             };
             for (uint32_t j = 0; j < W; ++j)
                 for (uint32_t k = 0; k < hl; ++k) cpt[static_cast<size_t>(j) * hl + k] = cell(j, 2 * k) | (cell(j, 2 * k + 1) << 16);

@@ -363,7 +363,7 @@ struct StepHot {
         if (t.dwin_cpt) {  // bank-private rows expanded from the compact source (plan.hpp DevTables::dwin_cpt)
             uint32_t* tbl = reinterpret_cast<uint32_t*>(dsmem);
             const uint32_t L = tid & 31, w = tid >> 5, nw = nthreads >> 5, X4 = t.dwin_X >> 2, hl = t.dwin_hl;
-            const uint32_t units = t.W * hl, l4 = 4u * L;
+            const uint32_t units = t.W * hl;
             // warp w: units [32 b, 32 b + 32) for b = w, w + nw, ...: one load per lane
             // (one L2 round trip per 32 units), each unit broadcast to the 32 lanes
             for (uint32_t u0 = 32 * w; u0 < units; u0 += 32 * nw) {
@@ -372,7 +372,7 @@ struct StepHot {
                 uint32_t j = u0 / hl, k = u0 - j * hl;
                 for (uint32_t i = 0; i < n; ++i) {
                     const uint32_t c = __shfl_sync(0xffffffffu, mine, i);
-                    tbl[j * X4 + k * 32 + L] = (c & 0x7fff7fffu) + ((c >> 15) & 0x00010001u) * l4;
+                    tbl[j * X4 + k * 32 + L] = cpt_expand(c, L);
                     if (++k == hl) {
                         k = 0;
                         ++j;
@@ -470,11 +470,7 @@ struct StepDfaMix {
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
         return ld_tbl_u16(window_col(byte, neg_lo, wmax) * X + st);
     }
-    __device__ __forceinline__ uint32_t fix(uint32_t st) const {
-        const uint32_t d = st - hotb;  // 2r for a twin (wraps for a hot state)
-        const uint32_t h = ((d & ~3u) << 5) + (d & 2u) + lane4;  // mix_hot(d / 2, lane)
-        return d < twoH ? h : st;
-    }
+    __device__ __forceinline__ uint32_t fix(uint32_t st) const { return mix_fix(st, hotb, twoH, lane4); }
 };
 
 // Steps that re-normalise their state between 16-byte pieces (StepDfaMix)

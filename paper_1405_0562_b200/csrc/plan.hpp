@@ -125,6 +125,21 @@ __host__ __device__ __forceinline__ uint32_t mix_X(uint32_t nD, uint32_t H) { re
 __host__ __device__ __forceinline__ uint32_t mix_rank_of(uint32_t e, uint32_t hotb) {
     return e < hotb ? 2u * (e >> 7) + ((e >> 1) & 1u) : (e - hotb) >> 1;
 }
+// StepDfaMix::fix: the twin of a hot state (rank r < H) -> its private cell of
+// lane L (lane4 = 4L); any other encoding unchanged
+__host__ __device__ __forceinline__ uint32_t mix_fix(uint32_t e, uint32_t hotb, uint32_t twoH, uint32_t lane4) {
+    const uint32_t d = e - hotb;  // 2r for a twin (wraps for a hot state)
+    const uint32_t h = ((d & ~3u) << 5) + (d & 2u) + lane4;  // mix_hot(d / 2, lane)
+    return d < twoH ? h : e;
+}
+// The compact source of a bank-private window (DevTables::dwin_cpt): a pair
+// word of lane 0's cells with bit 15 set on private targets -> lane L's word
+__host__ __device__ __forceinline__ uint32_t cpt_expand(uint32_t c, uint32_t lane) {
+    return (c & 0x7fff7fffu) + ((c >> 15) & 0x00010001u) * (4u * lane);
+}
+__host__ __device__ __forceinline__ uint32_t cpt_cell(uint32_t enc_lane0, bool private_target) {
+    return enc_lane0 | (private_target ? 0x8000u : 0u);
+}
 // a DFA state in the factored step's encoding (any layout) and back
 __device__ __forceinline__ uint32_t dw_enc(const DevTables& t, uint32_t q, uint32_t lane) {
     if (t.dwin_u8) return enc8(q, lane);

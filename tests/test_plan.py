@@ -120,3 +120,72 @@ def test_plan_equal_texts(planner):
         assert tail == count * ln
         assert rows <= G * R and hi - lo <= 1 and hi <= NB * bh
     assert out[0][1] == 32768          # cfg5: two rows of 32 KiB per 64 KiB text
+
+
+MIX_SRC = r'''
+#include <cstdio>
+#include <set>
+#include "plan.hpp"
+// The MIXED DFA-window encoding (plan.hpp mix_*), the 16-byte fix and the
+// compact source expansion: prints "ok" or the first violated property.
+int main() {
+    const unsigned Hs[] = {2, 8, 68, 70, 100}, nDs[] = {101, 145, 300, 513};
+    for (unsigned H : Hs)
+        for (unsigned nD : nDs) {
+            if (H >= nD) continue;
+            const unsigned hotb = 64 * H, X = sfa::mix_X(nD, H);
+            if (X % 128) { printf("X %u not a multiple of 128\n", X); return 0; }
+            std::set<unsigned> seen;
+            for (unsigned r = 0; r < H; ++r)
+                for (unsigned L = 0; L < 32; ++L) {
+                    const unsigned e = sfa::mix_hot(r, L);
+                    if (e + 2 > hotb) { printf("hot %u,%u outside the hot region\n", r, L); return 0; }
+                    if ((e >> 2) % 32 != L) { printf("hot %u,%u not in bank %u\n", r, L, L); return 0; }
+                    if (!seen.insert(e).second) { printf("hot %u,%u shares a cell\n", r, L); return 0; }
+                    if (sfa::mix_rank_of(e, hotb) != r) { printf("rank of hot %u,%u\n", r, L); return 0; }
+                    if (sfa::mix_fix(e, hotb, 2 * H, 4 * L) != e) { printf("fix moved hot %u,%u\n", r, L); return 0; }
+                    for (unsigned j = 1; j < 4; ++j)  // other columns keep the bank
+                        if (((j * X + e) >> 2) % 32 != L) { printf("column %u moves bank\n", j); return 0; }
+                }
+            for (unsigned r = 0; r < nD; ++r) {
+                const unsigned t = sfa::mix_twin(r, hotb);
+                if (t < hotb || t + 2 > X) { printf("twin %u outside the twin region\n", r); return 0; }
+                if (!seen.insert(t).second) { printf("twin %u shares a cell\n", r); return 0; }
+                if (sfa::mix_rank_of(t, hotb) != r) { printf("rank of twin %u\n", r); return 0; }
+                for (unsigned L = 0; L < 32; L += 7) {
+                    const unsigned f = sfa::mix_fix(t, hotb, 2 * H, 4 * L);
+                    if (f != (r < H ? sfa::mix_hot(r, L) : t)) { printf("fix of twin %u lane %u\n", r, L); return 0; }
+                }
+            }
+            if (X > 32768) continue;  // the compact source needs values < 2^15
+            for (unsigned a = 0; a < nD; a += 3)
+                for (unsigned b = 0; b < nD; b += 5) {
+                    auto cell = [&](unsigned q) {
+                        return q < H ? sfa::cpt_cell(sfa::mix_hot(q, 0), true) : sfa::cpt_cell(sfa::mix_twin(q, hotb), false);
+                    };
+                    auto enc = [&](unsigned q, unsigned L) { return q < H ? sfa::mix_hot(q, L) : sfa::mix_twin(q, hotb); };
+                    for (unsigned L = 0; L < 32; ++L)
+                        if (sfa::cpt_expand(cell(a) | (cell(b) << 16), L) != (enc(a, L) | (enc(b, L) << 16))) {
+                            printf("compact expansion %u %u lane %u\n", a, b, L);
+                            return 0;
+                        }
+                }
+        }
+    printf("ok\n");
+}
+'''
+
+
+def test_mixed_window_encoding(tmp_path):
+    """MIXED DFA window (plan.hpp): lane L's private cells of the hot states
+    all sit in bank L in every column, no two cells of the layout coincide,
+    ranks decode from both encodings, the 16-byte fix sends exactly the twins
+    of hot states back to the lane's own cell, and the compact source
+    (bit 15 = private target) expands to every lane's pair word."""
+    src = tmp_path / "mix.cpp"
+    src.write_text(MIX_SRC)
+    exe = tmp_path / "mix"
+    csrc = os.path.join(ROOT, "paper_1405_0562_b200", "csrc")
+    subprocess.check_call(["g++", "-O1", "-std=c++17", "-I", csrc, "-I", os.path.join(ROOT, "include"),
+                           "-I", "/usr/local/cuda/include", str(src), "-o", str(exe)])
+    assert subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.strip() == "ok"
