@@ -362,6 +362,9 @@ typedef struct {
                                  lane-group copies, 2 = MIXED (the most visited DFA states in 32
                                  bank-private copies, every state in one shared copy)          */
     uint32_t dfa_hot;         /* MIXED: cap on the bank-private DFA states (0 = all that fit)   */
+    uint32_t fact_fold;       /* FACTORED chunk values in the folds: 0 auto (marked sets in smem
+                                 when small), 1 = marked sets read from global memory, 2 = off
+                                 (canonical SFA ids, as before round 2b)                         */
 } sfa_tuning_t;
 SFA_API int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* t);
 

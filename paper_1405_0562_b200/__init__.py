@@ -62,7 +62,8 @@ class sfa_tuning_t(C.Structure):
     _fields_ = [("tma_k", C.c_int32), ("tma_rowb", C.c_int32), ("tma_ring", C.c_int32), ("tma_promo", C.c_int32),
                 ("hot_rows", C.c_uint32), ("no_factor", C.c_uint32), ("dfa_copies", C.c_uint32),
                 ("private_copies", C.c_uint32), ("row_align", C.c_uint32), ("direct_piece", C.c_uint32),
-                ("dfa_u8", C.c_uint32), ("dfa_layout", C.c_uint32), ("dfa_hot", C.c_uint32)]
+                ("dfa_u8", C.c_uint32), ("dfa_layout", C.c_uint32), ("dfa_hot", C.c_uint32),
+                ("fact_fold", C.c_uint32)]
 
 
 class sfa_rows_plan(C.Structure):

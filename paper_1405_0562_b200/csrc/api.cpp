@@ -279,9 +279,11 @@ struct sfa_handle {
             t.dwin_rank = ddrank;
             t.dwin_unrank = ddunrank;
             t.dwin_cpt = ddcpt;
-            t.fam_bits = dfam_bits;
-            t.fam_img = dfam_img;
-            if (!t.aux && dfam_bits && fam_aux_bytes()) {  // the marked sets in smem for the folds
+            if (tuning.fact_fold != 2) {  // tuning fact_fold = 2: the folds use canonical SFA ids
+                t.fam_bits = dfam_bits;
+                t.fam_img = dfam_img;
+            }
+            if (!t.aux && t.fam_bits && fam_aux_bytes() && tuning.fact_fold == 0) {  // the marked sets in smem for the folds
                 t.aux = dfam_bits;
                 t.aux_bytes = fam_aux_bytes();
                 t.aux_fam = 1;
@@ -1204,7 +1206,7 @@ int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* tu) {
         (t.row_align && t.row_align != 64 && t.row_align != 128 && t.row_align != 256) ||
         (t.dfa_copies & (t.dfa_copies - 1)) || t.dfa_copies > 32 ||
         (t.private_copies & (t.private_copies - 1)) || t.private_copies > 32 ||
-        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)) || t.dfa_u8 > 1 || t.dfa_layout > 2)
+        (t.direct_piece && (t.direct_piece < 16 || t.direct_piece > 4096)) || t.dfa_u8 > 1 || t.dfa_layout > 2 || t.fact_fold > 2)
         return fail(SFA_ERR_INVALID_ARG, "bad tuning value");
     if (!tu) t.tma_promo = -1;
     std::lock_guard<std::mutex> lk(h->mu);

@@ -43,6 +43,9 @@ if os.environ.get("SWEEP") == "k2":      # two rows per thread (ILP 2) with 32-b
     shapes = [dict(), dict(tma_k=2, tma_rowb=32, hot_rows=16), dict(tma_k=2, tma_rowb=32, hot_rows=16, dfa_hot=40),
               dict(tma_k=2, tma_rowb=32, hot_rows=16, dfa_hot=24), dict(tma_k=1, tma_rowb=64, hot_rows=16),
               dict(tma_k=1, tma_rowb=64, hot_rows=16, dfa_hot=40)]
+if os.environ.get("SWEEP") == "k2promo":  # two chains per thread on 16-byte stages, L2 promotion for whole lines
+    shapes = [dict(), dict(tma_k=2, tma_rowb=16, tma_promo=128), dict(tma_k=2, tma_rowb=16, tma_promo=256),
+              dict(tma_k=2, tma_rowb=16, tma_promo=128, hot_rows=16), dict(tma_k=2, tma_rowb=16, tma_promo=256, hot_rows=16)]
 s = torch.cuda.Stream()
 for cfg in cfgs:
     rx, alpha, text = bench.workload(cfg)

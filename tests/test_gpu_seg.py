@@ -387,3 +387,68 @@ def test_guard_bytes_and_determinism(torch_cuda):
                 if first is None:
                     first = rows
                 assert (rows == first).all()          # same plan, same ids, every time
+
+
+# --------------------------------------------------------------------------- factored folds (round 2b)
+@pytest.mark.parametrize("fold", [0, 1, 2])
+def test_factored_fold_modes(torch_cuda, fold):
+    """FACTORED chunk values through the folds: (F, g) pairs composed from the
+    families' marked sets in smem (0), the same sets read from global memory
+    (1), or canonical SFA ids as before (2) -- same results on cfg3 texts with
+    words planted everywhere (single texts and a ragged batch) and cfg4."""
+    torch = torch_cuda
+    rx = W.cfg3_regex()
+    t = W.cfg3_text(48 << 20, plant=False)
+    words = W.cfg3_words()
+    rng = np.random.default_rng(31 + fold)
+    sfa = P.SFA(rx, None)
+    sfa.set_tuning(fact_fold=fold)
+    d = odfa(rx, None)
+    for trial in range(4):
+        u = t.copy()
+        for _ in range(trial * 3):
+            w = np.frombuffer(words[int(rng.integers(0, 32))], np.uint8)
+            o = int(rng.integers(0, u.size - w.size))
+            u[o:o + w.size] = w
+        n = int(rng.integers(5 << 20, u.size))
+        buf, v = dev(torch, u[:n], trial)
+        assert sfa.match(v) == d.run(u[:n]), (fold, trial)
+    assert P.sfa_info(sfa.h)["dfa_window_hot"] > 0                  # MIXED window, factored rows
+    texts, off = W.ragged_batch(23, 3000, 50_000, AZ)
+    check_batch(torch, sfa, d, texts, off)
+    sfa4 = P.SFA(*CFG4)
+    sfa4.set_tuning(fact_fold=fold)
+    t4 = W.cfg4_text(24 << 20)
+    buf, v = dev(torch, t4, 0)
+    assert sfa4.match(v) == odfa(*CFG4).run(t4)
+
+
+def test_factored_two_absorbing_states(torch_cuda):
+    """x.*|[ab]* over all bytes: two absorbing states (the accepting sink after
+    a leading x, the dead state after any other byte), so a family's marked
+    states go to different absorbing images (DevTables::fam_img).  HOT +
+    FACTORED forced; texts accepted by either branch, rejected by one byte
+    planted anywhere, single and batched."""
+    torch = torch_cuda
+    rx = "x.*|[ab]*"
+    d = odfa(rx, None)
+    sfa = P.SFA(rx, None)
+    sfa.set_residency(P.RES_HOT_L2)
+    rng = np.random.default_rng(77)
+    base = rng.integers(0, 2, size=12 << 20).astype(np.uint8) + ord("a")
+    cases = []
+    cases.append(base.copy())                                    # [ab]*: accepted
+    u = base.copy(); u[int(rng.integers(0, u.size))] = ord("c"); cases.append(u)   # one c: dead
+    u = base.copy(); u[0] = ord("x"); cases.append(u)            # x...: the accepting sink
+    u = base.copy(); u[0] = ord("x"); u[-5] = 0; cases.append(u)  # x... then anything: still accepted
+    u = base.copy(); u[7 << 20] = ord("x"); cases.append(u)      # an x later: dead
+    for i, u in enumerate(cases):
+        for n in (u.size, u.size - 12_345):
+            buf, v = dev(torch, u[:n], i % 16)
+            assert sfa.match(v) == d.run(u[:n]), (i, n)
+    info = P.sfa_info(sfa.h)
+    assert info["residency"] == P.RES_HOT_L2 and info["dfa_window_copies"] > 0   # the FACTORED step ran
+    texts = np.concatenate([c[: 40_000 + 997 * i] for i, c in enumerate(cases * 6)])
+    lens = [40_000 + 997 * i for i in range(len(cases) * 6)]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    check_batch(torch, sfa, d, texts, off)
