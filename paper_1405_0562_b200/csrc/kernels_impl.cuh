@@ -1024,13 +1024,8 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
         // walk), checked after stages 1, 2, 4, 8, ...; the rest with the
         // factored DFA step.  A batch row's piece that starts a text needs
         // only f(q0): it continues as the DFA run from q0 (kTagFam).
-        uint32_t i = 0, next_check = 1;
-        while (i < nstages) {
-            if constexpr (SEG) scan_stages_seg<K, ROWB, Sh>(S, st, rsrc, rrow, ring, i, i + 1, lane, rs.nb, close_sfa);
-            else scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, i, i + 1, lane);
-            ++i;
-            if (!t.fact_fam || i != next_check || i == nstages) continue;
-            next_check *= 2;
+        // every lane factorable?  (a batch row's text-start piece: its f(q0) as a tagged DFA state)
+        auto check = [&]() -> bool {
             bool ok = true;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
@@ -1042,39 +1037,92 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                     ok &= fact_from_id(t, sid, fam[k], g[k]);
                 }
             }
-            if (__all_sync(kFull, ok)) {
-                // the rest of the rows through the DFA window table (u8 or u16 layout)
-                auto run_dfa = [&](const auto& D) {
-                    if constexpr (SEG) {
-                        const uint32_t g0 = dw_enc(t, 0u, lane);
-                        auto close_fact = [&](int k) {
-                            const uint32_t v = fam[k] == kTagFam ? (kTag | dw_dec(t, g[k], lane))
-                                               : fact_values(t) ? fact_pack(fam[k], dw_dec(t, g[k], lane))
-                                                                : fact_to_id(t, fam[k], g[k]);
-                            seg_close(k, v);
-                            fam[k] = kTagFam;
-                            g[k] = g0;
-                        };
-                        scan_stages_seg<K, ROWB, Sh>(D, g, rsrc, rrow, ring, i, nstages, lane, rs.nb, close_fact);
-                    } else {
-                        scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i, nstages, lane);
-                    }
+            return __all_sync(kFull, ok);
+        };
+        // stages [i0, nstages) through the DFA window table (u8 or u16 layout)
+        auto run_dfa = [&](const auto& D, uint32_t i0) {
+            if constexpr (SEG) {
+                const uint32_t g0 = dw_enc(t, 0u, lane);
+                auto close_fact = [&](int k) {
+                    const uint32_t v = fam[k] == kTagFam ? (kTag | dw_dec(t, g[k], lane))
+                                       : fact_values(t) ? fact_pack(fam[k], dw_dec(t, g[k], lane))
+                                                        : fact_to_id(t, fam[k], g[k]);
+                    seg_close(k, v);
+                    fam[k] = kTagFam;
+                    g[k] = g0;
                 };
-                if (t.dwin_u8) {
-                    StepDfa8 D;
-                    D.params(t);
-                    run_dfa(D);
-                } else if (t.dwin_H) {
-                    StepDfaMix D;
-                    D.params(t);
-                    run_dfa(D);
-                } else {
-                    StepDfa D;
-                    D.params(t);
-                    run_dfa(D);
-                }
+                scan_stages_seg<K, ROWB, Sh>(D, g, rsrc, rrow, ring, i0, nstages, lane, rs.nb, close_fact);
+            } else {
+                scan_stages<K, ROWB, Sh>(D, g, rsrc, ring, i0, nstages, lane);
+            }
+        };
+        auto with_dfa_step = [&](auto&& fn) {
+            if (t.dwin_u8) {
+                StepDfa8 D;
+                D.params(t);
+                fn(D);
+            } else if (t.dwin_H) {
+                StepDfaMix D;
+                D.params(t);
+                fn(D);
+            } else {
+                StepDfa D;
+                D.params(t);
+                fn(D);
+            }
+        };
+        uint32_t i = 0, next_check = 1;
+        // The first stage: its first 8 bytes through the SFA table, then the
+        // check -- chunks of most automata synchronise within a few bytes
+        // (cfg3: <= 4 bytes for all but 5e-5 of them) and the SFA table's
+        // rows for those first bytes are mostly cold (L2) -- and the rest of
+        // the stage through whichever step applies.  Skipped when a text
+        // boundary of the warp falls in the first stage (batch).
+        bool boundary0 = false;
+        if constexpr (SEG) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) boundary0 |= rs.nb[k] <= static_cast<uint32_t>(ROWB);
+            boundary0 = __any_sync(kFull, boundary0);
+        }
+        if (t.fact_fam && nstages > 1 && !boundary0) {
+            uint4 v[K][ROWB / 16];
+            load_stage<K, ROWB, Sh>(v, rsrc, ring);
+#pragma unroll
+            for (int k = 0; k < K; ++k) st[k] = step4(S, step4(S, st[k], v[k][0].x), v[k][0].y);
+            // bytes 8 .. ROWB of the stage from the registers
+            auto rest = [&](const auto& X, uint32_t(&s)[K]) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) s[k] = maybe_fix(X, step4(X, step4(X, s[k], v[k][0].z), v[k][0].w));
+#pragma unroll
+                for (int c = 1; c < ROWB / 16; ++c)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) s[k] = step16(X, s[k], v[k][c]);
+            };
+            if (check()) {
+                with_dfa_step([&](const auto& D) {
+                    rest(D, g);
+                    ring.release(lane);
+                    SFA_STAMP(15);  // thread 0: first stage done
+                    run_dfa(D, 1);
+                });
                 factored = true;
-                break;
+            } else {
+                rest(S, st);
+                ring.release(lane);
+                SFA_STAMP(15);
+                i = 1;
+                next_check = 2;
+            }
+        }
+        while (!factored && i < nstages) {
+            if constexpr (SEG) scan_stages_seg<K, ROWB, Sh>(S, st, rsrc, rrow, ring, i, i + 1, lane, rs.nb, close_sfa);
+            else scan_stages<K, ROWB, Sh>(S, st, rsrc, ring, i, i + 1, lane);
+            ++i;
+            if (!t.fact_fam || i != next_check || i == nstages) continue;
+            next_check *= 2;
+            if (check()) {  // the rest of the rows through the DFA window table
+                with_dfa_step([&](const auto& D) { run_dfa(D, i); });
+                factored = true;
             }
         }
     } else {

@@ -34,7 +34,7 @@ def report(name, h, G):
     rel[st == 0] = np.nan
     q = lambda c: (np.nanmin(rel[:, c]), np.nanmedian(rel[:, c]), np.nanmax(rel[:, c]))  # noqa: E731
     print(f"{name}: ctas={st.shape[0]}")
-    for c, what in [(0, "entry"), (7, "first TMA issued"), (1, "tables built"), (2, "after pdl wait"),
+    for c, what in [(0, "entry"), (7, "first TMA issued"), (1, "tables built"), (2, "after pdl wait"), (15, "first stage done"),
                     (3, "rows scanned"), (8, "aux+tail done"), (9, "values"), (10, "warps folded"),
                     (4, "CTA folded"), (11, "last: ticket"), (12, "last: parts+tail"), (13, "last: final fold"), (14, "last: fold again"),
                     (5, "epilogue end")]:
