@@ -211,6 +211,7 @@ struct Comp<Step, false> {
             }
             return __shfl_sync(kFull, s, 0);
         }
+        if (t.aux_fam) SFA_CTR(t, 4);  // diag: a fold with an SFA id among factored values
         if (fact_values(t)) {  // factored values: the inline (F, g) rule, the rest by combine
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {

@@ -42,7 +42,8 @@ def report(name, h, G):
         print(f"  {what:18s} min {mn:8.2f}  median {md:8.2f}  max {mx:8.2f} us")
     ctr = np.zeros(16, np.uint64)
     if hasattr(L, "sfa_diag_counters") and L.sfa_diag_counters(h, ctr.ctypes.data, 16) == 0:
-        print("  counters: combine_fact %d  combine_ids %d  combine_slow %d  replay %d" % tuple(int(x) for x in ctr[:4]))
+        print("  counters: combine_fact %d  combine_ids %d  combine_slow %d  replay %d  mixed folds %d"
+              % tuple(int(x) for x in ctr[:5]))
     scan = rel[:, 3] - rel[:, 2]
     print(f"  scan duration      min {np.nanmin(scan):.2f} median {np.nanmedian(scan):.2f} max {np.nanmax(scan):.2f}")
     order = np.argsort(scan)
