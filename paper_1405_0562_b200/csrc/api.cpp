@@ -127,6 +127,19 @@ struct sfa_handle {
     uint32_t fam_w = 0, fam_a0 = 0;
     uint32_t dwin_hl = 0, dwin_tw = 0;
     sfa_tuning_t tuning{};                    // shape knobs (sfa_set_tuning); zero = automatic
+    // The last single-text TMA launch's decisions (residency, tables, shape,
+    // plan) for the same text and size: a repeated call skips them (host cost
+    // per call).  Any setter that can change them bumps cfg_epoch.
+    uint64_t cfg_epoch = 1;
+    struct LaunchCache {
+        uint64_t epoch = 0;
+        const uint8_t* text = nullptr;
+        uint64_t n = 0;
+        sfa::Res mode{};
+        sfa::DevTables t{};
+        sfa::TmaConfig cfg{};
+        sfa::TmaPlan plan{};
+    } lcache;
     bool factor_on() const { return tuning.no_factor == 0; }
     sfa::Tuning ktune() const {
         sfa::Tuning k;
@@ -175,6 +188,7 @@ struct sfa_handle {
     // Frees every device table and scratch buffer (after the device work that
     // used them); the next device call uploads again.
     void release_device() {
+        ++cfg_epoch;
         if (!uploaded) return;
         int prev = 0;
         cudaGetDevice(&prev);
@@ -365,6 +379,7 @@ struct sfa_handle {
     // (Re)builds the HOT tables from a ranking and writes them to the device
     // buffers (allocated on first use).  Synchronous.
     int upload_hot(const uint8_t* sample, size_t ns) {
+        ++cfg_epoch;
         const uint32_t nS = A.nS;
         std::vector<uint32_t> perm;
         hot_ranking(perm, sample, ns);
@@ -851,7 +866,11 @@ struct sfa_handle {
                    sfa::TmaPlan* plan_out = nullptr) {
         const bool direct = !force_tma && (force_pieces > 0 || n < kTmaMin);
         sfa::Res mode;
-        int rc = resolve(direct ? 1 : 0, &mode);
+        int rc = SFA_OK;
+        if (!direct && lcache.epoch == cfg_epoch && lcache.text == d_text && lcache.n == n && !row_ids)
+            mode = lcache.mode;  // the same text again: the cached decisions below
+        else
+            rc = resolve(direct ? 1 : 0, &mode);
         if (rc) return rc;
         cudaError_t e;
         if (direct) {
@@ -878,7 +897,8 @@ struct sfa_handle {
             e = sfa::launch_scan_direct(mode, vec(), a, stream);
         } else {
             sfa::ScanArgs a{};
-            a.t = tables(mode, 0);
+            const bool cached = lcache.epoch == cfg_epoch && lcache.text == d_text && lcache.n == n && !row_ids;
+            a.t = cached ? lcache.t : tables(mode, 0);
             a.text = d_text;
             a.n = n;
             a.sc = scratch();
@@ -892,8 +912,20 @@ struct sfa_handle {
             CU(cudaMemsetAsync(dstamps, 0, (kMaxSlots + 1) * 16 * sizeof(uint64_t), stream));
 #endif
             sfa::TmaConfig cfg;
-            rc = tma_plan(mode, a.t, d_text, n, &cfg, &a.plan);
-            if (rc) return rc;
+            if (cached) {
+                cfg = lcache.cfg;
+                a.plan = lcache.plan;
+            } else {
+                rc = tma_plan(mode, a.t, d_text, n, &cfg, &a.plan);
+                if (rc) return rc;
+                lcache.epoch = cfg_epoch;
+                lcache.text = d_text;
+                lcache.n = n;
+                lcache.mode = mode;
+                lcache.t = a.t;
+                lcache.cfg = cfg;
+                lcache.plan = a.plan;
+            }
             if (row_ids && a.plan.nchunks > row_cap) return fail(SFA_ERR_CAPACITY, "row_cap is smaller than the row count");
             if (plan_out) *plan_out = a.plan;
             e = sfa::launch_scan_tma(mode, vec(), a, cfg, stream);
@@ -1161,15 +1193,20 @@ int sfa_set_residency(sfa_handle* h, int mode) {
     std::lock_guard<std::mutex> lk(h->mu);
     if (mode == SFA_RES_AUTO) {
         h->forced = mode;
+        ++h->cfg_epoch;
         return SFA_OK;
     }
     int rc = h->ensure_uploaded();
     if (rc) return rc;
     const int prev = h->forced;
     h->forced = mode;
+    ++h->cfg_epoch;
     sfa::Res m;
     rc = h->resolve(1, &m);
-    if (rc) h->forced = prev;
+    if (rc) {
+        h->forced = prev;
+        ++h->cfg_epoch;
+    }
     return rc;
 }
 
@@ -1193,6 +1230,7 @@ int sfa_set_compose(sfa_handle* h, int mode) {
     if (mode == SFA_COMPOSE_TABLE && !h->has_comp()) return fail(SFA_ERR_CAPACITY, "composition table needs |S| <= 4096");
     std::lock_guard<std::mutex> lk(h->mu);
     h->compose = mode;
+    ++h->cfg_epoch;
     return SFA_OK;
 }
 
@@ -1213,6 +1251,7 @@ int sfa_set_tuning(sfa_handle* h, const sfa_tuning_t* tu) {
     // the table layouts depend on the copy caps and the factoring switch: rebuild lazily
     h->release_device();
     h->tuning = t;
+    ++h->cfg_epoch;
     return SFA_OK;
 }
 
