@@ -833,27 +833,16 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 mbar_expect_tx(cbar, stage_bytes);
                 bulk_g2s(smem_u32(staging), Step::staged_src(a.t), stage_bytes, cbar);
             }
-            // the composition aux image (needed at the folds; the marked sets
-            // after the table build) and the fold tables' L2 prefetch: issued
-            // once the first text stage is on its way (or before any return)
-            bool aux_issued = false;
-            auto issue_aux = [&]() {
-                if (aux_issued) return;
-                aux_issued = true;
-                if (a.t.aux_bytes) {
-                    const uint32_t tb = static_cast<uint32_t>((Step::smem_bytes(a.t) + 15) & ~size_t(15));
-                    mbar_expect_tx(abar, a.t.aux_bytes);
-                    bulk_g2s(smem_u32(dsmem + tb), a.t.aux, a.t.aux_bytes, abar);
-                }
-                if (gridDim.x > 1) prefetch_fold_tables(a.t, blockIdx.x, gridDim.x);
-            };
+            if (gridDim.x > 1) prefetch_fold_tables(a.t, blockIdx.x, gridDim.x);
+            if (a.t.aux_bytes) {  // composition aux image: needed only at the fold
+                const uint32_t tb = static_cast<uint32_t>((Step::smem_bytes(a.t) + 15) & ~size_t(15));
+                mbar_expect_tx(abar, a.t.aux_bytes);
+                bulk_g2s(smem_u32(dsmem + tb), a.t.aux, a.t.aux_bytes, abar);
+            }
             // The text (and a batch's plan) may come from the previous kernel of
             // the stream: nothing of it is read before that kernel completed.
             pdl_wait();
-            if (SEG && a.err && *a.err == a.epoch) {  // bad offsets: the compute warps report
-                issue_aux();
-                return;
-            }
+            if (SEG && a.err && *a.err == a.epoch) return;  // bad offsets: the compute warps report
             const TmaPlan P = a.dplan ? *a.dplan : a.plan;
             if (blockIdx.x == gridDim.x - 1) {  // the tail this CTA runs after its rows, and the head: into L2 now
                 const uint8_t* base = a.text + (a.off ? __ldg(a.off) : 0ull);
@@ -865,10 +854,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                 if (P.head && h1 > h0) bulk_prefetch_l2(reinterpret_cast<const void*>(h0), static_cast<uint32_t>(h1 - h0));
             }
             const uint32_t rc = P.cta_rows(blockIdx.x);
-            if (rc == 0) {
-                issue_aux();
-                return;
-            }
+            if (rc == 0) return;
             const CUtensorMap* gm = static_cast<const CUtensorMap*>(a.gmaps);
             const CUtensorMap* mload = gm ? gm : &maps.load;
             const CUtensorMap* mpart = gm ? gm + (rc == P.rc_hi ? 1 : 2) : (rc == P.rc_hi ? &maps.part_hi : &maps.part_lo);
@@ -900,9 +886,7 @@ k_scan_tma(const __grid_constant__ TmaMaps maps, const __grid_constant__ ScanArg
                     slot = 0;
                     phase ^= 1;
                 }
-                if (i == 0) issue_aux();
             }
-            issue_aux();  // nstages == 0
         }
         return;
     }
