@@ -137,6 +137,50 @@ def test_cfg2_scaled_sizes_every_alignment(torch_cuda):
             check_text(torch, sfa, d, t, pad)
 
 
+def test_cfg2_text_beyond_4_gib(torch_cuda):
+    """Maximum sizes: one text (and a batch) past 2^32 bytes, so every offset,
+    row start and row length of the plan needs 64 bits.  cfg2's DFA does not
+    synchronise (the state is the position mod 10), so a row that starts at a
+    truncated offset, or a byte past 4 GiB that is never read, changes the
+    result.  Expected values: the oracle's Alg. 2 over the whole host text."""
+    torch = torch_cuda
+    sfa = P.SFA(*CFG2)
+    d = oracle_pair(*CFG2)
+    a = W.cfg2_accepted()                       # 268,435,450 bytes, a multiple of the 10-byte block
+    reps = 17                                   # 4,563,402,650 bytes > 2^32
+    n = reps * a.size + 7                       # ragged: ends 7 bytes into a block
+    host = np.empty(n, np.uint8)
+    for k in range(reps):
+        host[k * a.size:(k + 1) * a.size] = a
+    host[reps * a.size:] = a[:7]
+    assert n > (1 << 32)
+    buf, v = dev(torch, host, 3)
+    exp = d.run(host)
+    assert exp[0] != 2 and not exp[1]           # 7 bytes into a block: a live, non-final state
+    assert sfa.match(v) == exp
+    assert sfa.match(v[:reps * a.size]) == (0, True)      # whole blocks: accepted (closed form, C12)
+    # one wrong-half digit past 2^32: dead state 2 (closed form) -- the bytes past 4 GiB are read
+    pos = (1 << 32) + 123_456_789
+    old = int(host[pos])
+    host[pos] = 48 + (old - 48 + 5) % 10
+    v[pos:pos + 1].copy_(torch.from_numpy(host[pos:pos + 1]))
+    exp_r = d.run(host)
+    assert exp_r == (2, False)
+    assert sfa.match(v) == exp_r
+    host[pos] = old
+    v[pos:pos + 1].copy_(torch.from_numpy(host[pos:pos + 1]))
+    # a batch over the same buffer whose offsets pass 2^32 (an empty text among them)
+    off = np.array([0, 10, (1 << 32) + 5, (1 << 32) + 5, n - 7, n], np.uint64)
+    count = off.size - 1
+    do = torch.from_numpy(off.astype(np.int64)).cuda()
+    res = torch.zeros(2 * count, dtype=torch.int32, device="cuda")
+    sfa.match_batch(v, do, count, res)
+    torch.cuda.synchronize()
+    r = res.cpu().numpy().view(np.uint32).reshape(count, 2)
+    qo, acco = d.run_batch(host, off)
+    assert (r[:, 0] == qo).all() and (r[:, 1] == acco).all(), (r, qo, acco)
+
+
 # --------------------------------------------------------------------------- config 3
 def test_cfg3_full_size_contains_match(torch_cuda):
     torch = torch_cuda
