@@ -61,6 +61,8 @@ def main():
     for cfg in cfgs:
         rx, alpha, text = bench.workload(cfg)
         sfa = P.SFA(rx, alpha)
+        if os.environ.get("STAMPS_TUNING"):  # e.g. STAMPS_TUNING=fact_fold=1
+            sfa.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in os.environ["STAMPS_TUNING"].split(","))})
         if cfg == 5:
             texts, off, _ = text
             dt = torch.from_numpy(texts).cuda()
