@@ -357,7 +357,8 @@ typedef struct {
     uint32_t row_align;       /* TMA row length alignment: 0 auto, 64, 128 or 256              */
     uint32_t direct_piece;    /* bytes per thread of the short-text kernel: 0 auto, 16..4096   */
     uint32_t dfa_u8;          /* FACTORED: 1 = 32 bank-private u8 copies of the DFA window when
-                                 32 u16 copies do not fit (|D| <= 256, state-major); 0 = u16 */
+                                 32 u16 copies do not fit (|D| <= 256, state-major); 0 = auto:
+                                 u16 layouts, the u8 copies only where MIXED is not chosen      */
     uint32_t dfa_layout;      /* FACTORED u16 layout when 32 copies do not fit: 0 auto, 1 = R
                                  lane-group copies, 2 = MIXED (the most visited DFA states in 32
                                  bank-private copies, every state in one shared copy)          */

@@ -359,18 +359,44 @@ struct sfa_handle {
         const uint32_t nD = A.nD;
         cnt.assign(nD, 0);
         const uint32_t ob = lo + W - 1 < 256 ? lo + W - 1 : lo - 1;  // a byte of column W-1
+        // The walk stays out of absorbing DFA states while some column avoids
+        // them: a uniform walk over r_n's digits is dead after a few steps and
+        // would call every other state cold, while an accepted text visits them
+        // all.  The absorbing states themselves rank first (a text that reaches
+        // one keeps its rows there -- cfg5's texts after their planted word --
+        // and a lane left in the shared copy conflicts on every byte).
+        std::vector<uint8_t> sink(nD, 1);
+        for (uint32_t q = 0; q < nD; ++q)
+            for (uint32_t b = 0; b < 256 && sink[q]; ++b)
+                if (A.dfa[static_cast<size_t>(q) * 256 + b] != q) sink[q] = 0;
         uint64_t x = 0x2545f4914f6cdd1dull;
+        auto next = [&](uint32_t q, uint32_t j) { return A.dfa[static_cast<size_t>(q) * 256 + (j + 1 < W ? lo + j : ob)]; };
+        auto rnd = [&]() {
+            x ^= x << 13;
+            x ^= x >> 7;
+            x ^= x << 17;
+            return static_cast<uint32_t>((x >> 11) % W);
+        };
         for (int walk = 0; walk < 1024; ++walk) {
             uint32_t q = 0;
             for (int k = 0; k < 2048; ++k) {
-                x ^= x << 13;
-                x ^= x >> 7;
-                x ^= x << 17;
-                const uint32_t j = static_cast<uint32_t>((x >> 11) % W);
-                q = A.dfa[static_cast<size_t>(q) * 256 + (j + 1 < W ? lo + j : ob)];
+                uint32_t nx = next(q, rnd());
+                for (int tries = 0; tries < 4 && sink[nx] && nx != q; ++tries) nx = next(q, rnd());
+                if (sink[nx] && nx != q)
+                    for (uint32_t j = 0; j < W; ++j)
+                        if (!sink[next(q, j)]) {
+                            nx = next(q, j);
+                            break;
+                        }
+                q = nx;
                 ++cnt[q];
+                if (sink[q]) break;
             }
         }
+        uint64_t top = 0;
+        for (uint32_t q = 0; q < nD; ++q) top = std::max(top, cnt[q]);
+        for (uint32_t q = 0; q < nD; ++q)
+            if (sink[q]) cnt[q] = top + 1;
         order.resize(nD);
         for (uint32_t i = 0; i < nD; ++i) order[i] = i;
         std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
@@ -507,8 +533,8 @@ struct sfa_handle {
         uint32_t R = 32, X = 0, H = 0;
         const uint32_t Rmax = tuning.dfa_copies ? tuning.dfa_copies : 32u;  // tuning: cap R
         const bool u16_32 = Rmax >= 32 && static_cast<uint64_t>(sfa::dfa_X(nD, 32)) * W <= kDfaMax;
-        const bool u8_32 = tuning.dfa_u8 && !u16_32 && Rmax >= 32 && nD <= 256 &&
-                           static_cast<uint64_t>(nD) * sfa::dfa8_RB(W) <= kDfaMax;
+        const bool u8_fits = !u16_32 && Rmax >= 32 && nD <= 256 && static_cast<uint64_t>(nD) * sfa::dfa8_RB(W) <= kDfaMax;
+        bool u8_32 = tuning.dfa_u8 && u8_fits;
         // MIXED candidate (plan.hpp mix_*): DFA states ranked by visit frequency,
         // the largest even H whose 32 private copies + the shared copy fit
         std::vector<uint32_t> order, rank;
@@ -535,9 +561,7 @@ struct sfa_handle {
                 cold = tot ? 1.0 - static_cast<double>(hot) / static_cast<double>(tot) : 1.0;
             }
         }
-        if (u8_32) {
-            X = sfa::dfa8_RB(W);  // bytes per state row
-        } else {
+        if (!u8_32) {
             for (; R >= 1; R /= 2) {
                 X = sfa::dfa_X(nD, R);
                 if (R <= Rmax && static_cast<uint64_t>(X) * W <= (kDfaMax) && X <= 65535u) break;
@@ -555,7 +579,16 @@ struct sfa_handle {
                     X = sfa::mix_X(nD, H);
                 }
             }
-            if (R == 0) return SFA_OK;
+            // AUTO: neither 32 u16 copies nor a MIXED window with few visits outside
+            // its hot states (r_100, r_127: an accepted text visits every DFA state
+            // equally) -- the conflict-free u8 copies beat R = 16 lane-group copies
+            // (measured: r_100 3.15 vs 3.00 TB/s, r_127 3.30 vs 3.14; MIXED 2.33 / 2.61)
+            if (!H && R < 32 && u8_fits && tuning.dfa_layout == 0 && !tuning.dfa_copies) u8_32 = true;
+            if (R == 0 && !u8_32) return SFA_OK;
+        }
+        if (u8_32) {
+            R = 32;
+            X = sfa::dfa8_RB(W);  // bytes per state row
         }
         dwin_R = R;
         dwin_X = X;
