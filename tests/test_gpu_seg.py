@@ -255,6 +255,46 @@ def test_batch_async_does_not_synchronise(torch_cuda):
     assert r1.cpu().tolist() == [0, int(d.run(np.zeros(0, np.uint8))[1])]
 
 
+def test_cuda_graph_capture_and_replay(torch_cuda):
+    """sfa_match_async and sfa_match_batch inside a CUDA graph (include/sfa.h:
+    no host synchronisation, no allocation after a handle's first call): the
+    graph is captured once and replayed on a changed text and on changed device
+    offsets -- the batch plan is made on the device, so a replay follows them."""
+    torch = torch_cuda
+    sfa = P.SFA(*CFG2)
+    d = odfa(*CFG2)
+    text = W.cfg2_accepted(800_000)                       # 8 MB: the TMA scan
+    host = text.copy()
+    bt, vt = dev(torch, host)
+    offs = [np.array([0, 10, 4_000_000, 4_000_000, host.size], np.uint64),
+            np.array([0, 1_000_000, 1_000_020, 7_999_990, host.size], np.uint64)]
+    off = torch.from_numpy(offs[0].astype(np.int64)).cuda()
+    res = torch.zeros(8, dtype=torch.int32, device="cuda")
+    r1 = torch.zeros(2, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    sfa.match_async(vt, r1, s)                            # first calls: tables, scratch, kernel loading
+    sfa.match_batch(vt, off, 4, res, s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sfa.match_async(vt, r1, s)
+        sfa.match_batch(vt, off, 4, res, s)
+    r1.zero_()
+    res.zero_()
+    for trial in range(3):
+        if trial:                                         # change the text and the offsets in place
+            pos = 123_457 * trial
+            host[pos] = 48 + (int(host[pos]) - 48 + 5) % 10
+            vt.copy_(torch.from_numpy(host))
+            off.copy_(torch.from_numpy(offs[trial % 2].astype(np.int64)))
+        g.replay()
+        torch.cuda.synchronize()
+        assert tuple(r1.cpu().tolist()) == tuple(int(x) for x in d.run(host)), trial
+        got = res.cpu().numpy().view(np.uint32).reshape(4, 2)
+        qo, ao = d.run_batch(host, offs[trial % 2] if trial else offs[0])
+        assert (got[:, 0] == qo).all() and (got[:, 1] == ao).all(), (trial, got, qo, ao)
+
+
 @pytest.mark.parametrize("length,count,pad", [(65536, 300, 0), (1000, 777, 3), (1, 100_000, 0), (7, 50_000, 1),
                                               (4 << 20, 5, 0), (65537, 513, 9)])
 def test_batch_uniform_any_length(torch_cuda, length, count, pad):
