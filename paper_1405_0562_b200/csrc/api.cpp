@@ -611,11 +611,11 @@ struct sfa_handle {
             for (uint32_t j = 0; j < W; ++j)
                 for (uint32_t r = 0; r < nD; ++r) {
                     const uint32_t nr = rank[dw[static_cast<size_t>(order[r]) * W + j]];
-                    put16(static_cast<size_t>(j) * X + sfa::mix_twin(r, hotb), sfa::mix_twin(nr, hotb));
+                    put16(static_cast<size_t>(j) * X + sfa::mix_twin(r, hotb, H), sfa::mix_twin(nr, hotb, H));
                     if (r < H)
                         for (uint32_t L = 0; L < 32; ++L)
                             put16(static_cast<size_t>(j) * X + sfa::mix_hot(r, L),
-                                  nr < H ? sfa::mix_hot(nr, L) : sfa::mix_twin(nr, hotb));
+                                  nr < H ? sfa::mix_hot(nr, L) : sfa::mix_twin(nr, hotb, H));
                 }
             std::vector<uint16_t> rk(nD), ur(nD);
             for (uint32_t q = 0; q < nD; ++q) {
@@ -646,7 +646,7 @@ struct sfa_handle {
                 const uint32_t q = H ? order[r] : r;
                 const uint32_t nq = dw[static_cast<size_t>(q) * W + j];
                 const uint32_t nr = H ? rank[nq] : nq;
-                if (H && nr >= H) return sfa::cpt_cell(sfa::mix_twin(nr, hotb), false);
+                if (H && nr >= H) return sfa::cpt_cell(sfa::mix_twin(nr, hotb, H), false);
                 return sfa::cpt_cell(sfa::mix_hot(nr, 0), true);
             };
             for (uint32_t j = 0; j < W; ++j)

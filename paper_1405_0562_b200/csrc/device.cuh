@@ -458,19 +458,18 @@ struct StepDfa {
 // state is the twin of a hot state moves back to its own copy (arithmetic
 // only; the twin of a cold state stays).
 struct StepDfaMix {
-    uint32_t neg_lo, wmax, X, hotb, twoH, lane4;
+    uint32_t neg_lo, wmax, X, hotb, lane4;
     __device__ void params(const DevTables& t) {
         neg_lo = 0u - t.lo;
         wmax = t.W - 1;
         X = t.dwin_X;
         hotb = t.dwin_hotb;
-        twoH = 2u * t.dwin_H;
         lane4 = 4u * lane_id();
     }
     __device__ __forceinline__ uint32_t step(uint32_t st, uint32_t byte) const {
         return ld_tbl_u16(window_col(byte, neg_lo, wmax) * X + st);
     }
-    __device__ __forceinline__ uint32_t fix(uint32_t st) const { return mix_fix(st, hotb, twoH, lane4); }
+    __device__ __forceinline__ uint32_t fix(uint32_t st) const { return mix_fix(st, hotb, lane4); }
 };
 
 // Steps that re-normalise their state between 16-byte pieces (StepDfaMix)

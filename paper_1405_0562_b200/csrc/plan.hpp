@@ -107,30 +107,34 @@ __host__ __device__ __forceinline__ uint32_t dec8(uint32_t e) { return e; }
 __host__ __device__ __forceinline__ uint32_t col8(uint32_t j) { return ((j >> 2) << 7) | (j & 3u); }
 __host__ __device__ __forceinline__ uint32_t dfa8_RB(uint32_t W) { return 128u * ((W + 3) / 4); }
 // The MIXED u16 layout (|D| too large for 32 u16 copies): DFA states ranked by
-// visit frequency; ranks r < H (even) are "hot" and every rank has a "twin".
+// visit frequency; ranks r < H (even) are "hot" and every rank has a "twin",
+// a lane-independent cell any lane may run in.
 // Column j occupies [j*X, (j+1)*X), X = hotb + 128 * ceil(nD / 64):
 //   hot  (r, lane L): j*X + mix_hot(r, L),  mix_hot(r, L) = (r >> 1) * 128 + 4L + 2 (r & 1)
 //                     (32 bank-private copies: lane L only touches bank L; hotb = 64 H)
-//   twin (r):         j*X + mix_twin(r),    mix_twin(r) = hotb + 2r  (one copy shared by all lanes)
-// A hot cell holds the next state as mix_hot (lane L's own copy) if it is hot,
-// else as mix_twin; a twin cell always holds mix_twin (lane-independent).  Both
-// encodings are complete tables, so any mix of them runs the DFA exactly; a
-// lane in the twin copy is moved back to its private copy every 16 bytes
-// (StepDfaMix::fix) -- only the bank conflicts depend on where it runs.
+//   twin (r):         j*X + mix_twin(r):    a hot state's twin is lane 31's private cell,
+//                     mix_hot(r, 31) -- lane 31's copy doubles as the shared copy -- and a
+//                     cold state's (r >= H) the u16 at hotb + 2r (one copy for all lanes)
+// A hot cell of lane L holds the next state as mix_hot(., L) if it is hot, else
+// as its twin; lane 31's cells and the cold cells therefore hold twins only
+// (lane-independent).  Every encoding addresses a complete table, so any mix of
+// them runs the DFA exactly; a lane running in lane 31's copy is moved back to
+// its own every 16 bytes (StepDfaMix::fix: the lane field of the address, one
+// LOP3 + compare + select) -- only the bank conflicts depend on where it runs.
 __host__ __device__ __forceinline__ uint32_t mix_hot(uint32_t r, uint32_t lane) {
     return (r >> 1) * 128u + 4u * lane + 2u * (r & 1u);
 }
-__host__ __device__ __forceinline__ uint32_t mix_twin(uint32_t r, uint32_t hotb) { return hotb + 2u * r; }
+__host__ __device__ __forceinline__ uint32_t mix_twin(uint32_t r, uint32_t hotb, uint32_t H) {
+    return r < H ? mix_hot(r, 31u) : hotb + 2u * r;
+}
 __host__ __device__ __forceinline__ uint32_t mix_X(uint32_t nD, uint32_t H) { return 64u * H + 128u * ((nD + 63) / 64); }
 __host__ __device__ __forceinline__ uint32_t mix_rank_of(uint32_t e, uint32_t hotb) {
     return e < hotb ? 2u * (e >> 7) + ((e >> 1) & 1u) : (e - hotb) >> 1;
 }
-// StepDfaMix::fix: the twin of a hot state (rank r < H) -> its private cell of
-// lane L (lane4 = 4L); any other encoding unchanged
-__host__ __device__ __forceinline__ uint32_t mix_fix(uint32_t e, uint32_t hotb, uint32_t twoH, uint32_t lane4) {
-    const uint32_t d = e - hotb;  // 2r for a twin (wraps for a hot state)
-    const uint32_t h = ((d & ~3u) << 5) + (d & 2u) + lane4;  // mix_hot(d / 2, lane)
-    return d < twoH ? h : e;
+// StepDfaMix::fix: a hot state's cell in any lane's copy (its twin included)
+// -> the cell of lane L (lane4 = 4L); a cold state's twin unchanged
+__host__ __device__ __forceinline__ uint32_t mix_fix(uint32_t e, uint32_t hotb, uint32_t lane4) {
+    return e < hotb ? ((e & ~124u) | lane4) : e;
 }
 // The compact source of a bank-private window (DevTables::dwin_cpt): a pair
 // word of lane 0's cells with bit 15 set on private targets -> lane L's word
@@ -145,7 +149,7 @@ __device__ __forceinline__ uint32_t dw_enc(const DevTables& t, uint32_t q, uint3
     if (t.dwin_u8) return enc8(q, lane);
     if (t.dwin_H) {
         const uint32_t r = t.dwin_rank[q];
-        return r < t.dwin_H ? mix_hot(r, lane) : mix_twin(r, t.dwin_hotb);
+        return r < t.dwin_H ? mix_hot(r, lane) : mix_twin(r, t.dwin_hotb, t.dwin_H);
     }
     return dfa_enc(q, lane % t.dwin_R, t.dwin_R);
 }

@@ -143,17 +143,21 @@ int main() {
                     if ((e >> 2) % 32 != L) { printf("hot %u,%u not in bank %u\n", r, L, L); return 0; }
                     if (!seen.insert(e).second) { printf("hot %u,%u shares a cell\n", r, L); return 0; }
                     if (sfa::mix_rank_of(e, hotb) != r) { printf("rank of hot %u,%u\n", r, L); return 0; }
-                    if (sfa::mix_fix(e, hotb, 2 * H, 4 * L) != e) { printf("fix moved hot %u,%u\n", r, L); return 0; }
+                    if (sfa::mix_fix(e, hotb, 4 * L) != e) { printf("fix moved hot %u,%u\n", r, L); return 0; }
                     for (unsigned j = 1; j < 4; ++j)  // other columns keep the bank
                         if (((j * X + e) >> 2) % 32 != L) { printf("column %u moves bank\n", j); return 0; }
                 }
             for (unsigned r = 0; r < nD; ++r) {
-                const unsigned t = sfa::mix_twin(r, hotb);
-                if (t < hotb || t + 2 > X) { printf("twin %u outside the twin region\n", r); return 0; }
-                if (!seen.insert(t).second) { printf("twin %u shares a cell\n", r); return 0; }
+                const unsigned t = sfa::mix_twin(r, hotb, H);
+                if (r < H) {  // a hot state's twin is lane 31's private cell
+                    if (t != sfa::mix_hot(r, 31)) { printf("twin of hot %u is not lane 31's cell\n", r); return 0; }
+                } else {
+                    if (t < hotb || t + 2 > X) { printf("twin %u outside the twin region\n", r); return 0; }
+                    if (!seen.insert(t).second) { printf("twin %u shares a cell\n", r); return 0; }
+                }
                 if (sfa::mix_rank_of(t, hotb) != r) { printf("rank of twin %u\n", r); return 0; }
                 for (unsigned L = 0; L < 32; L += 7) {
-                    const unsigned f = sfa::mix_fix(t, hotb, 2 * H, 4 * L);
+                    const unsigned f = sfa::mix_fix(t, hotb, 4 * L);
                     if (f != (r < H ? sfa::mix_hot(r, L) : t)) { printf("fix of twin %u lane %u\n", r, L); return 0; }
                 }
             }
@@ -161,9 +165,9 @@ int main() {
             for (unsigned a = 0; a < nD; a += 3)
                 for (unsigned b = 0; b < nD; b += 5) {
                     auto cell = [&](unsigned q) {
-                        return q < H ? sfa::cpt_cell(sfa::mix_hot(q, 0), true) : sfa::cpt_cell(sfa::mix_twin(q, hotb), false);
+                        return q < H ? sfa::cpt_cell(sfa::mix_hot(q, 0), true) : sfa::cpt_cell(sfa::mix_twin(q, hotb, H), false);
                     };
-                    auto enc = [&](unsigned q, unsigned L) { return q < H ? sfa::mix_hot(q, L) : sfa::mix_twin(q, hotb); };
+                    auto enc = [&](unsigned q, unsigned L) { return q < H ? sfa::mix_hot(q, L) : sfa::mix_twin(q, hotb, H); };
                     for (unsigned L = 0; L < 32; ++L)
                         if (sfa::cpt_expand(cell(a) | (cell(b) << 16), L) != (enc(a, L) | (enc(b, L) << 16))) {
                             printf("compact expansion %u %u lane %u\n", a, b, L);
@@ -179,8 +183,9 @@ int main() {
 def test_mixed_window_encoding(tmp_path):
     """MIXED DFA window (plan.hpp): lane L's private cells of the hot states
     all sit in bank L in every column, no two cells of the layout coincide,
-    ranks decode from both encodings, the 16-byte fix sends exactly the twins
-    of hot states back to the lane's own cell, and the compact source
+    ranks decode from both encodings, a hot state's twin is lane 31's private
+    cell, the 16-byte fix sends exactly the twins of hot states to the lane's
+    own cell, and the compact source
     (bit 15 = private target) expands to every lane's pair word."""
     src = tmp_path / "mix.cpp"
     src.write_text(MIX_SRC)
