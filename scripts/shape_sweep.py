@@ -46,6 +46,11 @@ if os.environ.get("SWEEP") == "k2":      # two rows per thread (ILP 2) with 32-b
 if os.environ.get("SWEEP") == "k2promo":  # two chains per thread on 16-byte stages, L2 promotion for whole lines
     shapes = [dict(), dict(tma_k=2, tma_rowb=16, tma_promo=128), dict(tma_k=2, tma_rowb=16, tma_promo=256),
               dict(tma_k=2, tma_rowb=16, tma_promo=128, hot_rows=16), dict(tma_k=2, tma_rowb=16, tma_promo=256, hot_rows=16)]
+if os.environ.get("SWEEP") == "hot2":    # cfg2 through HOT + FACTORED (an 8 KB DFA window): room for two rows per thread
+    H = P.RES_HOT_L2
+    shapes = [dict(), dict(_res=H), dict(_res=H, tma_k=2, tma_rowb=32, tma_ring=3), dict(_res=H, tma_k=2, tma_rowb=32),
+              dict(_res=H, tma_k=2, tma_rowb=16), dict(_res=H, tma_k=1, tma_rowb=32, tma_ring=6),
+              dict(_res=H, tma_k=1, tma_rowb=64, tma_ring=3), dict(_res=H, tma_k=2, tma_rowb=64, tma_ring=2)]
 s = torch.cuda.Stream()
 for cfg in cfgs:
     rx, alpha, text = bench.workload(cfg)
@@ -63,7 +68,13 @@ for cfg in cfgs:
     for sh in shapes:
         sfa = P.SFA(rx, alpha)
         try:
-            sfa.set_tuning(**sh)
+            sh = dict(sh)
+            res_mode = sh.pop("_res", None)
+            if sh:
+                sfa.set_tuning(**sh)
+            if res_mode is not None:
+                sfa.set_residency(res_mode)
+                sh["_res"] = res_mode
             fn = (lambda: sfa.match_batch(dt, do, off.size - 1, res, s)) if cfg == 5 else (lambda: sfa.match_async(dt, res, s))
             ms, med = bench.steady(torch, fn, s, 30, 5)
             one = bench.single(torch, fn, s, 10)
