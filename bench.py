@@ -219,6 +219,16 @@ def smem_peaks(nsm, sm_mhz):
     return nsm * 32 * hz / 1e9, nsm * (1.0 / (1 / 32 + 2 / 128)) * hz / 1e9
 
 
+def pattern_ceiling():
+    """GB/s of the scan's TMA access pattern without lookups (the committed microbenchmark output)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2d_mb_tma.txt")) as f:
+            first = f.readline()
+        return float(first.split(":")[1].split("GB/s")[0])
+    except Exception:
+        return None
+
+
 def roofline(gbs, peak, peak_kind, nsm, sm_mhz, kernel, traffic, per_launch_bytes, key=None):
     lk, dp = smem_peaks(nsm, sm_mhz)
     extra = {}
@@ -230,6 +240,12 @@ def roofline(gbs, peak, peak_kind, nsm, sm_mhz, kernel, traffic, per_launch_byte
         extra = {"smem_ld_ceiling_gbs": ceil, "frac_of_smem_ld_ceiling": gbs / ceil,
                  "smem_conflicts_per_wavefront": e.get("smem_bank_conflicts_ld", 0) / e["smem_wavefronts_ld"],
                  "smem_ld_ceiling_source": "profiles/ncu_summary.json wavefronts of the same kernel"}
+    pat = pattern_ceiling()
+    if pat:
+        extra.update({"access_pattern_ceiling_gbs": pat, "frac_of_access_pattern_ceiling": gbs / pat,
+                      "access_pattern_ceiling_source": "profiles/r2d_mb_tma.txt line 1 (scripts/mb_tma.cu: k_scan_tma's "
+                                                       "TMA pattern on 1 GiB with the lookups removed; context, "
+                                                       "measured in another session)"})
     return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, **extra,
             "traffic": traffic, "traffic_source": "profiles/ncu_summary.json (ncu --set full of the same kernel)",
             "algorithmic_bytes_per_launch": per_launch_bytes,
