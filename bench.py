@@ -243,7 +243,7 @@ def roofline(gbs, peak, peak_kind, nsm, sm_mhz, kernel, traffic, per_launch_byte
     pat = pattern_ceiling()
     if pat:
         extra.update({"access_pattern_ceiling_gbs": pat, "frac_of_access_pattern_ceiling": gbs / pat,
-                      "access_pattern_ceiling_source": "profiles/r2d_mb_tma.txt line 1 (scripts/mb_tma.cu: k_scan_tma's "
+                      "access_pattern_ceiling_source": "profiles/r2d_mb_tma.txt line 1 (6-deep ring; 5.5-5.6 TB/s at 3-4 deep, r2d_mb_tma_ring.txt) (scripts/mb_tma.cu: k_scan_tma's "
                                                        "TMA pattern on 1 GiB with the lookups removed; context, "
                                                        "measured in another session)"})
     return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, **extra,

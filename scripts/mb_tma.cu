@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t c) {
@@ -224,6 +225,12 @@ int main(int argc, char** argv) {
     cudaMemset(d, 1, n);
     uint32_t* out;
     cudaMalloc(&out, 4);
+    if (argc > 2 && !strcmp(argv[2], "ring")) {  // the product's pattern per ring depth
+        for (int ring : {2, 3, 4, 5, 6, 7}) run<32>(enc, d, n, 1, ring, 0, out);
+        for (int ring : {2, 3}) run<64>(enc, d, n, 1, ring, 0, out);
+        for (int ring : {4, 6, 8}) run<16>(enc, d, n, 1, ring, 0, out);  // (the barrier block holds 8 slots)
+        return 0;
+    }
     for (int promo : {0, 256}) {
         run<32>(enc, d, n, 1, 6, promo, out);
         run<64>(enc, d, n, 1, 3, promo, out);
